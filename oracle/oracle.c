@@ -1,0 +1,648 @@
+/*
+ * oracle/oracle.c — PLAIN, SLOW, CPU-ONLY ORACLE.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load this library.  It shares no code, header, table or
+ * helper with the CUDA path (paper_1207_1773_b200/csrc); neither includes the
+ * other.  Everything is complex binary64 (C99 `double complex`), column-major,
+ * written loop by loop in the order the paper (and the textbook algorithm it
+ * names) states, with no blocking, fusion or reordering.
+ *
+ * Paper = /root/reference/PAPER.md (arXiv 1207.1773, "A hybrid Hermitian
+ * general eigenvalue solver").  "P:Lnn" = PAPER.md line nn.
+ *
+ * Method (Algorithm 1, with Algorithm 2):
+ *   1  B = L L^H                              orc_potrf
+ *   2  A' = L^-1 A L^-H  (explicit solves)    orc_std_form
+ *   3  A' y = lambda y:
+ *        one-stage reduction T = Q^H A' Q     orc_hetd2        (n=1 stage)
+ *        tridiagonal eigensolver T y' = l y'  orc_tql2 / orc_sturm_values
+ *        y = Q y'                             orc_apply_hetd2_q
+ *   4  x = L^-H y                             orc_backsub_lh
+ *   orc_solve_gen composes them.
+ *
+ * Stage-level references for the two-stage GPU path:
+ *   orc_larfg        LAPACK zlarfg convention (reading R1)
+ *   orc_he2hb        reduction to band, one reflector at a time, two-sided
+ *                    (Fig. 1 caption P:L97), reading R3/R6
+ *   orc_larft        T factor of a block of reflectors (forward, columnwise)
+ *   orc_hb2st        column-wise bulge chase on a dense copy, reading R5
+ *   orc_apply_q1     E <- Q1 E, one reflector at a time
+ *   orc_apply_q2     E <- Q2 E, one reflector at a time
+ *   orc_jacobi       cyclic complex Jacobi (independent second path, n <= 512)
+ *
+ * Pins (tests/test_oracle_pins.py) check these against closed forms, brute
+ * force, invariants and a library routine; see DESIGN.md "Oracle pins".
+ */
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef double complex zc;
+#define IX(i, j, ld) ((size_t)(i) + (size_t)(j) * (size_t)(ld))
+
+static double sq(double x) { return x * x; }
+static double abs2(zc z) { return creal(z) * creal(z) + cimag(z) * cimag(z); }
+
+/* ------------------------------------------------------------------------- */
+/* Householder generator, LAPACK zlarfg convention (reading R1).
+ * Given alpha and x[0..m-2] (the vector (alpha, x) of length m), computes
+ * beta (real), tau and v = (1, x/(alpha-beta)) such that
+ *   H^H (alpha; x) = (beta; 0),  H = I - tau v v^H.
+ * x is overwritten with v[1..m-1]; returns beta in *beta, tau in *tau.
+ * tau = 0 (H = I) iff x == 0 and Im(alpha) == 0. */
+void orc_larfg(int64_t m, zc *alpha, zc *x, int64_t incx, zc *tau) {
+  if (m <= 0) { *tau = 0; return; }
+  double xnorm2 = 0;
+  for (int64_t i = 0; i < m - 1; i++) xnorm2 += abs2(x[i * incx]);
+  double xnorm = sqrt(xnorm2);
+  double ar = creal(*alpha), ai = cimag(*alpha);
+  if (xnorm == 0.0 && ai == 0.0) { *tau = 0; return; }
+  double beta = -copysign(sqrt(ar * ar + ai * ai + xnorm * xnorm), ar);
+  const double safmin = 2.2250738585072014e-308 / 1.1102230246251565e-16;
+  double rsafmn = 1.0 / safmin, scale = 1.0;
+  int knt = 0;
+  if (fabs(beta) < safmin) {
+    /* rescale until beta is representable (LAPACK loop) */
+    do {
+      knt++;
+      for (int64_t i = 0; i < m - 1; i++) x[i * incx] *= rsafmn;
+      beta *= rsafmn; ar *= rsafmn; ai *= rsafmn; scale *= rsafmn;
+    } while (fabs(beta) < safmin && knt < 20);
+    xnorm2 = 0;
+    for (int64_t i = 0; i < m - 1; i++) xnorm2 += abs2(x[i * incx]);
+    xnorm = sqrt(xnorm2);
+    beta = -copysign(sqrt(ar * ar + ai * ai + xnorm * xnorm), ar);
+  }
+  *tau = CMPLX((beta - ar) / beta, -ai / beta);
+  zc denom = CMPLX(ar - beta, ai);
+  zc s = 1.0 / denom;
+  for (int64_t i = 0; i < m - 1; i++) x[i * incx] *= s;
+  for (int k = 0; k < knt; k++) beta *= safmin;
+  *alpha = beta;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Algorithm 1 step 1: Cholesky B = L L^H, unblocked Cholesky-Crout on
+ * the lower triangle.  Returns 0, or n + j + 1 if the leading minor of order
+ * j+1 is not positive definite (LAPACK zhegv INFO convention, reading R11).
+ * On exit the lower triangle of B holds L; the strict upper triangle is set
+ * to 0. */
+int64_t orc_potrf(int64_t n, zc *B, int64_t ldb) {
+  for (int64_t j = 0; j < n; j++) {
+    double d = creal(B[IX(j, j, ldb)]);
+    for (int64_t k = 0; k < j; k++) d -= abs2(B[IX(j, k, ldb)]);
+    if (!(d > 0.0) || !isfinite(d)) return n + j + 1;
+    double ljj = sqrt(d);
+    B[IX(j, j, ldb)] = ljj;
+    for (int64_t i = j + 1; i < n; i++) {
+      zc s = B[IX(i, j, ldb)];
+      for (int64_t k = 0; k < j; k++) s -= B[IX(i, k, ldb)] * conj(B[IX(j, k, ldb)]);
+      B[IX(i, j, ldb)] = s / ljj;
+    }
+  }
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < j; i++) B[IX(i, j, ldb)] = 0;
+  return 0;
+}
+
+/* Forward substitution: X <- L^-1 X (L lower, non-unit), X is n x m. */
+static void trsm_lower(int64_t n, int64_t m, const zc *L, int64_t ldl, zc *X, int64_t ldx) {
+  for (int64_t c = 0; c < m; c++)
+    for (int64_t i = 0; i < n; i++) {
+      zc s = X[IX(i, c, ldx)];
+      for (int64_t k = 0; k < i; k++) s -= L[IX(i, k, ldl)] * X[IX(k, c, ldx)];
+      X[IX(i, c, ldx)] = s / L[IX(i, i, ldl)];
+    }
+}
+
+/* Algorithm 1 step 4: X <- L^-H X, back substitution with L^H
+ * (upper, non-unit).  X is n x m. */
+void orc_backsub_lh(int64_t n, int64_t m, const zc *L, int64_t ldl, zc *X, int64_t ldx) {
+  for (int64_t c = 0; c < m; c++)
+    for (int64_t i = n - 1; i >= 0; i--) {
+      zc s = X[IX(i, c, ldx)];
+      for (int64_t k = i + 1; k < n; k++) s -= conj(L[IX(k, i, ldl)]) * X[IX(k, c, ldx)];
+      X[IX(i, c, ldx)] = s / conj(L[IX(i, i, ldl)]);
+    }
+}
+
+/* Algorithm 1 step 2: C = L^-1 A L^-H computed explicitly by dense
+ * solves (reading R2): form full Hermitian A from its lower triangle with
+ * real diagonal; X = L^-1 A; C = (L^-1 X^H)^H; symmetrise C = (C + C^H)/2.
+ * A is read (lower), C (n x n, ldc) is written in full. */
+void orc_std_form(int64_t n, const zc *A, int64_t lda, const zc *L, int64_t ldl, zc *C, int64_t ldc) {
+  zc *X = (zc *)malloc(sizeof(zc) * n * n);
+  zc *Y = (zc *)malloc(sizeof(zc) * n * n);
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) {
+      zc a = (i > j) ? A[IX(i, j, lda)] : (i < j ? conj(A[IX(j, i, lda)]) : creal(A[IX(i, i, lda)]));
+      X[IX(i, j, n)] = a;
+    }
+  trsm_lower(n, n, L, ldl, X, n);                          /* X = L^-1 A      */
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) Y[IX(i, j, n)] = conj(X[IX(j, i, n)]);   /* Y = X^H */
+  trsm_lower(n, n, L, ldl, Y, n);                          /* Y = L^-1 X^H    */
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) X[IX(i, j, n)] = conj(Y[IX(j, i, n)]);   /* X = Y^H = L^-1 A L^-H */
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) {
+      zc c = 0.5 * (X[IX(i, j, n)] + conj(X[IX(j, i, n)]));
+      if (i == j) c = creal(c);
+      C[IX(i, j, ldc)] = c;
+    }
+  free(X); free(Y);
+}
+
+/* Two-sided application of one reflector H = I - tau v v^H to the full
+ * Hermitian matrix M (order s, ld): M <- H^H M H, written the textbook way
+ * (LAPACK zhetd2 step): p = tau M v; w = p - 1/2 tau (p^H v) v;
+ * M <- M - v w^H - w v^H.  v[0..s-1] explicit (v[0] = 1).  Both triangles
+ * of M are kept. */
+static void herm_reflect(int64_t s, zc *M, int64_t ld, const zc *v, zc tau) {
+  if (tau == 0) return;
+  zc *p = (zc *)malloc(sizeof(zc) * s);
+  for (int64_t i = 0; i < s; i++) {
+    zc acc = 0;
+    for (int64_t k = 0; k < s; k++) acc += M[IX(i, k, ld)] * v[k];
+    p[i] = tau * acc;
+  }
+  zc phv = 0;
+  for (int64_t k = 0; k < s; k++) phv += conj(p[k]) * v[k];
+  zc alpha = -0.5 * tau * phv;
+  for (int64_t k = 0; k < s; k++) p[k] += alpha * v[k];      /* p := w */
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < s; j++)
+    for (int64_t i = 0; i < s; i++)
+      M[IX(i, j, ld)] -= v[i] * conj(p[j]) + p[i] * conj(v[j]);
+  for (int64_t i = 0; i < s; i++) M[IX(i, i, ld)] = creal(M[IX(i, i, ld)]);
+  free(p);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Algorithm 2 step 1 with one stage: Householder
+ * tridiagonalisation of the full Hermitian C (lower reflectors, zhetd2
+ * form).  For k = 0..n-2: (beta, tau_k, v_k) = larfg(C[k+1,k], C[k+2:,k]),
+ * e_k = beta, C[k+1:,k+1:] <- H_k^H C[k+1:,k+1:] H_k.  d_k = Re C[k,k].
+ * On exit v_k (without its unit head) is stored in C[k+2:, k].  With
+ * Q = H_0 H_1 ... H_{n-2}: T = Q^H C Q. */
+void orc_hetd2(int64_t n, zc *C, int64_t ldc, double *d, double *e, zc *tau) {
+  zc *v = (zc *)malloc(sizeof(zc) * (n > 0 ? n : 1));
+  for (int64_t k = 0; k + 1 < n; k++) {
+    zc alpha = C[IX(k + 1, k, ldc)];
+    zc t;
+    orc_larfg(n - k - 1, &alpha, &C[IX(k + 2, k, ldc)], 1, &t);
+    e[k] = creal(alpha);
+    tau[k] = t;
+    int64_t s = n - k - 1;
+    v[0] = 1;
+    for (int64_t i = 1; i < s; i++) v[i] = C[IX(k + 1 + i, k, ldc)];
+    herm_reflect(s, &C[IX(k + 1, k + 1, ldc)], ldc, v, t);
+    C[IX(k + 1, k, ldc)] = alpha;
+    C[IX(k, k + 1, ldc)] = alpha;
+  }
+  for (int64_t k = 0; k < n; k++) d[k] = creal(C[IX(k, k, ldc)]);
+  if (n >= 1) tau[n - 1 > 0 ? n - 1 : 0] = 0;
+  free(v);
+}
+
+/* Algorithm 2 step 3 for the one-stage reduction: Y <- Q Y,
+ * Q = H_0 ... H_{n-2}; applied right to left (H_{n-2} first).  Y is n x m. */
+void orc_apply_hetd2_q(int64_t n, int64_t m, const zc *C, int64_t ldc, const zc *tau, zc *Y, int64_t ldy) {
+  for (int64_t k = n - 2; k >= 0; k--) {
+    zc t = tau[k];
+    if (t == 0) continue;
+    int64_t r0 = k + 1, s = n - r0;
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < m; c++) {
+      zc w = Y[IX(r0, c, ldy)];                              /* v^H y, v[0] = 1 */
+      for (int64_t i = 1; i < s; i++) w += conj(C[IX(r0 + i, k, ldc)]) * Y[IX(r0 + i, c, ldy)];
+      w *= t;
+      Y[IX(r0, c, ldy)] -= w;
+      for (int64_t i = 1; i < s; i++) Y[IX(r0 + i, c, ldy)] -= C[IX(r0 + i, k, ldc)] * w;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Algorithm 2 step 2: symmetric tridiagonal QL with implicit shifts
+ * (EISPACK tql2), eigenvectors accumulated into Z (n x n real, ldz; pass the
+ * identity to get the eigenvectors of T).  d[0..n-1] diagonal,
+ * e[0..n-2] sub-diagonal (e is destroyed; needs n entries).  Eigenvalues
+ * sorted ascending with their vectors.  Returns 0 or l+1 if eigenvalue l
+ * needed more than 30 iterations. */
+int64_t orc_tql2(int64_t n, double *d, double *e, double *Z, int64_t ldz) {
+  if (n <= 1) return 0;
+  e[n - 1] = 0.0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = 2.220446049250313e-16;
+  for (int64_t l = 0; l < n; l++) {
+    int iter = 0;
+    tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
+    int64_t m = l;
+    while (m < n) {
+      if (fabs(e[m]) <= eps * tst1) break;
+      m++;
+    }
+    if (m >= n) m = n - 1;
+    if (m > l) {
+      do {
+        if (++iter > 30) return l + 1;
+        double g = d[l];
+        double p = (d[l + 1] - g) / (2.0 * e[l]);
+        double r = hypot(p, 1.0);
+        if (p < 0) r = -r;
+        d[l] = e[l] / (p + r);
+        d[l + 1] = e[l] * (p + r);
+        double dl1 = d[l + 1];
+        double h = g - d[l];
+        for (int64_t i = l + 2; i < n; i++) d[i] -= h;
+        f += h;
+        p = d[m];
+        double c = 1.0, c2 = 1.0, c3 = 1.0, el1 = e[l + 1], s = 0.0, s2 = 0.0;
+        for (int64_t i = m - 1; i >= l; i--) {
+          c3 = c2; c2 = c; s2 = s;
+          g = c * e[i];
+          h = c * p;
+          r = hypot(p, e[i]);
+          e[i + 1] = s * r;
+          s = e[i] / r;
+          c = p / r;
+          p = c * d[i] - s * g;
+          d[i + 1] = h + s * (c * g + s * d[i]);
+          double *zi = &Z[IX(0, i, ldz)], *zi1 = &Z[IX(0, i + 1, ldz)];
+          for (int64_t k = 0; k < n; k++) {
+            h = zi1[k];
+            zi1[k] = s * zi[k] + c * h;
+            zi[k] = c * zi[k] - s * h;
+          }
+        }
+        p = -s * s2 * c3 * el1 * e[l] / dl1;
+        e[l] = s * p;
+        d[l] = c * p;
+      } while (fabs(e[l]) > eps * tst1);
+    }
+    d[l] = d[l] + f;
+    e[l] = 0.0;
+  }
+  /* sort ascending (selection sort, stable index tie-break) */
+  for (int64_t i = 0; i < n - 1; i++) {
+    int64_t k = i;
+    double p = d[i];
+    for (int64_t j = i + 1; j < n; j++)
+      if (d[j] < p) { k = j; p = d[j]; }
+    if (k != i) {
+      d[k] = d[i];
+      d[i] = p;
+      for (int64_t r = 0; r < n; r++) {
+        double t = Z[IX(r, i, ldz)];
+        Z[IX(r, i, ldz)] = Z[IX(r, k, ldz)];
+        Z[IX(r, k, ldz)] = t;
+      }
+    }
+  }
+  return 0;
+}
+
+/* Number of eigenvalues of the symmetric tridiagonal (d, e) that are < x
+ * (Sturm sequence count). */
+static int64_t sturm_count(int64_t n, const double *d, const double *e, double x) {
+  int64_t cnt = 0;
+  double q = d[0] - x;
+  if (q < 0) cnt++;
+  for (int64_t i = 1; i < n; i++) {
+    if (q == 0.0) q = 1e-300;
+    q = d[i] - x - e[i - 1] * e[i - 1] / q;
+    if (q < 0) cnt++;
+  }
+  return cnt;
+}
+
+/* Eigenvalues il..iu (1-based, ascending) of the tridiagonal (d, e) by
+ * Sturm-count bisection on the Gershgorin interval, to full precision.
+ * An independent values-only path (reading R8). */
+void orc_sturm_values(int64_t n, const double *d, const double *e, int64_t il, int64_t iu, double *w) {
+  double lo = d[0], hi = d[0];
+  for (int64_t i = 0; i < n; i++) {
+    double r = (i > 0 ? fabs(e[i - 1]) : 0) + (i + 1 < n ? fabs(e[i]) : 0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+  }
+  double span = fmax(fabs(lo), fabs(hi));
+  lo -= 1e-14 * span + 1e-300;
+  hi += 1e-14 * span + 1e-300;
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t k = il; k <= iu; k++) {
+    double a = lo, b = hi;
+    for (int it = 0; it < 200; it++) {
+      double mid = 0.5 * (a + b);
+      if (mid <= a || mid >= b) break;
+      if (sturm_count(n, d, e, mid) >= k) b = mid; else a = mid;
+    }
+    w[k - il] = 0.5 * (a + b);
+  }
+}
+
+/* Cyclic complex Jacobi on a full Hermitian matrix (n <= 512): independent
+ * second path for the standard eigenproblem (reading R8).  A (n x n, lda) is
+ * destroyed; w receives eigenvalues ascending, V (n x n, ldv) the
+ * eigenvectors.  Returns the number of sweeps used (or -1 if not converged). */
+int64_t orc_jacobi(int64_t n, zc *A, int64_t lda, double *w, zc *V, int64_t ldv) {
+  for (int64_t j = 0; j < n; j++)
+    for (int64_t i = 0; i < n; i++) V[IX(i, j, ldv)] = (i == j) ? 1.0 : 0.0;
+  for (int64_t i = 0; i < n; i++) A[IX(i, i, lda)] = creal(A[IX(i, i, lda)]);
+  int64_t sweep;
+  for (sweep = 1; sweep <= 60; sweep++) {
+    double off = 0, tot = 0;
+    for (int64_t j = 0; j < n; j++)
+      for (int64_t i = 0; i < n; i++) {
+        double a = abs2(A[IX(i, j, lda)]);
+        tot += a;
+        if (i != j) off += a;
+      }
+    if (off <= 1e-32 * tot || off == 0.0) break;
+    for (int64_t p = 0; p < n - 1; p++)
+      for (int64_t q = p + 1; q < n; q++) {
+        zc apq = A[IX(p, q, lda)];
+        double mag = cabs(apq);
+        if (mag == 0.0) continue;
+        zc ph = apq / mag;                           /* e^{i phi} */
+        double app = creal(A[IX(p, p, lda)]), aqq = creal(A[IX(q, q, lda)]);
+        double theta = (aqq - app) / (2.0 * mag);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+        double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+        /* U = diag(1, conj(ph)) * [[c, s], [-s, c]]:
+           U_pp = c, U_pq = s, U_qp = -s conj(ph), U_qq = c conj(ph).  A <- U^H A U, V <- V U */
+        zc upp = c, upq = s, uqp = -s * conj(ph), uqq = c * conj(ph);
+        for (int64_t k = 0; k < n; k++) {            /* columns: A U */
+          zc akp = A[IX(k, p, lda)], akq = A[IX(k, q, lda)];
+          A[IX(k, p, lda)] = akp * upp + akq * uqp;
+          A[IX(k, q, lda)] = akp * upq + akq * uqq;
+          zc vkp = V[IX(k, p, ldv)], vkq = V[IX(k, q, ldv)];
+          V[IX(k, p, ldv)] = vkp * upp + vkq * uqp;
+          V[IX(k, q, ldv)] = vkp * upq + vkq * uqq;
+        }
+        for (int64_t k = 0; k < n; k++) {            /* rows: U^H (A U) */
+          zc apk = A[IX(p, k, lda)], aqk = A[IX(q, k, lda)];
+          A[IX(p, k, lda)] = conj(upp) * apk + conj(uqp) * aqk;
+          A[IX(q, k, lda)] = conj(upq) * apk + conj(uqq) * aqk;
+        }
+        A[IX(p, q, lda)] = 0;
+        A[IX(q, p, lda)] = 0;
+        A[IX(p, p, lda)] = creal(A[IX(p, p, lda)]);
+        A[IX(q, q, lda)] = creal(A[IX(q, q, lda)]);
+      }
+  }
+  for (int64_t i = 0; i < n; i++) w[i] = creal(A[IX(i, i, lda)]);
+  for (int64_t i = 0; i < n - 1; i++) {              /* sort ascending */
+    int64_t k = i;
+    for (int64_t j = i + 1; j < n; j++) if (w[j] < w[k]) k = j;
+    if (k != i) {
+      double t = w[i]; w[i] = w[k]; w[k] = t;
+      for (int64_t r = 0; r < n; r++) {
+        zc z = V[IX(r, i, ldv)]; V[IX(r, i, ldv)] = V[IX(r, k, ldv)]; V[IX(r, k, ldv)] = z;
+      }
+    }
+  }
+  return sweep > 60 ? -1 : sweep;
+}
+
+/* ------------------------------------------------------------------------- */
+/* The generalized solver, Algorithm 1 with the one-stage Algorithm 2
+ * (P:L66-L69): potrf -> explicit std form -> hetd2 -> tql2 ->
+ * select il..iu -> y = Q y' -> x = L^-H y.
+ * A, B: n x n, lower triangles read; B is overwritten by L.  w[n] receives
+ * all eigenvalues ascending; Z (n x m, ldz), m = iu - il + 1, the selected
+ * eigenvectors.  times[4] (nullable) receives seconds per step measured by
+ * the caller-provided clock (unused here; the Python wrapper times steps).
+ * Returns 0, n+j (B not PD), or the tql2 failure index. */
+int64_t orc_solve_gen(int64_t n, const zc *A, int64_t lda, zc *B, int64_t ldb, int64_t il, int64_t iu,
+                      double *w, zc *Z, int64_t ldz) {
+  int64_t info = orc_potrf(n, B, ldb);
+  if (info) return info;
+  zc *C = (zc *)malloc(sizeof(zc) * n * n);
+  zc *tau = (zc *)malloc(sizeof(zc) * n);
+  double *e = (double *)malloc(sizeof(double) * n);
+  double *Y = (double *)calloc((size_t)n * n, sizeof(double));
+  orc_std_form(n, A, lda, B, ldb, C, n);
+  orc_hetd2(n, C, n, w, e, tau);
+  for (int64_t i = 0; i < n; i++) Y[IX(i, i, n)] = 1.0;
+  info = orc_tql2(n, w, e, Y, n);
+  if (!info) {
+    int64_t m = iu - il + 1;
+    for (int64_t c = 0; c < m; c++)
+      for (int64_t r = 0; r < n; r++) Z[IX(r, c, ldz)] = Y[IX(r, il - 1 + c, n)];
+    orc_apply_hetd2_q(n, m, C, n, tau, Z, ldz);
+    orc_backsub_lh(n, m, B, ldb, Z, ldz);
+  }
+  free(C); free(tau); free(e); free(Y);
+  return info;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Reduction to band (two-stage step 1, Fig. 1), plain:
+ * panels at column i = k*nb, k = 0..K-1, K = #{i : i + nb < n} (reading R3).
+ * For each panel column c = i + j (j = 0..min(nb, n-i-nb)-1):
+ *   (beta, tau, v) = larfg(A[r0, c], A[r0+1:, c]) with r0 = i + nb + j;
+ *   the remaining panel columns c+1..i+nb-1 get H^H from the left (zgeqr2);
+ *   the trailing matrix A[i+nb:, i+nb:] gets H^H . H from both sides.
+ * A is the full Hermitian matrix (both triangles, n x n, lda) and is kept
+ * full.  On exit: band (0 <= r-c <= nb) holds the band matrix, v (without
+ * its unit head) is stored below the band (r - c > nb) in the panel
+ * columns, tau[k*nb + j] the tau of panel k column j (0 if absent).
+ * Q1 = prod_k (H_{k,0} ... H_{k,nb-1}); Band = Q1^H A Q1 (reading R6). */
+void orc_he2hb(int64_t n, int64_t nb, zc *A, int64_t lda, zc *tau) {
+  zc *v = (zc *)malloc(sizeof(zc) * (n > 0 ? n : 1));
+  for (int64_t i = 0; i + nb < n; i += nb) {
+    int64_t pn = n - i - nb;                         /* panel rows        */
+    int64_t nref = pn < nb ? pn : nb;
+    for (int64_t j = 0; j < nb; j++) tau[i + j] = 0;
+    for (int64_t j = 0; j < nref; j++) {
+      int64_t c = i + j, r0 = i + nb + j, len = n - r0;
+      zc alpha = A[IX(r0, c, lda)], t;
+      orc_larfg(len, &alpha, &A[IX(r0 + 1, c, lda)], 1, &t);
+      tau[i + j] = t;
+      v[0] = 1;
+      for (int64_t r = 1; r < len; r++) v[r] = A[IX(r0 + r, c, lda)];
+      /* left: remaining panel columns, rows r0..n-1: A <- H^H A */
+      for (int64_t cc = c + 1; cc < i + nb; cc++) {
+        zc s = 0;
+        for (int64_t r = 0; r < len; r++) s += conj(v[r]) * A[IX(r0 + r, cc, lda)];
+        s *= conj(t);
+        for (int64_t r = 0; r < len; r++) A[IX(r0 + r, cc, lda)] -= v[r] * s;
+      }
+      /* two-sided: trailing Hermitian block rows/cols r0..n-1 */
+      herm_reflect(len, &A[IX(r0, r0, lda)], lda, v, t);
+      /* the block A[r0:, i+nb : r0] (trailing columns left of r0) gets H^H from
+         the left, and its mirror A[i+nb : r0, r0:] gets H from the right */
+      for (int64_t cc = i + nb; cc < r0; cc++) {
+        zc s = 0;
+        for (int64_t r = 0; r < len; r++) s += conj(v[r]) * A[IX(r0 + r, cc, lda)];
+        s *= conj(t);
+        for (int64_t r = 0; r < len; r++) A[IX(r0 + r, cc, lda)] -= v[r] * s;
+        for (int64_t r = 0; r < len; r++) A[IX(cc, r0 + r, lda)] = conj(A[IX(r0 + r, cc, lda)]);
+      }
+      A[IX(r0, c, lda)] = alpha;                     /* beta: real band entry */
+      /* mirror the panel column into the upper triangle (band part only) */
+      for (int64_t r = i + nb; r <= r0; r++) A[IX(c, r, lda)] = conj(A[IX(r, c, lda)]);
+    }
+    /* mirror the updated panel columns (R part) for the full-matrix view */
+    for (int64_t j = 0; j < nb; j++)
+      for (int64_t r = i + nb; r < n && r <= i + nb + j; r++) A[IX(i + j, r, lda)] = conj(A[IX(r, i + j, lda)]);
+  }
+  free(v);
+}
+
+/* T factor of a block of k reflectors (zlarft Forward/Columnwise):
+ * H_0 H_1 ... H_{k-1} = I - V T V^H, V (m x k, ldv) unit lower-trapezoidal
+ * with v_j[0..j-1] = 0, v_j[j] = 1 implied (entries of V on/above the
+ * diagonal are not read).  T (k x k, ldt) upper triangular:
+ *   T[j,j] = tau_j,  T[0:j, j] = -tau_j T[0:j,0:j] (V[:,0:j]^H v_j). */
+void orc_larft(int64_t m, int64_t k, const zc *V, int64_t ldv, const zc *tau, zc *T, int64_t ldt) {
+  for (int64_t j = 0; j < k; j++) {
+    for (int64_t i = 0; i < k; i++) T[IX(i, j, ldt)] = 0;
+    for (int64_t i = 0; i < j; i++) {              /* g_i = v_i^H v_j */
+      zc g = 0;
+      for (int64_t r = j; r < m; r++) {
+        zc vi = V[IX(r, i, ldv)];                  /* r > i always here   */
+        zc vj = (r == j) ? 1.0 : V[IX(r, j, ldv)];
+        g += conj(vi) * vj;
+      }
+      T[IX(i, j, ldt)] = -tau[j] * g;
+    }
+    /* T[0:j, j] = T[0:j, 0:j] * (that vector), upper triangular times vector */
+    for (int64_t i = 0; i < j; i++) {
+      zc s = 0;
+      for (int64_t l = i; l < j; l++) s += T[IX(i, l, ldt)] * T[IX(l, j, ldt)];
+      T[IX(i, j, ldt)] = s;
+    }
+    T[IX(j, j, ldt)] = tau[j];
+  }
+}
+
+/* Back-transform step Q1: E <- Q1 E with the he2hb reflectors stored
+ * in A below the band (orc_he2hb layout) and tau; one reflector at a time,
+ * last first: for k = K-1..0, j = nb-1..0: E <- H_{k,j} E. E is n x m. */
+void orc_apply_q1(int64_t n, int64_t nb, int64_t m, const zc *A, int64_t lda, const zc *tau, zc *E, int64_t lde) {
+  int64_t K = 0;
+  for (int64_t i = 0; i + nb < n; i += nb) K++;
+  for (int64_t k = K - 1; k >= 0; k--)
+    for (int64_t j = nb - 1; j >= 0; j--) {
+      int64_t c = k * nb + j, r0 = (k + 1) * nb + j;
+      if (r0 >= n) continue;
+      zc t = tau[c];
+      if (t == 0) continue;
+      int64_t len = n - r0;
+#pragma omp parallel for schedule(static)
+      for (int64_t q = 0; q < m; q++) {
+        zc w = E[IX(r0, q, lde)];
+        for (int64_t r = 1; r < len; r++) w += conj(A[IX(r0 + r, c, lda)]) * E[IX(r0 + r, q, lde)];
+        w *= t;
+        E[IX(r0, q, lde)] -= w;
+        for (int64_t r = 1; r < len; r++) E[IX(r0 + r, q, lde)] -= A[IX(r0 + r, c, lda)] * w;
+      }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Column-wise bulge chase (two-stage step 2), simulated on a dense
+ * full Hermitian copy M (n x n) of the band matrix (reading R5).
+ * Sweep i = 0..n-2, step j = 0,1,...: target column c = i (j = 0) or
+ * i+1+(j-1)*nb (j >= 1); rows r0 = i+1+j*nb .. r1 = min(i+(j+1)*nb, n-1);
+ * stop when r0 > n-1.  (beta, tau, v) = larfg(M[r0,c], M[r0+1:r1+1,c]);
+ * M <- H^H M H on rows/cols r0..r1 (all other rows/cols); M[r0,c] = beta,
+ * M[r0+1:r1+1, c] = 0 (and mirrors).
+ * Outputs: d[n], e[n-1] (e_i = beta of step (i,0), real), and the
+ * reflectors in the V2 layout of include/eig.h: step-major packed,
+ * slot(j, i) = off_j + i with off_j = sum_{j'<j} (n-1-j'*nb), each slot
+ * holding nb complex entries (v[0] = 1 explicit, zero padded) in V2 and one
+ * tau in tau2.  Returns the number of slots. */
+int64_t orc_v2_slots(int64_t n, int64_t nb) {
+  int64_t tot = 0;
+  for (int64_t j = 0; 1 + j * nb <= n - 1; j++) tot += n - 1 - j * nb;
+  return tot;
+}
+
+static int64_t v2_off(int64_t n, int64_t nb, int64_t j) {
+  int64_t off = 0;
+  for (int64_t jj = 0; jj < j; jj++) off += n - 1 - jj * nb;
+  return off;
+}
+
+void orc_hb2st(int64_t n, int64_t nb, zc *M, int64_t ldm, double *d, double *e, zc *V2, zc *tau2) {
+  int64_t slots = orc_v2_slots(n, nb);
+  for (int64_t s = 0; s < slots * nb; s++) V2[s] = 0;
+  for (int64_t s = 0; s < slots; s++) tau2[s] = 0;
+  zc *v = (zc *)malloc(sizeof(zc) * (nb + 1));
+  zc *wrk = (zc *)malloc(sizeof(zc) * (n > 0 ? n : 1));
+  for (int64_t i = 0; i + 1 < n; i++) {
+    for (int64_t j = 0;; j++) {
+      int64_t c = (j == 0) ? i : i + 1 + (j - 1) * nb;
+      int64_t r0 = i + 1 + j * nb;
+      if (r0 > n - 1) break;
+      int64_t r1 = i + (j + 1) * nb;
+      if (r1 > n - 1) r1 = n - 1;
+      int64_t len = r1 - r0 + 1;
+      zc alpha = M[IX(r0, c, ldm)], t;
+      for (int64_t r = 1; r < len; r++) v[r] = M[IX(r0 + r, c, ldm)];
+      orc_larfg(len, &alpha, &v[1], 1, &t);
+      v[0] = 1;
+      int64_t slot = v2_off(n, nb, j) + i;
+      for (int64_t r = 0; r < len; r++) V2[slot * nb + r] = v[r];
+      tau2[slot] = t;
+      if (t != 0) {
+        /* rows r0..r1, all columns: M <- H^H M */
+        for (int64_t q = 0; q < n; q++) {
+          zc s = 0;
+          for (int64_t r = 0; r < len; r++) s += conj(v[r]) * M[IX(r0 + r, q, ldm)];
+          wrk[q] = conj(t) * s;
+        }
+        for (int64_t q = 0; q < n; q++)
+          for (int64_t r = 0; r < len; r++) M[IX(r0 + r, q, ldm)] -= v[r] * wrk[q];
+        /* columns r0..r1, all rows: M <- M H */
+        for (int64_t q = 0; q < n; q++) {
+          zc s = 0;
+          for (int64_t r = 0; r < len; r++) s += M[IX(q, r0 + r, ldm)] * v[r];
+          wrk[q] = t * s;
+        }
+        for (int64_t r = 0; r < len; r++)
+          for (int64_t q = 0; q < n; q++) M[IX(q, r0 + r, ldm)] -= wrk[q] * conj(v[r]);
+      }
+      M[IX(r0, c, ldm)] = alpha;
+      M[IX(c, r0, ldm)] = conj(alpha);
+      for (int64_t r = 1; r < len; r++) { M[IX(r0 + r, c, ldm)] = 0; M[IX(c, r0 + r, ldm)] = 0; }
+      for (int64_t r = r0; r <= r1; r++) M[IX(r, r, ldm)] = creal(M[IX(r, r, ldm)]);
+    }
+  }
+  for (int64_t i = 0; i < n; i++) d[i] = creal(M[IX(i, i, ldm)]);
+  for (int64_t i = 0; i + 1 < n; i++) e[i] = creal(M[IX(i + 1, i, ldm)]);
+  free(v); free(wrk);
+}
+
+/* Back-transform step Q2: E <- Q2 E, Q2 = prod over (i, j) in chase
+ * order of H_{i,j}; one reflector at a time, the last one first.  V2/tau2 in
+ * the orc_hb2st layout.  E is n x m. */
+void orc_apply_q2(int64_t n, int64_t nb, int64_t m, const zc *V2, const zc *tau2, zc *E, int64_t lde) {
+  for (int64_t i = n - 2; i >= 0; i--) {
+    int64_t jmax = -1;
+    for (int64_t j = 0; i + 1 + j * nb <= n - 1; j++) jmax = j;
+    for (int64_t j = jmax; j >= 0; j--) {
+      int64_t r0 = i + 1 + j * nb, r1 = i + (j + 1) * nb;
+      if (r1 > n - 1) r1 = n - 1;
+      int64_t len = r1 - r0 + 1;
+      int64_t slot = v2_off(n, nb, j) + i;
+      zc t = tau2[slot];
+      if (t == 0) continue;
+      const zc *v = &V2[slot * nb];
+#pragma omp parallel for schedule(static) if (m >= 64)
+      for (int64_t q = 0; q < m; q++) {
+        zc w = 0;
+        for (int64_t r = 0; r < len; r++) w += conj(v[r]) * E[IX(r0 + r, q, lde)];
+        w *= t;
+        for (int64_t r = 0; r < len; r++) E[IX(r0 + r, q, lde)] -= v[r] * w;
+      }
+    }
+  }
+}
