@@ -1,0 +1,146 @@
+/*
+ * include/eig.h — C ABI of the B200-native two-stage Hermitian generalized
+ * eigensolver hot path (arXiv 1207.1773, /root/reference/PAPER.md = "P:Lnn").
+ *
+ * Library: paper_1207_1773_b200/libeigb200.so (CUDA, sm_100a).
+ *
+ * Conventions (all entry points):
+ *   - complex128 = two little-endian binary64 (re, im), interleaved.
+ *   - Matrices are column-major with a leading dimension ld >= rows.
+ *   - Hermitian inputs: only the lower triangle is read; imag(diag) ignored.
+ *   - Pointers are CUDA device pointers unless the entry point says "host".
+ *     The caller owns every pointer it passes; the library owns its workspace
+ *     (allocated on first use, grown on demand, freed by eig_finalize).
+ *   - Work is enqueued on the handle's stream (eig_config.stream, or the
+ *     legacy default stream if NULL).  Entry points are asynchronous unless
+ *     they say "synchronous"; errors detected on the host are returned
+ *     immediately, launch errors are returned as EIG_ERR_CUDA.
+ *   - Return codes (LAPACK info style, reading R11):
+ *       0                success
+ *       -i               argument i (1-based, counting the handle as 1) illegal
+ *       EIG_ERR_CUDA     a CUDA call failed (eig_last_cuda_error() has it)
+ *       EIG_ERR_NOMEM    device allocation failed
+ *       EIG_ERR_STATE    bad handle / not initialised
+ *       EIG_ERR_NOTIMPL  entry point not available in this build
+ *       EIG_ERR_NCCL     reserved (multi-GPU plumbing is torch.distributed)
+ *   - One handle per host thread; many handles may coexist.
+ */
+#ifndef EIG_B200_H
+#define EIG_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EIG_ERR_CUDA    (-1001)
+#define EIG_ERR_NCCL    (-1002)
+#define EIG_ERR_NOMEM   (-1003)
+#define EIG_ERR_STATE   (-1004)
+#define EIG_ERR_NOTIMPL (-1005)
+
+/* eig_hotpath flags */
+#define EIG_HOST_BUFFERS 1u  /* pointers are host memory: copy in, run, copy E out (synchronous) */
+#define EIG_SKIP_HE2HB   2u  /* back-transform only (A already holds he2hb output + T1)        */
+#define EIG_SKIP_BT      4u  /* he2hb only                                                      */
+
+typedef struct eig_ctx *eig_handle;
+
+typedef struct {
+  int device;        /* CUDA ordinal for this process                              */
+  int nb;            /* band half-width = he2hb panel width; 0 -> 64; 1..64 allowed */
+  int q2_group;      /* sweeps per grouped Q2 block (g); 0 -> 32; 1..64 allowed     */
+  void *stream;      /* cudaStream_t to order with; NULL = legacy default stream    */
+} eig_config;
+
+/* Create a handle.  cfg may be NULL (defaults).  Returns 0 or an error. */
+int eig_init(eig_handle *h, const eig_config *cfg);
+/* Destroy a handle and free its workspace (synchronises its stream). */
+int eig_finalize(eig_handle h);
+/* Static text for a return code. */
+const char *eig_strerror(int code);
+/* Text of the last CUDA error seen by this handle ("" if none). */
+const char *eig_last_cuda_error(eig_handle h);
+/* Kernel launches issued by this handle since creation (for bench accounting). */
+int64_t eig_launch_count(eig_handle h);
+/* Synchronise the handle's stream. */
+int eig_sync(eig_handle h);
+
+/* Number of he2hb panels K for order n and width nb (reading R3):
+ * K = #{i = 0, nb, 2nb, ... : i + nb < n}. */
+int64_t eig_num_panels(int64_t n, int nb);
+/* Number of Q2 reflector slots (V2 layout below) for order n, width nb. */
+int64_t eig_v2_slots(int64_t n, int nb);
+
+/* ------------------------------------------------------------------ a1..a5
+ * Reduction to band form, he2hb (Fig. 1; readings R1, R3, R6).
+ *   A   [in/out] n x n complex128, lda >= n.  In: Hermitian, lower triangle.
+ *       Out: lower band (0 <= r-c <= nb) = Band = Q1^H A Q1; below the band,
+ *       in column k*nb+j, the tail of reflector v_{k,j} whose unit head sits
+ *       at row (k+1)*nb+j.  The strict upper triangle is not referenced.
+ *   tau [out] K*nb complex128: tau of reflector (k, j) at k*nb+j (0 if absent).
+ *   T   [out] K*nb*nb complex128: T_k (nb x nb, column-major, upper
+ *       triangular) with H_{k,0}...H_{k,nb-1} = I - V_k T_k V_k^H.
+ * Uses nb from the handle's config. */
+int eig_he2hb(eig_handle h, int64_t n, void *A, int64_t lda, void *tau, void *T);
+
+/* ------------------------------------------------------------------ a7
+ * E <- Q1 E: E is n x m (lde >= n), A/T as produced by eig_he2hb. */
+int eig_apply_q1(eig_handle h, int64_t n, const void *A, int64_t lda, const void *T, void *E, int64_t lde,
+                 int64_t m);
+
+/* ------------------------------------------------------------------ a6
+ * Q2 reflector (V2) layout (reading R5): slot (j, i) for sweep i = 0..n-2 and
+ * step j with i + 1 + j*nb <= n-1 is at index off_j + i,
+ * off_j = sum_{j' < j} (n - 1 - j'*nb).  It acts on rows
+ * i+1+j*nb .. min(i+(j+1)*nb, n-1); V2[slot*nb + r] = v[r] (v[0] = 1,
+ * zero padded to nb), tau2[slot] = tau.  H = I - tau v v^H.
+ * Q2 = product over sweeps i ascending, steps j ascending of H_{i,j}.
+ *
+ * E <- Q2 E:  Z [in] n x m real binary64 (ldz >= n) if Z != NULL, in which
+ * case E is first set to complex(Z) (the complexification of a6);
+ * E [in/out] n x m complex128 (lde >= n).  V2: slots*nb complex128,
+ * tau2: slots complex128. */
+int eig_apply_q2(eig_handle h, int64_t n, const void *V2, const void *tau2, const double *Z, int64_t ldz, void *E,
+                 int64_t lde, int64_t m);
+
+/* ------------------------------------------------------------------ a8
+ * E <- L^-H E (Algorithm 1 step 4): L n x n lower triangular
+ * (non-unit; only the lower triangle read), E n x m. */
+int eig_trsm_lh(eig_handle h, int64_t n, const void *L, int64_t ldl, void *E, int64_t lde, int64_t m);
+
+/* ------------------------------------------------------------------ a1..a9
+ * One pass of the whole hot path:
+ *   he2hb(A) -> E = complex(Z) -> E = Q2 E -> E = Q1 E -> E = L^-H E
+ * on the m selected eigenvector columns (a9: the caller passes the m columns
+ * of the tridiagonal eigenvectors it wants, il..iu).
+ *   A    n x n (lda), Hermitian lower; destroyed (he2hb output).
+ *   tau1 K*nb, T1 K*nb*nb complex128 outputs (device; when EIG_HOST_BUFFERS
+ *        is set they may be NULL and stay in library workspace).
+ *   V2, tau2  Q2 reflectors (layout above).
+ *   L    n x n lower (ldl).   Z n x m real (ldz).   E n x m complex128 (lde) out.
+ * flags: EIG_HOST_BUFFERS -> A, V2, tau2, L, Z, E are HOST pointers (pinned
+ * recommended); the call copies them to the device, runs, copies E back and
+ * returns synchronously.  EIG_SKIP_HE2HB / EIG_SKIP_BT select a part. */
+int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void *T1, const void *V2,
+                const void *tau2, const void *L, int64_t ldl, const double *Z, int64_t ldz, void *E, int64_t lde,
+                int64_t m, unsigned flags);
+
+/* ------------------------------------------------------------------ expert
+ * Complex GEMM on the FP64 DMMA tile engine (exposed for parity tests):
+ *   C = alpha op(A) op(B) + beta C, op in {'N','C'} (C = conjugate transpose);
+ *   herm_a != 0: A is Hermitian with only its lower triangle stored (opa 'N');
+ *   lower_c != 0: only the lower triangle of C (M == N) is written, imag(diag)=0.
+ * alpha, beta real. */
+int eig_zgemm(eig_handle h, char opa, char opb, int64_t M, int64_t N, int64_t K, double alpha, const void *A,
+              int64_t lda, const void *B, int64_t ldb, double beta, void *C, int64_t ldc, int herm_a, int lower_c);
+
+/* Generalized solver (Algorithm 1).  Needs the NEXT stages
+ * (device hb2st, stedc, potrf/hegst); returns EIG_ERR_NOTIMPL in this build. */
+int eig_solve_gen(eig_handle h, int64_t n, void *A, int64_t lda, void *B, int64_t ldb, int range, double fraction,
+                  int64_t il, int64_t iu, double *w, void *Z, int64_t ldz, int64_t *m_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) hot path of the two-stage Hermitian generalized
+eigensolver of arXiv 1207.1773: he2hb (panel QR, T factor, two-sided update)
+and the eigenvector back-transform E = L^-H Q1 (Q2 Z).
+
+All compute runs in ``libeigb200.so`` (hand-written CUDA, FP64 DMMA).  This
+package is the C-ABI binding (``include/eig.h``) plus torch plumbing.  It
+never imports ``oracle/`` and has no CPU fallback.
+"""
+from ._binding import (EIG_HOST_BUFFERS, EIG_SKIP_BT, EIG_SKIP_HE2HB, EigError, Solver, colmajor,  # noqa: F401
+                       empty_colmajor, exported_symbols, lib, num_panels, v2_slots)
+
+__all__ = ["Solver", "EigError", "colmajor", "empty_colmajor", "lib", "num_panels", "v2_slots", "exported_symbols",
+           "EIG_HOST_BUFFERS", "EIG_SKIP_BT", "EIG_SKIP_HE2HB"]

@@ -1,0 +1,224 @@
+"""Thin ctypes binding of include/eig.h (argument marshalling only).
+
+Every step of the hot path runs in libeigb200.so's CUDA kernels; this module
+only converts torch tensors to (pointer, leading dimension) pairs.  torch is
+used for device memory and streams.  There is no CPU fallback: if the
+extension or the GPU is missing, every call raises.
+
+Matrices are column-major: a math m x n matrix is a torch tensor of shape
+(m, n) with strides (1, ld), ld >= m (see ``colmajor`` / ``empty_colmajor``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libeigb200.so")
+
+EIG_HOST_BUFFERS = 1
+EIG_SKIP_HE2HB = 2
+EIG_SKIP_BT = 4
+
+_lib = None
+
+
+class EigError(RuntimeError):
+    pass
+
+
+class _Config(C.Structure):
+    _fields_ = [("device", C.c_int), ("nb", C.c_int), ("q2_group", C.c_int), ("stream", C.c_void_p)]
+
+
+def lib():
+    """Load libeigb200.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise EigError(f"{_SO} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(_SO)
+        P, I, D, U = C.c_void_p, C.c_int64, C.c_double, C.c_uint
+        h = C.c_void_p
+        sig = {
+            "eig_init": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(_Config)]),
+            "eig_finalize": (C.c_int, [h]),
+            "eig_strerror": (C.c_char_p, [C.c_int]),
+            "eig_last_cuda_error": (C.c_char_p, [h]),
+            "eig_launch_count": (I, [h]),
+            "eig_sync": (C.c_int, [h]),
+            "eig_num_panels": (I, [I, C.c_int]),
+            "eig_v2_slots": (I, [I, C.c_int]),
+            "eig_he2hb": (C.c_int, [h, I, P, I, P, P]),
+            "eig_apply_q1": (C.c_int, [h, I, P, I, P, P, I, I]),
+            "eig_apply_q2": (C.c_int, [h, I, P, P, P, I, P, I, I]),
+            "eig_trsm_lh": (C.c_int, [h, I, P, I, P, I, I]),
+            "eig_hotpath": (C.c_int, [h, I, P, I, P, P, P, P, P, I, P, I, P, I, I, U]),
+            "eig_zgemm": (C.c_int, [h, C.c_char, C.c_char, I, I, I, D, P, I, P, I, D, P, I, C.c_int, C.c_int]),
+            "eig_solve_gen": (C.c_int, [h, I, P, I, P, I, C.c_int, D, I, I, P, P, I, P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return ["eig_init", "eig_finalize", "eig_strerror", "eig_last_cuda_error", "eig_launch_count", "eig_sync",
+            "eig_num_panels", "eig_v2_slots", "eig_he2hb", "eig_apply_q1", "eig_apply_q2", "eig_trsm_lh",
+            "eig_hotpath", "eig_zgemm", "eig_solve_gen"]
+
+
+def num_panels(n: int, nb: int) -> int:
+    return int(lib().eig_num_panels(n, nb))
+
+
+def v2_slots(n: int, nb: int) -> int:
+    return int(lib().eig_v2_slots(n, nb))
+
+
+# ------------------------------------------------------------ layout helpers
+def empty_colmajor(rows, cols, dtype=torch.complex128, device="cuda", ld=None):
+    ld = rows if ld is None else ld
+    return torch.empty((cols, ld), dtype=dtype, device=device).t()[:rows]
+
+
+def colmajor(x: torch.Tensor, device=None) -> torch.Tensor:
+    """Column-major (Fortran) copy of a 2-D tensor or numpy array."""
+    if isinstance(x, np.ndarray):
+        x = torch.from_numpy(np.ascontiguousarray(x))
+    if x.dim() == 1:
+        x = x[:, None]
+    y = x.t().contiguous().t()
+    return y.to(device) if device is not None else y
+
+
+def _ld(x: torch.Tensor) -> int:
+    if x.dim() != 2:
+        raise EigError("expected a 2-D column-major tensor")
+    if x.shape[1] > 1 and x.stride(0) != 1:
+        raise EigError("tensor is not column-major (stride(0) must be 1); use colmajor()")
+    return max(x.stride(1) if x.shape[1] > 1 else x.shape[0], 1)
+
+
+def _ptr(x):
+    return None if x is None else C.c_void_p(x.data_ptr())
+
+
+class Solver:
+    """One library handle (eig_init) bound to a CUDA device and stream."""
+
+    def __init__(self, device: int = 0, nb: int = 64, q2_group: int = 0, stream=None):
+        if not torch.cuda.is_available():
+            raise EigError("no CUDA device: the B200 path has no CPU fallback")
+        self.device = device
+        self.nb = nb
+        self.q2_group = q2_group
+        torch.cuda.set_device(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        cfg = _Config(device, nb, q2_group, C.c_void_p(stream.cuda_stream))
+        h = C.c_void_p()
+        self._check(lib().eig_init(C.byref(h), C.byref(cfg)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().eig_finalize(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = lib().eig_strerror(rc).decode()
+            extra = ""
+            if getattr(self, "h", None):
+                extra = lib().eig_last_cuda_error(self.h).decode()
+            raise EigError(f"eig rc={rc}: {msg} {extra}".strip())
+
+    @property
+    def launches(self) -> int:
+        return int(lib().eig_launch_count(self.h))
+
+    def sync(self):
+        self._check(lib().eig_sync(self.h))
+
+    # ------------------------------------------------------------ stages
+    def he2hb(self, A: torch.Tensor):
+        """a1..a5: A (n x n column-major complex128, lower) -> band + V in place.
+        Returns (tau [K*nb], T [K, nb, nb] column-major blocks as (K, nb*nb))."""
+        n = A.shape[0]
+        K = num_panels(n, self.nb)
+        tau = torch.zeros(max(K * self.nb, 1), dtype=torch.complex128, device=A.device)
+        T = torch.zeros(max(K * self.nb * self.nb, 1), dtype=torch.complex128, device=A.device)
+        self._check(lib().eig_he2hb(self.h, n, _ptr(A), _ld(A), _ptr(tau), _ptr(T)))
+        return tau, T
+
+    def apply_q1(self, A, T, E):
+        n, m = E.shape
+        self._check(lib().eig_apply_q1(self.h, n, _ptr(A), _ld(A), _ptr(T), _ptr(E), _ld(E), m))
+        return E
+
+    def apply_q2(self, V2, tau2, E, Z=None):
+        n, m = E.shape
+        ldz = _ld(Z) if Z is not None else n
+        self._check(lib().eig_apply_q2(self.h, n, _ptr(V2), _ptr(tau2), _ptr(Z), ldz, _ptr(E), _ld(E), m))
+        return E
+
+    def trsm_lh(self, L, E):
+        n, m = E.shape
+        self._check(lib().eig_trsm_lh(self.h, n, _ptr(L), _ld(L), _ptr(E), _ld(E), m))
+        return E
+
+    def zgemm(self, opa, opb, A, B, Cm, alpha=1.0, beta=0.0, herm_a=False, lower_c=False, K=None):
+        M, N = Cm.shape
+        if K is None:
+            K = A.shape[1] if opa == "N" else A.shape[0]
+        self._check(lib().eig_zgemm(self.h, opa.encode(), opb.encode(), M, N, K, alpha, _ptr(A), _ld(A), _ptr(B),
+                                    _ld(B), beta, _ptr(Cm), _ld(Cm), int(herm_a), int(lower_c)))
+        return Cm
+
+    def hotpath(self, A, V2, tau2, L, Z, E=None, flags=0, tau1=None, T1=None):
+        """One pass of the whole hot path on device tensors:
+        he2hb(A) -> E = complex(Z) -> Q2 -> Q1 -> L^-H.  Returns (E, tau1, T1)."""
+        n = A.shape[0]
+        m = Z.shape[1]
+        K = num_panels(n, self.nb)
+        if tau1 is None:
+            tau1 = torch.zeros(max(K * self.nb, 1), dtype=torch.complex128, device=A.device)
+        if T1 is None:
+            T1 = torch.zeros(max(K * self.nb * self.nb, 1), dtype=torch.complex128, device=A.device)
+        if E is None:
+            E = empty_colmajor(n, m, device=A.device)
+        self._check(lib().eig_hotpath(self.h, n, _ptr(A), _ld(A), _ptr(tau1), _ptr(T1), _ptr(V2), _ptr(tau2),
+                                      _ptr(L), _ld(L), _ptr(Z), _ld(Z), _ptr(E), _ld(E), m, flags))
+        return E, tau1, T1
+
+    def hotpath_host(self, A: np.ndarray, V2: np.ndarray, tau2: np.ndarray, L: np.ndarray, Z: np.ndarray,
+                     E: np.ndarray):
+        """Same pass through the C ABI with HOST buffers (EIG_HOST_BUFFERS):
+        copies in, runs, copies E out, synchronously.  Arrays must be
+        Fortran-ordered (column-major); pinned memory is recommended."""
+        n = A.shape[0]
+        m = Z.shape[1]
+        for name, x in (("A", A), ("L", L), ("Z", Z), ("E", E)):
+            if not x.flags.f_contiguous:
+                raise EigError(f"{name} must be Fortran-ordered")
+
+        def hp(x):
+            return C.c_void_p(x.ctypes.data)
+
+        self._check(lib().eig_hotpath(self.h, n, hp(A), n, None, None, hp(V2), hp(tau2), hp(L), n, hp(Z), n,
+                                      hp(E), n, m, EIG_HOST_BUFFERS))
+        return E

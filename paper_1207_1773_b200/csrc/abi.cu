@@ -1,0 +1,425 @@
+// abi.cu — C ABI (include/eig.h) and the stage drivers of libeigb200.
+//
+// he2hb driver (Fig. 1; readings R3, R6), Q1 / Q2 / trsm
+// back-transform drivers, the whole hot-path pass, and the
+// handle / workspace management.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/eig.h"
+#include "ctx.h"
+#include "kernels.h"
+
+namespace eig {
+
+void *Ctx::ws(int id, size_t need) {
+  if (need == 0) need = 16;
+  if (buf[id] && bytes[id] >= need) return buf[id];
+  if (buf[id]) {
+    cudaFree(buf[id]);  // synchronising: no in-flight kernel can still use it
+    buf[id] = nullptr;
+    bytes[id] = 0;
+  }
+  size_t alloc = need + need / 8;
+  if (cudaMalloc(&buf[id], alloc) != cudaSuccess) {
+    cudaGetLastError();
+    if (cudaMalloc(&buf[id], need) != cudaSuccess) {
+      cudaGetLastError();
+      buf[id] = nullptr;
+      last_err = "cudaMalloc failed";
+      return nullptr;
+    }
+    alloc = need;
+  }
+  bytes[id] = alloc;
+  return buf[id];
+}
+
+int Ctx::check(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return 0;
+  last_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return EIG_ERR_CUDA;
+}
+
+static int64_t num_panels(int64_t n, int nb) {
+  if (n <= nb) return 0;
+  return (n - nb - 1) / nb + 1;
+}
+
+static int64_t v2_slots(int64_t n, int nb) {
+  int64_t tot = 0;
+  for (int64_t j = 0; 1 + j * nb <= n - 1; j++) tot += n - 1 - j * nb;
+  return tot;
+}
+
+// ------------------------------------------------------------------ he2hb
+static int he2hb_run(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau, double2 *T) {
+  const int nb = c.nb;
+  const int64_t K = num_panels(n, nb);
+  EIG_TRY(real_diag(c, n, A, lda));
+  if (K == 0) return 0;
+  const int64_t ldw = n - nb;
+  double2 *VXV = (double2 *)c.ws(WS_VXV, (size_t)ldw * 3 * nb * sizeof(double2));
+  double2 *Wb = (double2 *)c.ws(WS_W, (size_t)ldw * nb * sizeof(double2));
+  double2 *Sm = (double2 *)c.ws(WS_SMALL, (size_t)2 * nb * nb * sizeof(double2));
+  if (!VXV || !Wb || !Sm) return EIG_ERR_NOMEM;
+  double2 *V = VXV, *X = VXV + ldw * nb, *V2 = VXV + 2 * ldw * nb;
+  for (int64_t k = 0; k < K; k++) {
+    const int64_t i = k * nb, r0 = i + nb, s = n - r0;
+    double2 *P = A + r0 + i * lda;
+    double2 *A22 = A + r0 + r0 * lda;
+    double2 *Tk = T + k * nb * nb;
+    // a1 + a2: panel QR and T
+    EIG_TRY(panel_qr(c, P, lda, s, nb, tau + k * nb, Tk, V, V2, ldw));
+    Zgemm g;
+    // a3: W = A22 V T
+    g = Zgemm();
+    g.herm_a = 1; g.M = s; g.N = nb; g.K = s; g.A = A22; g.lda = lda; g.B = V; g.ldb = ldw; g.C = Wb; g.ldc = ldw;
+    EIG_TRY(zgemm(c, g));
+    g = Zgemm();
+    g.M = s; g.N = nb; g.K = nb; g.A = Wb; g.lda = ldw; g.B = Tk; g.ldb = nb; g.C = X; g.ldc = ldw;
+    EIG_TRY(zgemm(c, g));
+    // a4: M = T^H (V^H W);  X = W - 1/2 V M
+    g = Zgemm();
+    g.opa = OP_C; g.M = nb; g.N = nb; g.K = s; g.A = V; g.lda = ldw; g.B = X; g.ldb = ldw; g.C = Sm; g.ldc = nb;
+    EIG_TRY(zgemm(c, g));
+    g = Zgemm();
+    g.opa = OP_C; g.M = nb; g.N = nb; g.K = nb; g.A = Tk; g.lda = nb; g.B = Sm; g.ldb = nb; g.C = Sm + nb * nb;
+    g.ldc = nb;
+    EIG_TRY(zgemm(c, g));
+    g = Zgemm();
+    g.M = s; g.N = nb; g.K = nb; g.A = V; g.lda = ldw; g.B = Sm + nb * nb; g.ldb = nb; g.C = X; g.ldc = ldw;
+    g.alpha = -0.5; g.beta = 1.0;
+    EIG_TRY(zgemm(c, g));
+    // a5: A22 -= [V X] [X V]^H   (lower triangle)
+    g = Zgemm();
+    g.opb = OP_C; g.lower_c = 1; g.M = s; g.N = s; g.K = 2 * nb; g.A = VXV; g.lda = ldw; g.B = X; g.ldb = ldw;
+    g.C = A22; g.ldc = lda; g.alpha = -1.0; g.beta = 1.0;
+    EIG_TRY(zgemm(c, g));
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ Q1
+static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const double2 *T, double2 *E, int64_t lde,
+                        int64_t m) {
+  const int nb = c.nb;
+  const int64_t K = num_panels(n, nb);
+  if (K == 0 || m <= 0) return 0;
+  const int64_t ldv = n - nb;
+  double2 *Vb = (double2 *)c.ws(WS_V, (size_t)ldv * nb * sizeof(double2));
+  double2 *Y = (double2 *)c.ws(WS_Y, (size_t)nb * m * sizeof(double2));
+  double2 *Y2 = (double2 *)c.ws(WS_Y2, (size_t)nb * m * sizeof(double2));
+  if (!Vb || !Y || !Y2) return EIG_ERR_NOMEM;
+  for (int64_t k = K - 1; k >= 0; k--) {
+    const int64_t r0 = (k + 1) * nb, s = n - r0;
+    EIG_TRY(extract_v(c, A + r0 + k * nb * lda, lda, s, nb, Vb, ldv));
+    Zgemm g;
+    g.opa = OP_C; g.M = nb; g.N = m; g.K = s; g.A = Vb; g.lda = ldv; g.B = E + r0; g.ldb = lde; g.C = Y; g.ldc = nb;
+    EIG_TRY(zgemm(c, g));
+    g = Zgemm();
+    g.M = nb; g.N = m; g.K = nb; g.A = T + k * nb * nb; g.lda = nb; g.B = Y; g.ldb = nb; g.C = Y2; g.ldc = nb;
+    EIG_TRY(zgemm(c, g));
+    g = Zgemm();
+    g.M = s; g.N = m; g.K = nb; g.A = Vb; g.lda = ldv; g.B = Y2; g.ldb = nb; g.C = E + r0; g.ldc = lde;
+    g.alpha = -1.0; g.beta = 1.0;
+    EIG_TRY(zgemm(c, g));
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ trsm
+static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2 *E, int64_t lde, int64_t m) {
+  if (n <= 0 || m <= 0) return 0;
+  const int bs = 64;
+  const int64_t nblk = (n + bs - 1) / bs;
+  double2 *Linv = (double2 *)c.ws(WS_LINV, (size_t)nblk * bs * bs * sizeof(double2));
+  if (!Linv) return EIG_ERR_NOMEM;
+  EIG_TRY(trinv_blocks(c, n, bs, L, ldl, Linv));
+  for (int64_t I = nblk - 1; I >= 0; I--) {
+    const int64_t I0 = I * bs, b = std::min<int64_t>(bs, n - I0), I1 = I0 + b;
+    Zgemm g;
+    if (I1 < n) {
+      g.opa = OP_C; g.M = b; g.N = m; g.K = n - I1; g.A = L + I1 + I0 * ldl; g.lda = ldl; g.B = E + I1; g.ldb = lde;
+      g.C = E + I0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+    }
+    // in place: one 64-row M tile per column tile, no split-K -> every CTA reads
+    // its whole K range before its epilogue writes
+    g = Zgemm();
+    g.opa = OP_C; g.M = b; g.N = m; g.K = b; g.A = Linv + I * bs * bs; g.lda = bs; g.B = E + I0; g.ldb = lde;
+    g.C = E + I0; g.ldc = lde; g.alpha = 1.0; g.beta = 0.0; g.splitk = 1;
+    EIG_TRY(zgemm(c, g));
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ Q2
+struct Q2Cache {
+  int64_t n = -1;
+  int nb = 0, g = 0;
+  Q2Plan plan;
+};
+
+static int q2_plan(Ctx &c, int64_t n, Q2Plan &p) {
+  const int nb = c.nb, g = c.q2g;
+  p.n = n;
+  p.nb = nb;
+  p.g = g;
+  p.ngroups = (n - 1 + g - 1) / g;
+  std::vector<int64_t> first(p.ngroups + 1);
+  int64_t tot = 0;
+  for (int64_t gi = 0; gi < p.ngroups; gi++) {
+    first[gi] = tot;
+    const int64_t i0 = gi * g;
+    tot += (i0 > n - 2) ? 0 : (n - 2 - i0) / nb + 1;
+  }
+  first[p.ngroups] = tot;
+  p.nblocks = tot;
+  std::vector<int64_t> off;
+  int64_t o = 0;
+  for (int64_t j = 0; 1 + j * nb <= n - 1; j++) {
+    off.push_back(o);
+    o += n - 1 - j * nb;
+  }
+  p.J = (int64_t)off.size();
+  int64_t *d = (int64_t *)c.ws(WS_Q2PLAN, (first.size() + off.size() + 1) * sizeof(int64_t));
+  if (!d) return EIG_ERR_NOMEM;
+  EIG_TRY(c.check(cudaMemcpy(d, first.data(), first.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "q2 plan"));
+  if (!off.empty())
+    EIG_TRY(c.check(cudaMemcpy(d + first.size(), off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice),
+                    "q2 plan"));
+  p.d_group_first_block = d;
+  p.d_off = d + first.size();
+  return 0;
+}
+
+static int apply_q2_run(Ctx &c, int64_t n, const double2 *V2, const double2 *tau2, double2 *E, int64_t lde,
+                        int64_t m) {
+  if (n <= 1 || m <= 0) return 0;
+  if (c.q2g < 4) return EIG_ERR_NOTIMPL;  // nb < 3: no grouped blocks
+  static thread_local Q2Cache cache;  // plan tables are tiny; rebuilt when (n, nb, g) or the buffer changes
+  Q2Plan p;
+  if (cache.n == n && cache.nb == c.nb && cache.g == c.q2g && cache.plan.d_group_first_block == c.buf[WS_Q2PLAN]) {
+    p = cache.plan;
+  } else {
+    EIG_TRY(q2_plan(c, n, p));
+    cache.n = n;
+    cache.nb = c.nb;
+    cache.g = c.q2g;
+    cache.plan = p;
+  }
+  double2 *T2 = (double2 *)c.ws(WS_T2, (size_t)p.nblocks * p.g * p.g * sizeof(double2));
+  if (!T2) return EIG_ERR_NOMEM;
+  EIG_TRY(q2_tfactors(c, p, V2, tau2, T2));
+  return q2_apply(c, p, V2, T2, E, lde, m);
+}
+
+}  // namespace eig
+
+using namespace eig;
+
+struct eig_ctx {
+  Ctx c;
+};
+
+static int valid(eig_handle h) { return (h != nullptr) ? 0 : EIG_ERR_STATE; }
+
+extern "C" {
+
+int eig_init(eig_handle *h, const eig_config *cfg) {
+  if (!h) return -1;
+  eig_ctx *x = new (std::nothrow) eig_ctx();
+  if (!x) return EIG_ERR_NOMEM;
+  if (cfg) {
+    x->c.device = cfg->device;
+    x->c.stream = (cudaStream_t)cfg->stream;
+    if (cfg->nb) x->c.nb = cfg->nb;
+    if (cfg->q2_group) x->c.q2g = cfg->q2_group;
+  }
+  if (x->c.nb < 1 || x->c.nb > 64) { delete x; return -2; }
+  if (!cfg || !cfg->q2_group) x->c.q2g = std::min(32, ((x->c.nb + 1) / 4) * 4);  // g <= nb + 1, multiple of 4
+  if (x->c.q2g != 0 && (x->c.q2g < 4 || x->c.q2g > 32 || x->c.q2g % 4 || x->c.q2g - 1 > x->c.nb)) {
+    delete x;
+    return -2;
+  }
+  int rc = x->c.check(cudaSetDevice(x->c.device), "cudaSetDevice");
+  if (rc) { delete x; return rc; }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->c.device);
+  if (sms > 0) x->c.num_sms = sms;
+  void *bar = x->c.ws(WS_BARRIER, 64);
+  if (!bar) { delete x; return EIG_ERR_NOMEM; }
+  rc = x->c.check(cudaMemset(bar, 0, 64), "barrier init");
+  if (rc) { delete x; return rc; }
+  *h = x;
+  return 0;
+}
+
+int eig_finalize(eig_handle h) {
+  if (!h) return EIG_ERR_STATE;
+  cudaSetDevice(h->c.device);
+  cudaStreamSynchronize(h->c.stream);
+  for (int i = 0; i < WS_COUNT; i++) {
+    if (h->c.buf[i]) cudaFree(h->c.buf[i]);
+  }
+  delete h;
+  return 0;
+}
+
+const char *eig_strerror(int code) {
+  switch (code) {
+    case 0: return "success";
+    case EIG_ERR_CUDA: return "CUDA error";
+    case EIG_ERR_NCCL: return "NCCL error";
+    case EIG_ERR_NOMEM: return "device allocation failed";
+    case EIG_ERR_STATE: return "bad handle or state";
+    case EIG_ERR_NOTIMPL: return "not implemented in this build";
+    default: return code < 0 ? "illegal argument" : "matrix B not positive definite / stage failure";
+  }
+}
+
+const char *eig_last_cuda_error(eig_handle h) { return h ? h->c.last_err.c_str() : "no handle"; }
+int64_t eig_launch_count(eig_handle h) { return h ? h->c.launches : -1; }
+int eig_sync(eig_handle h) {
+  if (!h) return EIG_ERR_STATE;
+  return h->c.check(cudaStreamSynchronize(h->c.stream), "cudaStreamSynchronize");
+}
+int64_t eig_num_panels(int64_t n, int nb) { return num_panels(n, nb); }
+int64_t eig_v2_slots(int64_t n, int nb) { return v2_slots(n, nb); }
+
+int eig_he2hb(eig_handle h, int64_t n, void *A, int64_t lda, void *tau, void *T) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (!A && n > 0) return -3;
+  if (lda < std::max<int64_t>(1, n)) return -4;
+  if (num_panels(n, h->c.nb) > 0 && (!tau || !T)) return !tau ? -5 : -6;
+  cudaSetDevice(h->c.device);
+  return he2hb_run(h->c, n, (double2 *)A, lda, (double2 *)tau, (double2 *)T);
+}
+
+int eig_apply_q1(eig_handle h, int64_t n, const void *A, int64_t lda, const void *T, void *E, int64_t lde, int64_t m) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (lda < std::max<int64_t>(1, n)) return -4;
+  if (lde < std::max<int64_t>(1, n)) return -7;
+  if (m < 0) return -8;
+  cudaSetDevice(h->c.device);
+  return apply_q1_run(h->c, n, (const double2 *)A, lda, (const double2 *)T, (double2 *)E, lde, m);
+}
+
+int eig_apply_q2(eig_handle h, int64_t n, const void *V2, const void *tau2, const double *Z, int64_t ldz, void *E,
+                 int64_t lde, int64_t m) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (Z && ldz < std::max<int64_t>(1, n)) return -6;
+  if (lde < std::max<int64_t>(1, n)) return -8;
+  if (m < 0) return -9;
+  cudaSetDevice(h->c.device);
+  if (Z) EIG_TRY(complexify(h->c, n, m, Z, ldz, (double2 *)E, lde));
+  return apply_q2_run(h->c, n, (const double2 *)V2, (const double2 *)tau2, (double2 *)E, lde, m);
+}
+
+int eig_trsm_lh(eig_handle h, int64_t n, const void *L, int64_t ldl, void *E, int64_t lde, int64_t m) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (ldl < std::max<int64_t>(1, n)) return -4;
+  if (lde < std::max<int64_t>(1, n)) return -6;
+  if (m < 0) return -7;
+  cudaSetDevice(h->c.device);
+  return trsm_lh_run(h->c, n, (const double2 *)L, ldl, (double2 *)E, lde, m);
+}
+
+int eig_zgemm(eig_handle h, char opa, char opb, int64_t M, int64_t N, int64_t K, double alpha, const void *A,
+              int64_t lda, const void *B, int64_t ldb, double beta, void *C, int64_t ldc, int herm_a, int lower_c) {
+  EIG_TRY(valid(h));
+  Zgemm g;
+  if (opa != 'N' && opa != 'C') return -2;
+  if (opb != 'N' && opb != 'C') return -3;
+  if (M < 0) return -4;
+  if (N < 0) return -5;
+  if (K < 0) return -6;
+  g.opa = (opa == 'C') ? OP_C : OP_N;
+  g.opb = (opb == 'C') ? OP_C : OP_N;
+  g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = beta;
+  g.A = (const double2 *)A; g.lda = lda; g.B = (const double2 *)B; g.ldb = ldb; g.C = (double2 *)C; g.ldc = ldc;
+  g.herm_a = herm_a; g.lower_c = lower_c;
+  cudaSetDevice(h->c.device);
+  return zgemm(h->c, g);
+}
+
+int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void *T1, const void *V2,
+                const void *tau2, const void *L, int64_t ldl, const double *Z, int64_t ldz, void *E, int64_t lde,
+                int64_t m, unsigned flags) {
+  EIG_TRY(valid(h));
+  Ctx &c = h->c;
+  if (n < 1) return -2;
+  if (lda < n) return -4;
+  if (ldl < n) return -11;
+  if (ldz < n) return -13;
+  if (lde < n) return -15;
+  if (m < 0 || m > n) return -16;
+  cudaSetDevice(c.device);
+  const int nb = c.nb;
+  const int64_t K = num_panels(n, nb), slots = v2_slots(n, nb);
+  const bool host = flags & EIG_HOST_BUFFERS;
+  double2 *dA = (double2 *)A, *dT1 = (double2 *)T1, *dtau1 = (double2 *)tau1, *dE = (double2 *)E;
+  const double2 *dV2 = (const double2 *)V2, *dtau2 = (const double2 *)tau2, *dL = (const double2 *)L;
+  const double *dZ = Z;
+  int64_t dlda = lda, dldl = ldl, dldz = ldz, dlde = lde;
+  if (host) {
+    // device staging in library workspace, packed leading dimensions
+    dA = (double2 *)c.ws(WS_HOST_A, (size_t)n * n * sizeof(double2));
+    double2 *v2 = (double2 *)c.ws(WS_HOST_V2, (size_t)std::max<int64_t>(slots, 1) * nb * sizeof(double2));
+    double2 *t2 = (double2 *)c.ws(WS_HOST_TAU2, (size_t)std::max<int64_t>(slots, 1) * sizeof(double2));
+    double2 *l = (double2 *)c.ws(WS_HOST_L, (size_t)n * n * sizeof(double2));
+    double *z = (double *)c.ws(WS_HOST_Z, (size_t)n * std::max<int64_t>(m, 1) * sizeof(double));
+    dE = (double2 *)c.ws(WS_HOST_E, (size_t)n * std::max<int64_t>(m, 1) * sizeof(double2));
+    dtau1 = (double2 *)c.ws(WS_HOST_TAU1, (size_t)std::max<int64_t>(K, 1) * nb * sizeof(double2));
+    dT1 = (double2 *)c.ws(WS_HOST_T1, (size_t)std::max<int64_t>(K, 1) * nb * nb * sizeof(double2));
+    if (!dA || !v2 || !t2 || !l || !z || !dE || !dtau1 || !dT1) return EIG_ERR_NOMEM;
+    EIG_TRY(c.check(cudaMemcpy2DAsync(dA, n * sizeof(double2), A, lda * sizeof(double2), n * sizeof(double2), n,
+                                      cudaMemcpyHostToDevice, c.stream), "H2D A"));
+    if (!(flags & EIG_SKIP_BT)) {
+      EIG_TRY(c.check(cudaMemcpyAsync(v2, V2, (size_t)slots * nb * sizeof(double2), cudaMemcpyHostToDevice, c.stream),
+                      "H2D V2"));
+      EIG_TRY(c.check(cudaMemcpyAsync(t2, tau2, (size_t)slots * sizeof(double2), cudaMemcpyHostToDevice, c.stream),
+                      "H2D tau2"));
+      EIG_TRY(c.check(cudaMemcpy2DAsync(l, n * sizeof(double2), L, ldl * sizeof(double2), n * sizeof(double2), n,
+                                        cudaMemcpyHostToDevice, c.stream), "H2D L"));
+      if (m > 0)
+        EIG_TRY(c.check(cudaMemcpy2DAsync(z, n * sizeof(double), Z, ldz * sizeof(double), n * sizeof(double), m,
+                                          cudaMemcpyHostToDevice, c.stream), "H2D Z"));
+    }
+    dV2 = v2; dtau2 = t2; dL = l; dZ = z;
+    dlda = n; dldl = n; dldz = n; dlde = n;
+  }
+  if (!(flags & EIG_SKIP_HE2HB)) EIG_TRY(he2hb_run(c, n, dA, dlda, dtau1, dT1));
+  if (!(flags & EIG_SKIP_BT) && m > 0) {
+    EIG_TRY(complexify(c, n, m, dZ, dldz, dE, dlde));                      // a6: complexify
+    EIG_TRY(apply_q2_run(c, n, dV2, dtau2, dE, dlde, m));                   // a6: Q2
+    EIG_TRY(apply_q1_run(c, n, dA, dlda, dT1, dE, dlde, m));                // a7: Q1
+    EIG_TRY(trsm_lh_run(c, n, dL, dldl, dE, dlde, m));                      // a8: L^-H
+  }
+  if (host) {
+    if (!(flags & EIG_SKIP_BT) && m > 0 && E)
+      EIG_TRY(c.check(cudaMemcpy2DAsync(E, lde * sizeof(double2), dE, n * sizeof(double2), n * sizeof(double2), m,
+                                        cudaMemcpyDeviceToHost, c.stream), "D2H E"));
+    EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync"));
+  }
+  return 0;
+}
+
+int eig_solve_gen(eig_handle h, int64_t n, void *A, int64_t lda, void *B, int64_t ldb, int range, double fraction,
+                  int64_t il, int64_t iu, double *w, void *Z, int64_t ldz, int64_t *m_out) {
+  (void)n; (void)A; (void)lda; (void)B; (void)ldb; (void)range; (void)fraction; (void)il; (void)iu; (void)w; (void)Z;
+  (void)ldz; (void)m_out;
+  EIG_TRY(valid(h));
+  return EIG_ERR_NOTIMPL;
+}
+
+}  // extern "C"

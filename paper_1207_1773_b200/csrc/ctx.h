@@ -1,0 +1,58 @@
+// ctx.h — handle state of libeigb200 (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/eig.h"
+
+namespace eig {
+
+enum WsId {
+  WS_VXV = 0,     // s x 3nb: [V | X | V]
+  WS_W,           // s x nb
+  WS_PART,        // split-K partials
+  WS_SMALL,       // nb x nb scratch (Mh, M)
+  WS_PANEL_REC,   // panel reduction records
+  WS_PANEL_GRAM,  // panel Gram partials
+  WS_BARRIER,     // grid barrier words
+  WS_V,           // BT: explicit V_k
+  WS_Y,           // BT: nb x m
+  WS_Y2,          // BT: nb x m
+  WS_LINV,        // trsm: inverted diagonal blocks
+  WS_T2,          // Q2 T factors
+  WS_Q2PLAN,      // Q2 plan tables
+  WS_HOST_A, WS_HOST_V2, WS_HOST_TAU2, WS_HOST_L, WS_HOST_Z, WS_HOST_E, WS_HOST_TAU1, WS_HOST_T1,
+  WS_COUNT
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int nb = 64;
+  int q2g = 32;
+  int num_sms = 148;
+  int64_t launches = 0;
+  std::string last_err;
+  void *buf[WS_COUNT] = {};
+  size_t bytes[WS_COUNT] = {};
+
+  // Returns a device buffer of at least `need` bytes (grown, contents lost).
+  void *ws(int id, size_t need);
+  // Record a CUDA error; returns EIG_ERR_CUDA or 0.
+  int check(cudaError_t e, const char *what);
+  // After a kernel launch: count it and check for launch errors.
+  int launched(const char *what) {
+    launches++;
+    return check(cudaGetLastError(), what);
+  }
+};
+
+}  // namespace eig
+
+#define EIG_TRY(x)            \
+  do {                        \
+    int _rc = (x);            \
+    if (_rc) return _rc;      \
+  } while (0)

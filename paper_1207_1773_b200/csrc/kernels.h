@@ -1,0 +1,64 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal to libeigb200).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace eig {
+
+struct Ctx;  // defined in abi.cu
+
+// ------------------------------------------------------------- zgemm engine
+enum Op { OP_N = 0, OP_C = 1 };
+
+struct Zgemm {
+  int opa = OP_N, opb = OP_N;
+  int herm_a = 0;   // A Hermitian, lower stored (opa must be N)
+  int lower_c = 0;  // only lower triangle of C (M == N), imag(diag) = 0
+  int64_t M = 0, N = 0, K = 0;
+  const double2 *A = nullptr;
+  int64_t lda = 0;
+  const double2 *B = nullptr;
+  int64_t ldb = 0;
+  double2 *C = nullptr;
+  int64_t ldc = 0;
+  double alpha = 1.0, beta = 0.0;
+  int splitk = 0;   // 0 = choose automatically, 1 = none, >1 = forced
+};
+
+// Enqueue C = alpha op(A) op(B) + beta C on ctx's stream.  Returns 0 or error.
+int zgemm(Ctx &ctx, const Zgemm &g);
+
+// ------------------------------------------------------------- he2hb pieces
+// Panel QR + T factor (cooperative).  Panel P = A[r0:n, c0:c0+nb] (pn rows),
+// writes V (explicit, pn x nb, ldv) into vout (and vout2 if non-null),
+// tau[nb], T (nb x nb, ld nb).
+int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau, double2 *T, double2 *vout,
+             double2 *vout2, int64_t ldv);
+
+// Copy the reflectors of panel k from the he2hb layout into an explicit
+// unit-lower s x nb matrix (ld ldv).
+int extract_v(Ctx &ctx, const double2 *P, int64_t lda, int64_t pn, int nb, double2 *V, int64_t ldv);
+
+// Inverse of the diagonal blocks of a lower triangular L: Linv[b] (bs x bs).
+int trinv_blocks(Ctx &ctx, int64_t n, int bs, const double2 *L, int64_t ldl, double2 *Linv);
+
+// E = complex(Z)
+int complexify(Ctx &ctx, int64_t n, int64_t m, const double *Z, int64_t ldz, double2 *E, int64_t lde);
+
+// Zero the imaginary part of the diagonal of A (n x n).
+int real_diag(Ctx &ctx, int64_t n, double2 *A, int64_t lda);
+
+// ------------------------------------------------------------- Q2
+struct Q2Plan {
+  int64_t n = 0;
+  int nb = 0, g = 0;
+  int64_t ngroups = 0;
+  int64_t nblocks = 0;
+  int64_t *d_group_first_block = nullptr;  // [ngroups+1] device
+  int64_t *d_off = nullptr;                // [J] device slot offsets per step j
+  int64_t J = 0;
+};
+int q2_tfactors(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *tau2, double2 *T2);
+int q2_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, double2 *E, int64_t lde, int64_t m);
+
+}  // namespace eig

@@ -1,0 +1,322 @@
+// zgemm.cu — complex-FP64 tile engine on the DMMA pipe (sm_100a).
+//
+// C = alpha op(A) op(B) + beta C via the real embedding described in
+// common.cuh.  Block tile 64 x 64 complex (128 real rows x 64 cols of C~),
+// K tile 16 complex, 3-stage cp.async pipeline, 8 warps as 4 (M) x 2 (N),
+// warp tile 32 real rows x 32 cols = 4 x 4 DMMA.8x8x4 accumulators.
+// Modes: Hermitian-lower A (hemm, a3), lower-triangular C (her2k, a5),
+// split-K with a deterministic reduction (skinny products, a4/a7/a8).
+// Used by he2hb (Fig. 1 (c) P:L97), Q1 and trsm.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "kernels.h"
+
+namespace eig {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int LDA_S = BM + 4;  // sA[k][m]: k-major, m contiguous (+4 complex pad -> conflict free)
+constexpr int LDB_S = BK + 2;  // sB[n][k]: n-major, k contiguous (+2 complex pad)
+constexpr int SA_ELEMS = BK * LDA_S;
+constexpr int SB_ELEMS = BN * LDB_S;
+constexpr int STAGE_ELEMS = SA_ELEMS + SB_ELEMS;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double2);
+
+struct Params {
+  int64_t M, N, K;
+  const double2 *A;
+  int64_t lda;
+  const double2 *B;
+  int64_t ldb;
+  double2 *C;
+  int64_t ldc;
+  double alpha, beta;
+  double2 *part;   // split-K partials [split][M*N] (ld M), or nullptr
+  int64_t kchunk;  // K per split (multiple of BK)
+  int tiles_m;
+};
+
+template <int OPA, int OPB, bool HERM, bool LOWER>
+__global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
+  extern __shared__ __align__(16) double2 smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+
+  int tm, tn;
+  if (LOWER) {
+    const int64_t x = blockIdx.x;
+    int64_t I = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
+    while ((I + 1) * (I + 2) / 2 <= x) I++;
+    while (I * (I + 1) / 2 > x) I--;
+    tm = (int)I;
+    tn = (int)(x - I * (I + 1) / 2);
+  } else {
+    tm = blockIdx.x % p.tiles_m;
+    tn = blockIdx.x / p.tiles_m;
+  }
+  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+  const int64_t kbeg = (int64_t)blockIdx.y * p.kchunk;
+  const int64_t kend = min(p.K, kbeg + p.kchunk);
+  const int nk = (int)((kend - kbeg + BK - 1) / BK);
+
+  auto load = [&](int stage, int64_t k0) {
+    double2 *sA = smem + stage * STAGE_ELEMS;
+    double2 *sB = sA + SA_ELEMS;
+    int mode;  // 0: A[m,k]; 1: A[k,m] (conj applied at fragment time); 2: Hermitian diagonal-crossing
+    if (HERM)
+      mode = (k0 + BK - 1 <= m0) ? 0 : ((k0 >= m0 + BM) ? 1 : 2);
+    else
+      mode = (OPA == OP_C) ? 1 : 0;
+#pragma unroll
+    for (int r = 0; r < (BM * BK) / THREADS; r++) {
+      const int i = tid + r * THREADS;
+      int m, k;
+      if (mode == 1) {
+        k = i % BK;
+        m = i / BK;
+      } else {
+        m = i % BM;
+        k = i / BM;
+      }
+      const int64_t gm = m0 + m, gk = k0 + k;
+      const bool valid = gm < p.M && gk < kend;
+      const double2 *src;
+      if (mode == 0)
+        src = p.A + gm + gk * p.lda;
+      else if (mode == 1)
+        src = p.A + gk + gm * p.lda;
+      else
+        src = (gm >= gk) ? p.A + gm + gk * p.lda : p.A + gk + gm * p.lda;
+      cp_async16(&sA[k * LDA_S + m], valid ? src : p.A, valid);
+    }
+#pragma unroll
+    for (int r = 0; r < (BN * BK) / THREADS; r++) {
+      const int i = tid + r * THREADS;
+      int n, k;
+      const double2 *src;
+      if (OPB == OP_N) {
+        k = i % BK;
+        n = i / BK;
+      } else {
+        n = i % BN;
+        k = i / BN;
+      }
+      const int64_t gn = n0 + n, gk = k0 + k;
+      const bool valid = gn < p.N && gk < kend;
+      src = (OPB == OP_N) ? p.B + gk + gn * p.ldb : p.B + gn + gk * p.ldb;
+      cp_async16(&sB[n * LDB_S + k], valid ? src : p.B, valid);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const LaneEmb le(lane);
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; s++) {
+    if (s < nk) load(s, kbeg + (int64_t)s * BK);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < nk; kt++) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + STAGES - 1;
+      if (nxt < nk) load(nxt % STAGES, kbeg + (int64_t)nxt * BK);
+      cp_async_commit();
+    }
+    const int st = kt % STAGES;
+    bool conjA = (OPA == OP_C);
+    if (HERM) {
+      const int64_t k0 = kbeg + (int64_t)kt * BK;
+      if (k0 >= m0 + BM) {
+        conjA = true;
+      } else if (k0 + BK - 1 <= m0) {
+        conjA = false;
+      } else {
+        conjA = false;
+        double2 *sA = smem + st * STAGE_ELEMS;
+        for (int i = tid; i < BM * BK; i += THREADS) {
+          const int m = i % BM, k = i / BM;
+          const int64_t gm = m0 + m, gk = k0 + k;
+          double2 v = sA[k * LDA_S + m];
+          if (gm < gk) v.y = -v.y;
+          else if (gm == gk) v.y = 0.0;
+          sA[k * LDA_S + m] = v;
+        }
+        __syncthreads();
+      }
+    }
+    const double *a = reinterpret_cast<const double *>(smem + st * STAGE_ELEMS);
+    const double *b = reinterpret_cast<const double *>(smem + st * STAGE_ELEMS + SA_ELEMS);
+    const unsigned anm = conjA ? le.a_neg_conj : le.a_neg;
+    const unsigned bnm = (OPB == OP_C) ? le.b_neg_conj : 0u;
+#pragma unroll
+    for (int ks = 0; ks < BK / 2; ks++) {
+      const int kk = ks * 2 + ((lane & 3) >> 1);
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int mm = wm * 16 + i * 4 + (lane >> 3);
+        af[i] = xsign(a[(kk * LDA_S + mm) * 2 + le.a_comp], anm);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int nn = wn * 32 + j * 8 + (lane >> 2);
+        bf[j] = xsign(b[(nn * LDB_S + kk) * 2 + le.b_comp], bnm);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: pair lanes (lane, lane^4) hold (Re, Im) rows of the same complex row
+  const int rp = (lane >> 2) & 1;
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const double send = rp ? acc[i][j][0] : acc[i][j][1];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, 4);
+      const double2 v = rp ? make_double2(recv, acc[i][j][1]) : make_double2(acc[i][j][0], recv);
+      const int64_t gm = m0 + wm * 16 + i * 4 + (lane >> 3);
+      const int64_t gn = n0 + wn * 32 + j * 8 + (lane & 3) * 2 + rp;
+      if (gm < p.M && gn < p.N) {
+        if (p.part) {
+          p.part[(int64_t)blockIdx.y * p.M * p.N + gm + gn * p.M] = v;
+        } else {
+          if (LOWER && gm < gn) continue;
+          double2 out = make_double2(p.alpha * v.x, p.alpha * v.y);
+          double2 *cp = p.C + gm + gn * p.ldc;
+          if (p.beta != 0.0) {
+            const double2 c = *cp;
+            out.x += p.beta * c.x;
+            out.y += p.beta * c.y;
+          }
+          if (LOWER && gm == gn) out.y = 0.0;
+          *cp = out;
+        }
+      }
+    }
+}
+
+// C = alpha * sum_z part[z] + beta * C  (fixed summation order -> deterministic)
+__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int split, const double2 *__restrict__ part, double2 *C,
+                                     int64_t ldc, double alpha, double beta, int lower) {
+  const int64_t total = M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t gm = e % M, gn = e / M;
+    if (lower && gm < gn) continue;
+    double2 s = part[e];
+    for (int z = 1; z < split; z++) {
+      const double2 t = part[(int64_t)z * total + e];
+      s.x += t.x;
+      s.y += t.y;
+    }
+    double2 out = make_double2(alpha * s.x, alpha * s.y);
+    double2 *cp = C + gm + gn * ldc;
+    if (beta != 0.0) {
+      const double2 c = *cp;
+      out.x += beta * c.x;
+      out.y += beta * c.y;
+    }
+    if (lower && gm == gn) out.y = 0.0;
+    *cp = out;
+  }
+}
+
+template <int OPA, int OPB, bool HERM, bool LOWER>
+int launch_t(Ctx &ctx, const Params &p, dim3 grid) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    EIG_TRY(ctx.check(cudaFuncSetAttribute(zgemm_kernel<OPA, OPB, HERM, LOWER>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES),
+                      "zgemm attr"));
+    attr_done = true;
+  }
+  zgemm_kernel<OPA, OPB, HERM, LOWER><<<grid, THREADS, SMEM_BYTES, ctx.stream>>>(p);
+  return ctx.launched("zgemm_kernel");
+}
+
+}  // namespace
+
+int zgemm(Ctx &ctx, const Zgemm &g) {
+  if (g.M <= 0 || g.N <= 0) return 0;
+  if (g.K <= 0 && g.beta == 1.0) return 0;  // K = 0 otherwise runs the epilogue only: C = beta C
+  if (g.herm_a && (g.opa != OP_N || g.M != g.K)) return -2;
+  if (g.lower_c && g.M != g.N) return -2;
+
+  const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
+  const int64_t tiles = g.lower_c ? (int64_t)tiles_m * (tiles_m + 1) / 2 : (int64_t)tiles_m * tiles_n;
+  const int64_t ktiles = std::max<int64_t>(1, (g.K + BK - 1) / BK);
+  int split = g.splitk;
+  if (split <= 0) {
+    const int64_t target = 2LL * ctx.num_sms;
+    split = 1;
+    if (tiles < target) {
+      int64_t want = (target + tiles - 1) / tiles;
+      int64_t maxs = std::max<int64_t>(1, ktiles / 4);
+      split = (int)std::min<int64_t>(want, maxs);
+    }
+  }
+  int64_t kt_per = (ktiles + split - 1) / split;
+  split = (int)((ktiles + kt_per - 1) / kt_per);
+
+  Params p;
+  p.M = g.M;
+  p.N = g.N;
+  p.K = std::max<int64_t>(g.K, 0);
+  p.A = g.A;
+  p.lda = g.lda;
+  p.B = g.B;
+  p.ldb = g.ldb;
+  p.C = g.C;
+  p.ldc = g.ldc;
+  p.alpha = g.alpha;
+  p.beta = g.beta;
+  p.kchunk = kt_per * BK;
+  p.tiles_m = tiles_m;
+  p.part = nullptr;
+  if (split > 1) {
+    p.part = (double2 *)ctx.ws(WS_PART, (size_t)split * g.M * g.N * sizeof(double2));
+    if (!p.part) return EIG_ERR_NOMEM;
+  }
+  dim3 grid((unsigned)tiles, (unsigned)split);
+  int rc;
+  if (g.herm_a)
+    rc = launch_t<OP_N, OP_N, true, false>(ctx, p, grid);
+  else if (g.lower_c) {
+    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, true>(ctx, p, grid);
+    else if (g.opa == OP_N && g.opb == OP_N) rc = launch_t<OP_N, OP_N, false, true>(ctx, p, grid);
+    else return -2;
+  } else if (g.opa == OP_N && g.opb == OP_N)
+    rc = launch_t<OP_N, OP_N, false, false>(ctx, p, grid);
+  else if (g.opa == OP_C && g.opb == OP_N)
+    rc = launch_t<OP_C, OP_N, false, false>(ctx, p, grid);
+  else if (g.opa == OP_N && g.opb == OP_C)
+    rc = launch_t<OP_N, OP_C, false, false>(ctx, p, grid);
+  else
+    rc = launch_t<OP_C, OP_C, false, false>(ctx, p, grid);
+  if (rc) return rc;
+  if (split > 1) {
+    const int64_t total = g.M * g.N;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8LL * ctx.num_sms);
+    splitk_reduce_kernel<<<blocks, 256, 0, ctx.stream>>>(g.M, g.N, split, p.part, g.C, g.ldc, g.alpha, g.beta,
+                                                          g.lower_c);
+    EIG_TRY(ctx.launched("splitk_reduce_kernel"));
+  }
+  return 0;
+}
+
+}  // namespace eig

@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on the same seeded inputs (marker: gpu).
+
+Tolerances: all paths are binary64; the CUDA kernels sum in a different
+order (DMMA, split-K, blocked reflectors), so elementwise errors are bounded
+by c * n * eps * ||.|| with c <= ~100 for these well-conditioned inputs;
+the tests use 1e-11 relative to the largest entry unless stated.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+gpu = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+def _solver(nb=64, g=0):
+    from paper_1207_1773_b200 import Solver
+    return Solver(0, nb=nb, q2_group=g)
+
+
+def _dev(x):
+    from paper_1207_1773_b200 import colmajor
+    return colmajor(x, torch.device("cuda:0"))
+
+
+def _rel(a, b):
+    return np.max(np.abs(np.asarray(a) - np.asarray(b))) / max(np.max(np.abs(b)), 1e-300)
+
+
+# ------------------------------------------------------------------ engine
+@gpu
+@pytest.mark.parametrize("opa,opb", [("N", "N"), ("C", "N"), ("N", "C"), ("C", "C")])
+@pytest.mark.parametrize("M,N,K", [(100, 70, 45), (64, 64, 16), (1, 130, 300), (257, 3, 129)])
+def test_zgemm_ops(opa, opb, M, N, K):
+    s = _solver()
+    A = synth.cnormal(1, 1, (M, K) if opa == "N" else (K, M))
+    B = synth.cnormal(1, 2, (K, N) if opb == "N" else (N, K))
+    C0 = synth.cnormal(1, 3, (M, N))
+    opA = A if opa == "N" else A.conj().T
+    opB = B if opb == "N" else B.conj().T
+    ref = -0.5 * opA @ opB + 1.0 * C0
+    dC = _dev(C0)
+    s.zgemm(opa, opb, _dev(A), _dev(B), dC, alpha=-0.5, beta=1.0, K=K)
+    assert _rel(dC.cpu().numpy(), ref) < TOL
+
+
+@gpu
+def test_zgemm_splitk_and_hermitian_and_lower():
+    s = _solver()
+    n, k = 333, 40
+    H = synth.rand_hermitian(n, 5)
+    Hs = np.tril(H) + np.triu(synth.cnormal(5, 9, (n, n)), 1)   # garbage above the diagonal
+    Hs[np.diag_indices(n)] += 1j * 7.0                           # imag(diag) must be ignored
+    V = synth.cnormal(5, 2, (n, k))
+    dW = _dev(np.zeros((n, k), complex))
+    s.zgemm("N", "N", _dev(Hs), _dev(V), dW, herm_a=True)
+    assert _rel(dW.cpu().numpy(), H @ V) < TOL
+    # lower-C her2k-style update leaves the strict upper triangle untouched
+    X = synth.cnormal(5, 3, (n, k))
+    C0 = synth.cnormal(5, 4, (n, n))
+    dC = _dev(C0)
+    VX = np.concatenate([V, X], axis=1)
+    XV = np.concatenate([X, V], axis=1)
+    s.zgemm("N", "C", _dev(VX), _dev(XV), dC, alpha=-1.0, beta=1.0, lower_c=True)
+    got = dC.cpu().numpy()
+    ref = C0 - V @ X.conj().T - X @ V.conj().T
+    low = np.tril(np.ones((n, n), bool), -1)
+    assert _rel(got[low], ref[low]) < TOL
+    assert np.array_equal(np.triu(got, 1), np.triu(C0, 1))
+    assert np.allclose(np.diag(got).real, np.diag(ref).real, rtol=0, atol=1e-12) and np.all(np.diag(got).imag == 0)
+    # skinny K-long product -> automatic split-K
+    Y = _dev(np.zeros((k, k), complex))
+    s.zgemm("C", "N", _dev(V), _dev(X), Y)
+    assert _rel(Y.cpu().numpy(), V.conj().T @ X) < TOL
+
+
+# ------------------------------------------------------------------ he2hb
+def _check_he2hb(n, nb, seed=0, gen="rand"):
+    s = _solver(nb=nb)
+    if gen == "rand":
+        A = synth.rand_hermitian(n, seed)
+    else:
+        A, _, _ = synth.pencil_known(n, seed)
+    dA = _dev(A)
+    tau, T = s.he2hb(dA)
+    Ag = dA.cpu().numpy()
+    A_o, tau_o = oracle.he2hb(A, nb)
+    r, c = np.indices((n, n))
+    low = r >= c
+    assert _rel(Ag[low], A_o[low]) < TOL * max(1, n / 256)
+    from paper_1207_1773_b200 import num_panels
+    K = num_panels(n, nb)
+    tg = tau.cpu().numpy()[:K * nb]
+    if K > 0:
+        assert np.max(np.abs(tg - tau_o[:K * nb])) < TOL * max(1, n / 256)
+    # T_k vs the oracle's larft on the oracle's V_k
+    Tg = T.cpu().numpy()[:K * nb * nb].reshape(K, nb, nb).transpose(0, 2, 1)   # column-major blocks
+    for k in range(K):
+        r0 = (k + 1) * nb
+        V = np.tril(A_o[r0:, k * nb:(k + 1) * nb], -1)
+        for j in range(min(nb, n - r0)):
+            V[j, j] = 1
+        T_o = oracle.larft(V, tau_o[k * nb:(k + 1) * nb])
+        assert _rel(Tg[k], T_o) < 1e-10
+    return A, Ag, tau, T
+
+
+@gpu
+@pytest.mark.parametrize("n,nb", [(256, 16), (300, 32), (517, 64), (130, 64), (65, 64), (64, 64), (97, 8)])
+def test_he2hb_parity(n, nb):
+    _check_he2hb(n, nb)
+
+
+@gpu
+def test_he2hb_parity_structured_known_spectrum():
+    _check_he2hb(200, 16, seed=3, gen="known")
+
+
+@gpu
+def test_he2hb_diagonal_input_is_noop():
+    s = _solver(nb=16)
+    n = 100
+    D = np.diag(synth.uniform(1, 1, n)).astype(complex)
+    dA = _dev(D)
+    tau, T = s.he2hb(dA)
+    assert np.array_equal(np.tril(dA.cpu().numpy()), D)
+    assert np.all(tau.cpu().numpy() == 0)
+
+
+# ------------------------------------------------------------------ Q1
+@gpu
+@pytest.mark.parametrize("n,nb,m", [(256, 16, 256), (300, 32, 37), (517, 64, 130)])
+def test_apply_q1_parity(n, nb, m):
+    s = _solver(nb=nb)
+    A = synth.rand_hermitian(n, 1)
+    A_o, tau_o = oracle.he2hb(A, nb)
+    from paper_1207_1773_b200 import num_panels
+    K = num_panels(n, nb)
+    Ts = np.zeros((K, nb, nb), complex)
+    for k in range(K):
+        r0 = (k + 1) * nb
+        V = np.tril(A_o[r0:, k * nb:(k + 1) * nb], -1)
+        for j in range(min(nb, n - r0)):
+            V[j, j] = 1
+        Ts[k] = oracle.larft(V, tau_o[k * nb:(k + 1) * nb])
+    T_flat = torch.from_numpy(Ts.transpose(0, 2, 1).reshape(-1).copy()).cuda()
+    E0 = synth.cnormal(2, 2, (n, m))
+    dE = _dev(E0)
+    s.apply_q1(_dev(A_o), T_flat, dE)
+    assert _rel(dE.cpu().numpy(), oracle.apply_q1(A_o, tau_o, nb, E0)) < TOL
+
+
+# ------------------------------------------------------------------ Q2
+@gpu
+@pytest.mark.parametrize("n,nb,g,m", [(256, 16, 8, 256), (300, 32, 16, 70), (517, 64, 32, 130), (100, 64, 32, 5),
+                                      (40, 8, 4, 64)])
+def test_apply_q2_parity_synthetic(n, nb, g, m):
+    s = _solver(nb=nb, g=g)
+    V2, tau2 = synth.synthetic_v2(n, nb, 4)
+    Z = synth.real_orthonormalish(n, m, 4)
+    from paper_1207_1773_b200 import empty_colmajor
+    dE = empty_colmajor(n, m)
+    s.apply_q2(torch.from_numpy(V2).cuda(), torch.from_numpy(tau2).cuda(), dE, Z=_dev(Z))
+    ref = oracle.apply_q2(V2, tau2, nb, Z.astype(complex))
+    assert _rel(dE.cpu().numpy(), ref) < TOL
+
+
+@gpu
+def test_apply_q2_parity_real_bulge_chase_reflectors():
+    n, nb, g = 150, 16, 8
+    A = synth.rand_hermitian(n, 9)
+    A_o, _ = oracle.he2hb(A, nb)
+    r, c = np.indices((n, n))
+    Bl = np.where((r - c >= 0) & (r - c <= nb), A_o, 0)
+    Band = np.tril(Bl) + np.tril(Bl, -1).conj().T
+    d, e, V2, tau2 = oracle.hb2st(Band, nb)
+    E0 = synth.cnormal(9, 1, (n, 40))
+    s = _solver(nb=nb, g=g)
+    dE = _dev(E0)
+    s.apply_q2(torch.from_numpy(np.ascontiguousarray(V2)).cuda(), torch.from_numpy(tau2).cuda(), dE)
+    assert _rel(dE.cpu().numpy(), oracle.apply_q2(V2, tau2, nb, E0)) < TOL
+
+
+# ------------------------------------------------------------------ trsm
+@gpu
+@pytest.mark.parametrize("n,m", [(256, 256), (300, 7), (517, 130), (64, 64), (1, 3)])
+def test_trsm_lh_parity(n, m):
+    s = _solver()
+    B = synth.hpd_with_condition(n, 1e2, 3) if n > 1 else np.array([[4.0 + 0j]])
+    L, info = oracle.potrf(B)
+    assert info == 0
+    E0 = synth.cnormal(3, 3, (n, m))
+    dE = _dev(E0)
+    s.trsm_lh(_dev(L), dE)
+    assert _rel(dE.cpu().numpy(), oracle.backsub_lh(L, E0)) < TOL
+
+
+# ------------------------------------------------------------------ whole pass
+@gpu
+@pytest.mark.parametrize("n,nb,g,m", [(256, 16, 8, 256), (600, 64, 32, 60)])
+def test_hotpath_parity(n, nb, g, m):
+    s = _solver(nb=nb, g=g)
+    A = synth.rand_hermitian(n, 11)
+    V2, tau2 = synth.synthetic_v2(n, nb, 11)
+    L = synth.unit_lower(n, 11)
+    Z = synth.real_orthonormalish(n, m, 11)
+    dA = _dev(A)
+    E, tau1, T1 = s.hotpath(dA, torch.from_numpy(V2).cuda(), torch.from_numpy(tau2).cuda(), _dev(L), _dev(Z))
+    A_o, tau_o = oracle.he2hb(A, nb)
+    E_o = oracle.backsub_lh(L, oracle.apply_q1(A_o, tau_o, nb, oracle.apply_q2(V2, tau2, nb, Z.astype(complex))))
+    assert _rel(E.cpu().numpy(), E_o) < TOL
+    # the same pass through the C ABI with HOST buffers
+    Eh = np.zeros((n, m), complex, order="F")
+    s.hotpath_host(np.asfortranarray(A), V2, tau2, np.asfortranarray(L), np.asfortranarray(Z), Eh)
+    assert _rel(Eh, E_o) < TOL
