@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path: one step = he2hb of the
+standard-form matrix + complexify + Q2 + Q1 + L^-H on the m eigenvector columns.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Metric (BASELINE.json): FP64 TFLOP/s of he2hb + back-transform, nominal flops
+16/3 n^3 + 20 n^2 m (8 real flops per complex multiply-add), workload n = 10000,
+m = 10000 (configs[3]).  N > 1: he2hb on rank 0, factors broadcast over NCCL,
+back-transform sharded by eigenvector column slices (strong scaling).
+Inputs (1.6 GB each) exceed L2 (126 MB), so no explicit L2 flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 TFLOP/s he2hb+back-transform; zhegv seconds n=10k at 1/2/4/8 B200"
+DMMA_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+
+
+def nominal_flops(n, m):
+    return 16.0 / 3.0 * n ** 3 + 20.0 * n * n * m
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--n", type=int, default=10000)
+    p.add_argument("--m", type=int, default=None)
+    p.add_argument("--nb", type=int, default=64)
+    p.add_argument("--g", type=int, default=32)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
+    a = p.parse_args()
+    if a.m is None:
+        a.m = a.n
+    return a
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip() == "Active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dmma_peak():
+    try:
+        d = json.load(open(DMMA_PEAK_FILE))
+        return float(d["dmma_tflops_sustained"]), "measured DMMA (profiles/fp64_peak_r01.json)"
+    except Exception:
+        return 37.0, "fallback datasheet FP64 tensor"
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def cpu_sample(n, nb, seed, budget):
+    """The oracle as it stands, on a bounded sample of the same workload:
+    the first r he2hb reflectors of A' (n x n) and c eigenvector columns through
+    Q2, Q1, L^-H.  Returns (TFLOP/s, cores, description)."""
+    import oracle
+    import synth
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    A = synth.rand_hermitian(n, seed)
+    Ah = oracle.full_hermitian(A)
+    # he2hb sample
+    r = 4
+    t0 = time.perf_counter()
+    oracle.he2hb_partial(Ah, nb, r)
+    t_he = time.perf_counter() - t0
+    fl_he = sum(16.0 * (n - nb - j) ** 2 for j in range(r))
+    # BT sample
+    c = max(1, min(cores, 8))
+    V2, tau2 = synth.synthetic_v2(n, nb, seed)
+    A1, tau1 = synth.synthetic_v1(n, nb, seed)
+    L = synth.unit_lower(n, seed)
+    Z = synth.real_orthonormalish(n, c, seed).astype(complex)
+    t0 = time.perf_counter()
+    E = oracle.apply_q2(V2, tau2, nb, Z)
+    E = oracle.apply_q1(A1, tau1, nb, E)
+    E = oracle.backsub_lh(L, E)
+    t_bt = time.perf_counter() - t0
+    fl_bt = 20.0 * n * n * c
+    value = (fl_he + fl_bt) / (t_he + t_bt) / 1e12
+    desc = (f"oracle on n={n}: first {r} he2hb reflectors ({t_he:.1f} s) + {c} eigenvector columns through "
+            f"Q2,Q1,L^-H ({t_bt:.1f} s); nominal flops of the sample / time")
+    return value, cores, desc, t_he + t_bt
+
+
+def run_reference(a, rank, world):
+    if rank != 0:
+        return 0
+    vals = []
+    cores, desc = 0, ""
+    for i in range(a.warmup + a.steps):
+        v, cores, desc, _ = cpu_sample(a.n, a.nb, a.seed, a.cpu_budget)
+        if i >= a.warmup:
+            vals.append(v)
+    v = statistics.mean(vals)
+    line = {"metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "higher_is_better": True, "impl": "reference", "dtype": "f64",
+            "data": "synthetic", "scaling": "strong", "vs_baseline": None,
+            "config": {"workload": f"he2hb+BT n={a.n} m={a.m} nb={a.nb} (oracle sample)", "n": a.n, "m": a.m},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(a, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_1207_1773_b200 import Solver, colmajor, empty_colmajor, num_panels, v2_slots
+    from paper_1207_1773_b200.dist import column_slice, hotpath_sharded
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n, m, nb = a.n, a.m, a.nb
+    K = num_panels(n, nb)
+    slots = v2_slots(n, nb)
+    lo, hi = column_slice(m, rank, world)
+    ml = hi - lo
+
+    t_gen = time.perf_counter()
+    if rank == 0:
+        A_h = synth.rand_hermitian(n, a.seed)
+        V2_h, tau2_h = synth.synthetic_v2(n, nb, a.seed)
+        L_h = synth.unit_lower(n, a.seed)
+        A0 = colmajor(A_h, dev)
+        V2 = torch.from_numpy(V2_h).to(dev)
+        tau2 = torch.from_numpy(tau2_h).to(dev)
+        L = colmajor(L_h, dev)
+    else:
+        A_h = V2_h = tau2_h = L_h = None
+        A0 = empty_colmajor(n, n, device=dev)
+        V2 = torch.empty((max(slots, 1), nb), dtype=torch.complex128, device=dev)
+        tau2 = torch.empty(max(slots, 1), dtype=torch.complex128, device=dev)
+        L = empty_colmajor(n, n, device=dev)
+    Z_h = synth.real_orthonormalish(n, ml, a.seed, col0=lo)
+    Z = colmajor(Z_h, dev)
+    E = empty_colmajor(n, ml, device=dev)
+    A = empty_colmajor(n, n, device=dev)
+    tau1 = torch.zeros(max(K * nb, 1), dtype=torch.complex128, device=dev)
+    T1 = torch.zeros(max(K * nb * nb, 1), dtype=torch.complex128, device=dev)
+    t_gen = time.perf_counter() - t_gen
+
+    solver = Solver(local_rank, nb=nb, q2_group=a.g)
+    stream = solver.stream
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    stage_names = ["he2hb", "q2", "q1", "trsm"]
+
+    def step(events=None):
+        if world == 1:
+            if events:
+                events[0].record(stream)
+            A.copy_(A0)
+            tau_, T_ = solver.he2hb(A)
+            if events:
+                events[1].record(stream)
+            solver.apply_q2(V2, tau2, E, Z=Z)
+            if events:
+                events[2].record(stream)
+            solver.apply_q1(A, T_, E)
+            if events:
+                events[3].record(stream)
+            solver.trsm_lh(L, E)
+            if events:
+                events[4].record(stream)
+        else:
+            if events:
+                events[0].record(stream)
+            if rank == 0:
+                A.copy_(A0)
+            hotpath_sharded(solver, A, tau1, T1, V2, tau2, L, Z, E)
+            if events:
+                events[4].record(stream)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = solver.launches
+    t_start, t_end = ev(), ev()
+    step_events = [[ev() for _ in range(5)] for _ in range(a.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start.record(stream)
+    for s in range(a.steps):
+        step(step_events[s])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = solver.launches - launches0
+    clk = clocks.stop()
+    ms_total = t_start.elapsed_time(t_end)
+    if world > 1:
+        tt = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / a.steps
+    stages = {}
+    if world == 1:
+        for k, nm in enumerate(stage_names):
+            stages[nm] = statistics.mean(step_events[s][k].elapsed_time(step_events[s][k + 1])
+                                         for s in range(a.steps))
+    flops = nominal_flops(n, m)
+    value = flops / (ms_step * 1e-3) / 1e12
+
+    # roofline of the dominant kernel (per-stage events; Q2 is one kernel launch)
+    peak, peak_src = dmma_peak()
+    roof = None
+    if stages:
+        stage_flops = {"he2hb": 16.0 / 3.0 * n ** 3, "q2": 8.0 * n * n * m, "q1": 8.0 * n * n * m,
+                       "trsm": 4.0 * n * n * m}
+        kern = {"he2hb": "zgemm_kernel (hemm+her2k) + panel_qr_kernel", "q2": "apply_q2_kernel",
+                "q1": "zgemm_kernel", "trsm": "zgemm_kernel"}
+        dom = max(stages, key=stages.get)
+        ach = stage_flops[dom] / (stages[dom] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": kern[dom], "stage": dom, "achieved": ach, "peak": peak,
+                "unit": "TFLOP/s", "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+                "stage_tflops": {k: stage_flops[k] / (stages[k] * 1e-3) / 1e12 for k in stages}}
+
+    # e2e through the C ABI with HOST buffers (pinned), N = 1
+    e2e = None
+    if rank == 0 and world == 1 and not a.no_e2e:
+        def pinned(shape_cols, ld, dtype):
+            return torch.empty((shape_cols, ld), dtype=dtype, pin_memory=True)
+
+        Ap = pinned(n, n, torch.complex128)
+        Ap.numpy()[:] = A_h.T
+        Lp = pinned(n, n, torch.complex128)
+        Lp.numpy()[:] = L_h.T
+        Zp = pinned(m, n, torch.float64)
+        Zp.numpy()[:] = Z_h.T
+        V2p = torch.from_numpy(V2_h).pin_memory()
+        t2p = torch.from_numpy(tau2_h).pin_memory()
+        Ep = pinned(m, n, torch.complex128)
+        e_steps = max(1, min(a.steps, 3))
+        solver.hotpath_host(Ap.numpy().T, V2p.numpy(), t2p.numpy(), Lp.numpy().T, Zp.numpy().T, Ep.numpy().T)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            solver.hotpath_host(Ap.numpy().T, V2p.numpy(), t2p.numpy(), Lp.numpy().T, Zp.numpy().T, Ep.numpy().T)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / e_steps
+        h2d = n * n * 16 * 2 + slots * nb * 16 + slots * 16 + n * m * 8
+        d2h = n * m * 16
+        e2e = {"value": flops / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": dt * 1e3, "steps": e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        v, cores, desc, secs = cpu_sample(n, nb, a.seed, a.cpu_budget)
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded SplitMix64; G1 Hermitian A', random unitary V2, well-conditioned L, real Z)",
+                "config": {"workload": f"he2hb+BT n={n} m={m} nb={nb} g={a.g}", "n": n, "m": m, "nb": nb,
+                           "q2_group": a.g, "parallelism": f"bt-columns{world}" if world > 1 else "single",
+                           "zhegv_seconds_hotpath": ms_step * 1e-3,
+                           "l2": "inputs (1.6 GB each) exceed L2; no flush needed",
+                           "input_gen_s": round(t_gen, 1)},
+                "stages_ms": stages, "gpu_launches": launches,
+                "gpu_launches_per_step": launches / max(a.steps, 1), "roofline": roof, "clocks": clk,
+                "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    solver.close()
+    return 0
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    rc = run_b200(a, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -51,6 +51,7 @@ def lib():
             "orc_jacobi": (I, [I, P, I, P, P, I]),
             "orc_solve_gen": (I, [I, P, I, P, I, I, I, P, P, I]),
             "orc_he2hb": (None, [I, I, P, I, P]),
+            "orc_he2hb_partial": (None, [I, I, P, I, P, I]),
             "orc_larft": (None, [I, I, P, I, P, P, I]),
             "orc_apply_q1": (None, [I, I, I, P, I, P, P, I]),
             "orc_v2_slots": (I, [I, I]),
@@ -204,6 +205,15 @@ def he2hb(A_full, nb):
     n = A.shape[0]
     tau = np.zeros(max(n, 1), dtype=np.complex128)
     lib().orc_he2hb(n, nb, _p(A), n, _p(tau))
+    return A, tau
+
+
+def he2hb_partial(A_full, nb, max_reflectors):
+    """orc_he2hb stopped after max_reflectors reflectors (bench CPU sample)."""
+    A = _z(A_full).copy(order="F")
+    n = A.shape[0]
+    tau = np.zeros(max(n, 1), dtype=np.complex128)
+    lib().orc_he2hb_partial(n, nb, _p(A), n, _p(tau), max_reflectors)
     return A, tau
 
 

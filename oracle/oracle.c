@@ -453,13 +453,25 @@ int64_t orc_solve_gen(int64_t n, const zc *A, int64_t lda, zc *B, int64_t ldb, i
  * its unit head) is stored below the band (r - c > nb) in the panel
  * columns, tau[k*nb + j] the tau of panel k column j (0 if absent).
  * Q1 = prod_k (H_{k,0} ... H_{k,nb-1}); Band = Q1^H A Q1 (reading R6). */
-void orc_he2hb(int64_t n, int64_t nb, zc *A, int64_t lda, zc *tau) {
+static void he2hb_impl(int64_t n, int64_t nb, zc *A, int64_t lda, zc *tau, int64_t max_refl);
+
+void orc_he2hb(int64_t n, int64_t nb, zc *A, int64_t lda, zc *tau) { he2hb_impl(n, nb, A, lda, tau, -1); }
+
+/* The same loop stopped after max_refl reflectors (bench.py's bounded CPU
+ * sample of the he2hb workload; no arithmetic changes). */
+void orc_he2hb_partial(int64_t n, int64_t nb, zc *A, int64_t lda, zc *tau, int64_t max_refl) {
+  he2hb_impl(n, nb, A, lda, tau, max_refl);
+}
+
+static void he2hb_impl(int64_t n, int64_t nb, zc *A, int64_t lda, zc *tau, int64_t max_refl) {
   zc *v = (zc *)malloc(sizeof(zc) * (n > 0 ? n : 1));
+  int64_t done = 0;
   for (int64_t i = 0; i + nb < n; i += nb) {
     int64_t pn = n - i - nb;                         /* panel rows        */
     int64_t nref = pn < nb ? pn : nb;
     for (int64_t j = 0; j < nb; j++) tau[i + j] = 0;
     for (int64_t j = 0; j < nref; j++) {
+      if (max_refl >= 0 && done++ >= max_refl) { free(v); return; }
       int64_t c = i + j, r0 = i + nb + j, len = n - r0;
       zc alpha = A[IX(r0, c, lda)], t;
       orc_larfg(len, &alpha, &A[IX(r0 + 1, c, lda)], 1, &t);

@@ -1,0 +1,65 @@
+"""Multi-GPU back-transform driver: one process per GPU,
+eigenvector columns sharded in contiguous slices, he2hb on rank 0.
+
+Every back-transform step acts on the columns of Z independently (S:L469,
+"column-block parallelism"), so rank r owns columns
+[floor(r m / P), floor((r+1) m / P)) and the only exchange is the broadcast of
+the read-only factors from rank 0 (he2hb's A = band + V1 and T1, the bulge
+chase reflectors V2/tau2, and L) over NCCL (NVLink / NVSwitch).  E stays
+distributed (optionally gathered).  The compute is the single-GPU C-ABI path
+(`Solver`); this module only does plumbing with torch.distributed.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def column_slice(m: int, rank: int, world: int):
+    """Contiguous, balanced slice [lo, hi) of m columns owned by `rank`."""
+    return (m * rank) // world, (m * (rank + 1)) // world
+
+
+def broadcast_factors(tensors, src: int = 0, group=None):
+    """Broadcast the read-only factors from `src` (in place, list order).
+    One collective per tensor; NCCL pipelines them on its stream."""
+    for t in tensors:
+        dist.broadcast(t, src=src, group=group)
+
+
+def hotpath_sharded(solver, A, tau1, T1, V2, tau2, L, Z_slice, E_slice, group=None):
+    """One pass of the hot path with the back-transform sharded by columns.
+
+    rank 0: he2hb(A) (a1..a5).  All ranks: receive A (band + V1), T1, V2, tau2,
+    L from rank 0, then E_slice = L^-H Q1 Q2 complex(Z_slice) (a6..a8).
+    `solver` is a paper_1207_1773_b200.Solver (or any object with the same
+    methods, e.g. a CPU stand-in in the gloo tests).  Returns E_slice."""
+    rank = dist.get_rank(group)
+    if rank == 0:
+        tau1_, T1_ = solver.he2hb(A)
+        tau1.copy_(tau1_)
+        T1.copy_(T1_)
+    broadcast_factors([A, T1, V2, tau2, L], src=0, group=group)
+    solver.apply_q2(V2, tau2, E_slice, Z=Z_slice)
+    solver.apply_q1(A, T1, E_slice)
+    solver.trsm_lh(L, E_slice)
+    return E_slice
+
+
+def gather_columns(E_slice: torch.Tensor, m: int, group=None):
+    """Gather the column slices to every rank (column-major n x m result)."""
+    world = dist.get_world_size(group)
+    n = E_slice.shape[0]
+    parts = []
+    for r in range(world):
+        lo, hi = column_slice(m, r, world)
+        parts.append(torch.empty((hi - lo, n), dtype=E_slice.dtype, device=E_slice.device))
+    mine = E_slice.t().contiguous()
+    # all_gather needs equal sizes: pad to the largest slice
+    mx = max(p.shape[0] for p in parts)
+    pad = torch.zeros((mx, n), dtype=E_slice.dtype, device=E_slice.device)
+    pad[: mine.shape[0]] = mine
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    cols = [bufs[r][: parts[r].shape[0]] for r in range(world)]
+    return torch.cat(cols, dim=0).t()

@@ -39,22 +39,23 @@ def uniform(seed: int, stream: int, count: int, start: int = 0) -> np.ndarray:
     return ((z >> np.uint64(11)).astype(np.float64) + 1.0) * (1.0 / 9007199254740992.0)
 
 
-def cnormal(seed: int, stream: int, shape, chunk: int = 1 << 24) -> np.ndarray:
-    """Complex N(0, 1/2) + i N(0, 1/2) entries, Fortran order (Box-Muller)."""
+def cnormal(seed: int, stream: int, shape, chunk: int = 1 << 24, start: int = 0) -> np.ndarray:
+    """Complex N(0, 1/2) + i N(0, 1/2) entries, Fortran order (Box-Muller).
+    `start` offsets the element counter (a column slice of a larger matrix)."""
     count = int(np.prod(shape))
     out = np.empty(count, dtype=np.complex128)
     for s in range(0, count, chunk):
         k = min(chunk, count - s)
-        u = uniform(seed, stream, 2 * k, 2 * s)
+        u = uniform(seed, stream, 2 * k, 2 * (s + start))
         r = np.sqrt(-np.log(u[0::2]))
         th = 2.0 * np.pi * u[1::2]
         out[s:s + k] = r * np.cos(th) + 1j * (r * np.sin(th))
     return out.reshape(shape, order="F")
 
 
-def rnormal(seed: int, stream: int, shape) -> np.ndarray:
+def rnormal(seed: int, stream: int, shape, start: int = 0) -> np.ndarray:
     """Real N(0,1) entries, Fortran order."""
-    return np.sqrt(2.0) * cnormal(seed, stream, shape).real
+    return np.sqrt(2.0) * cnormal(seed, stream, shape, start=start).real
 
 
 def hermitian_full(M: np.ndarray) -> np.ndarray:
@@ -153,10 +154,28 @@ def unit_lower(n: int, seed: int = 0, stream: int = 30, offscale: float = 0.5) -
     return np.asfortranarray(L)
 
 
-def real_orthonormalish(n: int, m: int, seed: int = 0, stream: int = 40) -> np.ndarray:
+def real_orthonormalish(n: int, m: int, seed: int = 0, stream: int = 40, col0: int = 0) -> np.ndarray:
     """Real n x m matrix with N(0, 1/n) entries (stand-in for tridiagonal
-    eigenvectors Z in the timed step; columns have norm ~1)."""
-    return np.asfortranarray(rnormal(seed, stream, (n, m)) / np.sqrt(n))
+    eigenvectors Z in the timed step; columns have norm ~1).  col0 selects
+    columns col0..col0+m-1 of the same global matrix (column slices)."""
+    return np.asfortranarray(rnormal(seed, stream, (n, m), start=col0 * n) / np.sqrt(n))
+
+
+def synthetic_v1(n: int, nb: int, seed: int = 0, stream: int = 60):
+    """Random exactly-unitary reflectors in the he2hb layout (band entries
+    untouched, v tails below the band, tau = (1+e^{i theta})/|v|^2): the shape
+    of the Q1 workload for the CPU baseline sample.  Returns (A, tau)."""
+    A = np.asfortranarray(cnormal(seed, stream, (n, n)) / np.sqrt(n))
+    tau = np.zeros(max(n, 1), dtype=np.complex128)
+    th = 2.0 * np.pi * uniform(seed, stream + 1, n)
+    i = 0
+    while i + nb < n:
+        for j in range(min(nb, n - i - nb)):
+            r0 = i + nb + j
+            nrm2 = 1.0 + np.sum(np.abs(A[r0 + 1:, i + j]) ** 2)
+            tau[i + j] = (1.0 + np.exp(1j * th[i + j])) / nrm2
+        i += nb
+    return A, tau
 
 
 def v2_layout(n: int, nb: int):
