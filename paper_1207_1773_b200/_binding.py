@@ -59,6 +59,7 @@ def lib():
             "eig_hotpath": (C.c_int, [h, I, P, I, P, P, P, P, P, I, P, I, P, I, I, U]),
             "eig_zgemm": (C.c_int, [h, C.c_char, C.c_char, I, I, I, D, P, I, P, I, D, P, I, C.c_int, C.c_int]),
             "eig_solve_gen": (C.c_int, [h, I, P, I, P, I, C.c_int, D, I, I, P, P, I, P]),
+            "eig_debug_q2_profile": (C.c_int, [h, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -71,7 +72,7 @@ def lib():
 def exported_symbols():
     return ["eig_init", "eig_finalize", "eig_strerror", "eig_last_cuda_error", "eig_launch_count", "eig_sync",
             "eig_num_panels", "eig_v2_slots", "eig_he2hb", "eig_apply_q1", "eig_apply_q2", "eig_trsm_lh",
-            "eig_hotpath", "eig_zgemm", "eig_solve_gen"]
+            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile"]
 
 
 def num_panels(n: int, nb: int) -> int:
@@ -150,6 +151,12 @@ class Solver:
     @property
     def launches(self) -> int:
         return int(lib().eig_launch_count(self.h))
+
+    def q2_profile(self):
+        """Cycles of CTA 0 in apply_q2 phases (load, A, B, C, commit); needs EIG_Q2_PROFILE."""
+        out = (C.c_ulonglong * 5)()
+        self._check(lib().eig_debug_q2_profile(self.h, C.cast(out, C.c_void_p)))
+        return list(out)
 
     def sync(self):
         self._check(lib().eig_sync(self.h))

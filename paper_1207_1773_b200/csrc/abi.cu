@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -256,8 +257,18 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
   if (!bar) { delete x; return EIG_ERR_NOMEM; }
   rc = x->c.check(cudaMemset(bar, 0, 64), "barrier init");
   if (rc) { delete x; return rc; }
+  if (getenv("EIG_Q2_PROFILE")) {
+    x->c.q2_prof = (unsigned long long *)x->c.ws(WS_Q2PROF, 64);
+    if (x->c.q2_prof) cudaMemset(x->c.q2_prof, 0, 64);
+  }
   *h = x;
   return 0;
+}
+
+int eig_debug_q2_profile(eig_handle h, unsigned long long *out5) {
+  if (!h) return EIG_ERR_STATE;
+  if (!h->c.q2_prof) return EIG_ERR_NOTIMPL;
+  return h->c.check(cudaMemcpy(out5, h->c.q2_prof, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "prof");
 }
 
 int eig_finalize(eig_handle h) {

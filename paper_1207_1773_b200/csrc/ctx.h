@@ -23,6 +23,7 @@ enum WsId {
   WS_LINV,        // trsm: inverted diagonal blocks
   WS_T2,          // Q2 T factors
   WS_Q2PLAN,      // Q2 plan tables
+  WS_Q2PROF,      // debug counters
   WS_HOST_A, WS_HOST_V2, WS_HOST_TAU2, WS_HOST_L, WS_HOST_Z, WS_HOST_E, WS_HOST_TAU1, WS_HOST_T1,
   WS_COUNT
 };
@@ -34,6 +35,7 @@ struct Ctx {
   int q2g = 32;
   int num_sms = 148;
   int64_t launches = 0;
+  unsigned long long *q2_prof = nullptr;  // debug: device counters for apply_q2 phases (EIG_Q2_PROFILE)
   std::string last_err;
   void *buf[WS_COUNT] = {};
   size_t bytes[WS_COUNT] = {};

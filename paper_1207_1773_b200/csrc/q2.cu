@@ -30,7 +30,7 @@
 namespace eig {
 namespace {
 
-constexpr int QT = 256;
+constexpr int QT = 512;   // 16 warps: 8 reflector/row groups x 2 column halves
 constexpr int NFMAX = 9;           // 8-column fragments per slab
 constexpr int QBN = NFMAX * 8;     // 72 columns
 constexpr int LDV = 36;            // Vd row stride (complex), == 4 mod 8
@@ -49,6 +49,7 @@ struct Q2Args {
   const double2 *T2;
   double2 *E;
   int nfr_total;         // ceil(m / 8)
+  unsigned long long *prof;  // optional: CTA 0 phase cycle counters [5] (load, A, B, C, commit)
 };
 
 struct Smem {
@@ -66,171 +67,304 @@ __device__ __forceinline__ double2 c_pair(const double (&c)[2], int rp) {
   return rp ? make_double2(recv, c[1]) : make_double2(c[0], recv);
 }
 
-template <int NF>
-__device__ void q2_slab(const Q2Args &a, const Smem &s, int64_t c0, int ncols) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const LaneEmb le(lane);
-  const int rp = (lane >> 2) & 1;
-  const int nb = a.nb, g = a.g, W = a.W, Wp = a.Wp;
-  const int wu = __shfl_sync(0xffffffffu, warp, 0);   // provably warp-uniform copy of the warp id
-  const double *vd = reinterpret_cast<const double *>(s.Vd);
-  const double *se = reinterpret_cast<const double *>(s.E);
-  const double *sy = reinterpret_cast<const double *>(s.Y);
-  const double *st = reinterpret_cast<const double *>(s.T);
-  const int nmfA = g / 4;            // reflector groups of 4
-  const int nmfC = Wp / 4;           // row groups of 4
+// Window rows live in a ring of R = W slots (row q of the block starting at
+// ring offset `base` is slot (q + base) mod R), so sliding the window by nb
+// rows needs no data movement: block j+1's nb new rows overwrite the slots of
+// block j's first nb rows, which phase C writes straight to global memory.
+__device__ __forceinline__ int ring(int q, int base, int R) {
+  int r = q + base;
+  return r >= R ? r - R : r;
+}
 
-  for (int64_t gi = a.ngroups - 1; gi >= 0; gi--) {
-    const int64_t i0 = gi * g;
-    const int64_t J = q2_steps(a.n, nb, i0);
-    for (int64_t j = 0; j < J; j++) {
-      const int64_t rs = i0 + 1 + j * nb;
-      const int64_t blk = a.first[gi] + j;
-      // ---------------- loads: live V entries, T, new window rows
-      {
-        const int64_t last_i = a.n - 2 - j * nb;
-        const int64_t nvalid = imax64(0, imin64(g, last_i - i0 + 1));
-        const double2 *src = a.V2 + (a.off[j] + i0) * nb;
-        for (int e = tid; e < g * nb; e += QT) {
-          const int t = e / nb, sidx = e - t * nb;
-          const bool ok = t < nvalid;
-          cp_async16(&s.Vd[(t + sidx) * LDV + t], ok ? src + e : a.V2, ok);
-        }
-        const double2 *tsrc = a.T2 + blk * g * g;
-        for (int e = tid; e < g * g; e += QT) {
-          const int x = e % g, y = e / g;
-          cp_async16(&s.T[y * LDT + x], tsrc + e, true);
-        }
-        const int rfirst = (j == 0) ? 0 : g - 1;
-        const int nload = Wp - rfirst;
-        for (int e = tid; e < NF * 8 * nload; e += QT) {
-          const int q = rfirst + e % nload, c = e / nload;
-          const int64_t row = rs + q;
-          const bool ok = (q < W) && (row < a.n) && (c < ncols);
-          cp_async16(&s.E[c * LDE + q], ok ? a.E + row + (c0 + c) * a.lde : a.E, ok);
-        }
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-      }
-      // ---------------- phase A: Y = V^H E_win
-      if (warp < nmfA) {
-        double acc[NF][2];
+// Phase A for one warp: Y[t, cols] = sum_q conj(V[q][t]) E[q, cols] over the
+// nb/2+2 k-steps where reflectors 4mw..4mw+3 are nonzero.
+template <int NFH>
+__device__ __forceinline__ void phase_a(const double *vd, const double *se, double2 *sY, int mw, int nlo, int nb,
+                                        int base, int R, int lane, const LaneEmb &le, int rp) {
+  double acc[NFH][2];
 #pragma unroll
-        for (int jj = 0; jj < NF; jj++) acc[jj][0] = acc[jj][1] = 0.0;
-        const int t = wu * 4 + (lane >> 3);
-        const int ks0 = wu * 2, nks = nb / 2 + 2;
-        const int kq = (lane & 3) >> 1;
-        for (int ks = ks0; ks < ks0 + nks; ks++) {
-          const int q = ks * 2 + kq;
-          const double av = xsign(vd[(q * LDV + t) * 2 + le.a_comp], le.a_neg_conj);
+  for (int jj = 0; jj < NFH; jj++) acc[jj][0] = acc[jj][1] = 0.0;
+  const int t = mw * 4 + (lane >> 3);
+  const int kq = (lane & 3) >> 1;
+  const int ks0 = mw * 2, nks = nb / 2 + 2;
+  int q = ks0 * 2 + kq;
+  int r = ring(q, base, R);
+  const double *eb = se + le.b_comp + ((nlo * 8 + (lane >> 2)) * LDE) * 2;
+  // software pipeline: fragments of k-step ks+1 are loaded while ks computes
+  double fa = xsign(vd[(q * LDV + t) * 2 + le.a_comp], le.a_neg_conj);
+  double fb[NFH];
 #pragma unroll
-          for (int jj = 0; jj < NF; jj++) {
-            const int nn = jj * 8 + (lane >> 2);
-            dmma(acc[jj], av, se[(nn * LDE + q) * 2 + le.b_comp]);
-          }
-        }
+  for (int jj = 0; jj < NFH; jj++) fb[jj] = eb[(jj * 8 * LDE + r) * 2];
+  for (int ks = 0; ks < nks; ks++) {
+    q += 2;
+    r += 2;
+    if (r >= R) r -= R;
+    const bool more = ks + 1 < nks;
+    double na = 0.0, nbv[NFH];
+    if (more) na = xsign(vd[(q * LDV + t) * 2 + le.a_comp], le.a_neg_conj);
 #pragma unroll
-        for (int jj = 0; jj < NF; jj++) {
-          const double2 v = c_pair(acc[jj], rp);
-          const int nn = jj * 8 + (lane & 3) * 2 + rp;
-          s.Y[nn * LDY + t] = v;
-        }
-      }
-      __syncthreads();
-      // ---------------- phase B: Y = T Y   (T upper triangular)
-      {
-        double acc[NF][2];
+    for (int jj = 0; jj < NFH; jj++) nbv[jj] = more ? eb[(jj * 8 * LDE + r) * 2] : 0.0;
 #pragma unroll
-        for (int jj = 0; jj < NF; jj++) acc[jj][0] = acc[jj][1] = 0.0;
-        const bool act = warp < nmfA;
-        if (act) {
-          const int ra = warp * 4 + (lane >> 3);
-          const int kq = (lane & 3) >> 1;
-          for (int ks = wu * 2; ks < g / 2; ks++) {
-            const int kb = ks * 2 + kq;
-            const double av = st[(kb * LDT + ra) * 2 + le.a_comp];
-            const double avs = xsign(av, le.a_neg);
+    for (int jj = 0; jj < NFH; jj++) dmma(acc[jj], fa, fb[jj]);
+    fa = na;
 #pragma unroll
-            for (int jj = 0; jj < NF; jj++) {
-              const int nn = jj * 8 + (lane >> 2);
-              dmma(acc[jj], avs, sy[(nn * LDY + kb) * 2 + le.b_comp]);
-            }
-          }
-        }
-        __syncthreads();
-        if (act) {
-          const int ra = warp * 4 + (lane >> 3);
+    for (int jj = 0; jj < NFH; jj++) fb[jj] = nbv[jj];
+  }
 #pragma unroll
-          for (int jj = 0; jj < NF; jj++) {
-            const double2 v = c_pair(acc[jj], rp);
-            const int nn = jj * 8 + (lane & 3) * 2 + rp;
-            s.Y[nn * LDY + ra] = v;
-          }
-        }
-      }
-      __syncthreads();
-      // ---------------- phase C: E_win -= V Y
-      {
-        const int kq = (lane & 3) >> 1;
+  for (int jj = 0; jj < NFH; jj++) {
+    const double2 v = c_pair(acc[jj], rp);
+    sY[((nlo + jj) * 8 + (lane & 3) * 2 + rp) * LDY + t] = v;
+  }
+}
+
+// Phase B for one warp: Y2[t, cols] = sum_{k >= t} T[t][k] Y[k, cols] into
+// registers (nfh <= NFH fragments are live).
+template <int NFH>
+__device__ __forceinline__ void phase_b(const double *st, const double *sy, double (&acc)[NFH][2], int mw, int nlo,
+                                        int nfh, int g, int lane, const LaneEmb &le) {
+#pragma unroll
+  for (int jj = 0; jj < NFH; jj++) acc[jj][0] = acc[jj][1] = 0.0;
+  const int ra = mw * 4 + (lane >> 3);
+  const int kq = (lane & 3) >> 1;
+  const double *yb = sy + le.b_comp + ((nlo * 8 + (lane >> 2)) * LDY) * 2;
+#pragma unroll 2
+  for (int ks = mw * 2; ks < g / 2; ks++) {
+    const int kb = ks * 2 + kq;
+    const double av = xsign(st[(kb * LDT + ra) * 2 + le.a_comp], le.a_neg);
+#pragma unroll
+    for (int jj = 0; jj < NFH; jj++)
+      if (jj < nfh) dmma(acc[jj], av, yb[(jj * 8 * LDY + kb) * 2]);
+  }
+}
+
+// What phase C refills for the next block of the same group.
+struct NextBlk {
+  bool more;            // a next block exists in this group
+  int64_t rs1;          // its first window row
+  int base1;            // its ring offset
+  const double2 *v2;    // its V2 slots (slot t at v2 + t*nb)
+  int nvalid;           // live slots
+};
+
+// Phase C for one warp: E[q, cols] -= sum_t V[q][t] Y2[t, cols] for row groups
+// mw, mw+8, mw+16; rows q < nout leave the window and go straight to global.
+// As soon as the warp is done with a row group, it refills (cp.async) the
+// Vd rows of that group with the next block's V and, for rows q < nb, the
+// ring slots with the next block's new E rows; no other warp touches them
+// before the end-of-block barrier, so the loads overlap the rest of phase C.
+template <int NFH>
+__device__ __forceinline__ void phase_c(const Q2Args &a, double2 *sVd, const double *sy, double2 *sE, int mw,
+                                        int nlo, int h, int base, int R, int nout, int64_t rs, int64_t c0, int ncols,
+                                        int ncolsl, const NextBlk &nx, int lane, const LaneEmb &le, int rp) {
+  const int nb = a.nb, g = a.g, W = a.W, nmfC = a.Wp / 4;
+  const int kq = (lane & 3) >> 1;
+  const double *vd = reinterpret_cast<const double *>(sVd);
+  const double *yb = sy + le.b_comp + ((nlo * 8 + (lane >> 2)) * LDY) * 2;
 #pragma unroll 1
-        for (int i = 0; i < 3; i++) {
-          const int mf = wu + 8 * i;
-          if (mf >= nmfC) break;
-          const int q0 = mf * 4;
-          const int klo = max(0, q0 - nb + 1) >> 1, khi = min(g - 1, q0 + 3) >> 1;   // inclusive k-steps
-          double acc[NF][2];
+  for (int i = 0; i < 3; i++) {
+    const int mf = mw + 8 * i;
+    if (mf >= nmfC) break;
+    const int q0 = mf * 4;
+    const int klo = max(0, q0 - nb + 1) >> 1, khi = min(g - 1, q0 + 3) >> 1;
+    double acc[NFH][2];
 #pragma unroll
-          for (int jj = 0; jj < NF; jj++) acc[jj][0] = acc[jj][1] = 0.0;
-          const int q = q0 + (lane >> 3);
-          for (int ks = klo; ks <= khi; ks++) {
-            const int kt = ks * 2 + kq;
-            const double av = xsign(vd[(q * LDV + kt) * 2 + le.a_comp], le.a_neg);
+    for (int jj = 0; jj < NFH; jj++) acc[jj][0] = acc[jj][1] = 0.0;
+    const int q = q0 + (lane >> 3);
+    const double *vq = vd + le.a_comp + (q * LDV) * 2;
+    int kt = klo * 2 + kq;
+    double fa = xsign(vq[kt * 2], le.a_neg);
+    double fb[NFH];
 #pragma unroll
-            for (int jj = 0; jj < NF; jj++) {
-              const int nn = jj * 8 + (lane >> 2);
-              dmma(acc[jj], av, sy[(nn * LDY + kt) * 2 + le.b_comp]);
-            }
-          }
-          const int qo = q0 + (lane >> 3);
+    for (int jj = 0; jj < NFH; jj++) fb[jj] = yb[(jj * 8 * LDY + kt) * 2];
+    for (int ks = klo; ks <= khi; ks++) {
+      kt += 2;
+      const bool more = ks < khi;
+      double na = 0.0, nbv[NFH];
+      if (more) na = xsign(vq[kt * 2], le.a_neg);
 #pragma unroll
-          for (int jj = 0; jj < NF; jj++) {
-            const double2 v = c_pair(acc[jj], rp);
-            const int nn = jj * 8 + (lane & 3) * 2 + rp;
-            if (qo < W) {
-              double2 &ev = s.E[nn * LDE + qo];
-              ev.x -= v.x;
-              ev.y -= v.y;
-            }
-          }
+      for (int jj = 0; jj < NFH; jj++) nbv[jj] = more ? yb[(jj * 8 * LDY + kt) * 2] : 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NFH; jj++) dmma(acc[jj], fa, fb[jj]);
+      fa = na;
+#pragma unroll
+      for (int jj = 0; jj < NFH; jj++) fb[jj] = nbv[jj];
+    }
+    const bool live = q < W;
+    const int r = ring(q, base, R);
+    const int64_t row = rs + q;
+#pragma unroll
+    for (int jj = 0; jj < NFH; jj++) {
+      const double2 v = c_pair(acc[jj], rp);
+      const int nn = (nlo + jj) * 8 + (lane & 3) * 2 + rp;
+      if (live) {
+        double2 *ep = &sE[nn * LDE + r];
+        double2 ev = *ep;
+        ev.x -= v.x;
+        ev.y -= v.y;
+        if (q < nout) {
+          if (row < a.n && nn < ncols) a.E[row + (c0 + nn) * a.lde] = ev;
+        } else {
+          *ep = ev;
         }
       }
-      __syncthreads();
-      // ---------------- store rows leaving the window, shift the overlap
-      {
-        const bool lastj = (j == J - 1);
-        const int nstore = lastj ? W : nb;
-        for (int e = tid; e < NF * 8 * nstore; e += QT) {
-          const int q = e % nstore, c = e / nstore;
-          const int64_t row = rs + q;
-          if (row < a.n && c < ncols) a.E[row + (c0 + c) * a.lde] = s.E[c * LDE + q];
+    }
+    if (nx.more) {
+      // both column halves of this row group must be done before its slots are refilled
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + mw) : "memory");
+      // next block's V entries of rows q0..q0+3: Vd[qq][t] = v_t[qq - t]   (half 0)
+      if (h == 0)
+      for (int e = lane; e < 4 * g; e += 32) {
+        const int qq = q0 + e / g, t = e % g;
+        const int sidx = qq - t;
+        if (qq < W && sidx >= 0 && sidx < nb) {
+          const bool ok = t < nx.nvalid;
+          cp_async16(&sVd[qq * LDV + t], ok ? nx.v2 + t * nb + sidx : a.V2, ok);
         }
-        if (!lastj) {
-          __syncthreads();
-          for (int e = tid; e < NF * 8 * (g - 1); e += QT) {
-            const int q = e % (g - 1), c = e / (g - 1);
-            s.E[c * LDE + q] = s.E[c * LDE + nb + q];
+      }
+      // next block's new E rows land in the ring slots of rows q0..q0+3 (< nb)   (half 1)
+      if (h == 1 && q0 < nb) {
+        for (int e = lane; e < 4 * ncolsl; e += 32) {
+          const int qq = q0 + (e & 3), c = e >> 2;
+          if (qq < nb) {
+            const int64_t row1 = nx.rs1 + qq + g - 1;
+            const bool ok = (row1 < a.n) && (c < ncols);
+            cp_async16(&sE[c * LDE + ring(qq, base, R)], ok ? a.E + row1 + (c0 + c) * a.lde : a.E, ok);
           }
-        } else {
-          __threadfence();   // the next group re-reads these rows through L2
         }
-        __syncthreads();
       }
     }
   }
 }
 
-__global__ void __launch_bounds__(QT, 1) apply_q2_kernel(Q2Args a) {
+template <int NF>
+__device__ __forceinline__ void q2_slab(const Q2Args &a, const Smem &s, int64_t c0, int ncols) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int wu = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform warp id
+  const int mw = wu & 7, h = wu >> 3;
+  constexpr int NF0 = (NF + 1) / 2, NF1 = NF / 2, NF1c = NF1 > 0 ? NF1 : 1;
+  const int nlo = h ? NF0 : 0, nfh = h ? NF1 : NF0;
+  const LaneEmb le(lane);
+  const int rp = (lane >> 2) & 1;
+  const int nb = a.nb, g = a.g, W = a.W, R = a.W;
+  const double *vd = reinterpret_cast<const double *>(s.Vd);
+  const double *se = reinterpret_cast<const double *>(s.E);
+  const double *sy = reinterpret_cast<const double *>(s.Y);
+  const double *st = reinterpret_cast<const double *>(s.T);
+  const bool actAB = mw < g / 4 && nfh > 0;
+  constexpr int PV = (32 * 64 + QT - 1) / QT;          // prefetched V elements per thread (g <= 32)
+  const int ncolsl = NF * 8;
+  // element e = tid + k*QT of an (nb x *) array is (row e % nb, col e / nb): per-thread start and
+  // per-k increments, so the prefetch loops need no integer division
+  const int d_q = QT % nb, d_c = QT / nb;
+  const int q_0 = tid % nb, c_0 = tid / nb;
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && tid == 0;
+  long long t_mark = 0, t_acc[5] = {0, 0, 0, 0, 0};
+  auto mark = [&](int k) {
+    if (prof) {
+      const long long now = clock64();
+      if (k >= 0) t_acc[k] += now - t_mark;
+      t_mark = now;
+    }
+  };
+
+  for (int64_t gi = a.ngroups - 1; gi >= 0; gi--) {
+    const int64_t i0 = gi * g;
+    const int64_t J = q2_steps(a.n, nb, i0);
+    int base = 0;
+    for (int64_t j = 0; j < J; j++) {
+      const int64_t rs = i0 + 1 + j * nb;
+      const int64_t blk = a.first[gi] + j;
+      mark(-1);
+      if (j == 0) {
+        // group start: live V entries, T and the whole window, synchronously
+        const int64_t nvalid = imax64(0, imin64(g, a.n - 2 - i0 + 1));
+        const double2 *src = a.V2 + (a.off[0] + i0) * nb;
+        int qq = q_0, cc = c_0;
+        for (int k = 0; k < PV; k++) {
+          if (cc < g) {
+            const bool ok = cc < nvalid;
+            cp_async16(&s.Vd[(cc + qq) * LDV + cc], ok ? src + cc * nb + qq : a.V2, ok);
+          }
+          qq += d_q;
+          cc += d_c;
+          if (qq >= nb) { qq -= nb; cc++; }
+        }
+        const double2 *tsrc = a.T2 + blk * g * g;
+        for (int y = wu; y < g; y += QT / 32)
+          for (int x = lane; x < g; x += 32) cp_async16(&s.T[y * LDT + x], tsrc + y * g + x, true);
+        for (int c = wu; c < ncolsl; c += QT / 32)
+          for (int q = lane; q < W; q += 32) {
+            const int64_t row = rs + q;
+            const bool ok = (row < a.n) && (c < ncols);
+            cp_async16(&s.E[c * LDE + q], ok ? a.E + row + (c0 + c) * a.lde : a.E, ok);
+          }
+        cp_async_commit();
+      }
+      cp_async_wait<0>();
+      __syncthreads();
+      mark(0);
+      // ---------------- phase A: Y = V^H E_win
+      if (actAB) {
+        if (h == 0) phase_a<NF0>(vd, se, s.Y, mw, nlo, nb, base, R, lane, le, rp);
+        else phase_a<NF1c>(vd, se, s.Y, mw, nlo, nb, base, R, lane, le, rp);
+      }
+      __syncthreads();
+      mark(1);
+      // ---------------- phase B: Y = T Y
+      {
+        double acc[NF0][2];
+        if (actAB) phase_b<NF0>(st, sy, acc, mw, nlo, nfh, g, lane, le);
+        __syncthreads();
+        if (actAB) {
+          const int ra = mw * 4 + (lane >> 3);
+#pragma unroll
+          for (int jj = 0; jj < NF0; jj++) {
+            const double2 v = c_pair(acc[jj], rp);
+            if (jj < nfh) s.Y[((nlo + jj) * 8 + (lane & 3) * 2 + rp) * LDY + ra] = v;
+          }
+        }
+      }
+      __syncthreads();
+      mark(2);
+      // ---------------- phase C (+ refill for the next block of this group)
+      const bool more = (j + 1 < J);
+      NextBlk nx;
+      nx.more = more;
+      nx.rs1 = rs + nb;
+      nx.base1 = (base + nb) % R;
+      nx.v2 = more ? a.V2 + (a.off[j + 1] + i0) * nb : a.V2;
+      nx.nvalid = more ? (int)imax64(0, imin64(g, a.n - 2 - (j + 1) * nb - i0 + 1)) : 0;
+      if (more) {
+        const double2 *tsrc = a.T2 + (blk + 1) * g * g;
+        for (int y = wu; y < g; y += QT / 32)
+          for (int x = lane; x < g; x += 32) cp_async16(&s.T[y * LDT + x], tsrc + y * g + x, true);
+      }
+      if (h == 0)
+        phase_c<NF0>(a, s.Vd, sy, s.E, mw, nlo, h, base, R, more ? nb : W, rs, c0, ncols, ncolsl, nx, lane, le, rp);
+      else
+        phase_c<NF1c>(a, s.Vd, sy, s.E, mw, nlo, h, base, R, more ? nb : W, rs, c0, ncols, ncolsl, nx, lane, le, rp);
+      cp_async_commit();
+      mark(3);
+      if (more) {
+        base = nx.base1;
+      } else {
+        __threadfence();   // the next group re-reads these rows through L2
+      }
+      mark(4);
+    }
+  }
+  __syncthreads();
+  if (prof)
+    for (int k = 0; k < 5; k++) atomicAdd(&a.prof[k], (unsigned long long)t_acc[k]);
+}
+
+// Every CTA runs slabs of exactly NF fragments (one template instance per
+// launch keeps the register allocation of each NF separate); a CTA whose own
+// range is shorter computes the extra fragments on zero-filled columns and
+// never stores them, which costs nothing because the CTAs with the longest
+// range set the kernel time anyway.
+template <int NF>
+__global__ void __launch_bounds__(QT, 1) apply_q2_kernel(Q2Args a, int nslab) {
   extern __shared__ __align__(16) double2 sm[];
   Smem s;
   s.Vd = sm;
@@ -240,27 +374,14 @@ __global__ void __launch_bounds__(QT, 1) apply_q2_kernel(Q2Args a) {
   // the parallelogram's zeros never change: clear Vd once
   for (int e = threadIdx.x; e < WPMAX * LDV; e += QT) s.Vd[e] = czero();
   __syncthreads();
-  // balanced contiguous range of 8-column fragments for this CTA
   const int F = a.nfr_total, G = gridDim.x;
   const int f0 = (int)((int64_t)F * blockIdx.x / G), f1 = (int)((int64_t)F * (blockIdx.x + 1) / G);
-  const int nslab = (f1 - f0 + NFMAX - 1) / NFMAX;
   for (int sl = 0; sl < nslab; sl++) {
-    const int fa = f0 + (int)((int64_t)(f1 - f0) * sl / nslab), fb = f0 + (int)((int64_t)(f1 - f0) * (sl + 1) / nslab);
-    const int nf = fb - fa;
+    const int fa = f0 + sl * NF;
     const int64_t c0 = (int64_t)fa * 8;
-    const int ncols = (int)imin64((int64_t)nf * 8, a.m - c0);
-    switch (nf) {
-      case 1: q2_slab<1>(a, s, c0, ncols); break;
-      case 2: q2_slab<2>(a, s, c0, ncols); break;
-      case 3: q2_slab<3>(a, s, c0, ncols); break;
-      case 4: q2_slab<4>(a, s, c0, ncols); break;
-      case 5: q2_slab<5>(a, s, c0, ncols); break;
-      case 6: q2_slab<6>(a, s, c0, ncols); break;
-      case 7: q2_slab<7>(a, s, c0, ncols); break;
-      case 8: q2_slab<8>(a, s, c0, ncols); break;
-      case 9: q2_slab<9>(a, s, c0, ncols); break;
-      default: break;
-    }
+    const int ncols = (int)imin64(imin64((int64_t)(f1 - fa) * 8, a.m - c0), NF * 8);
+    if (ncols <= 0) break;
+    q2_slab<NF>(a, s, c0, ncols);
   }
 }
 
@@ -284,15 +405,27 @@ int q2_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, do
   a.T2 = T2;
   a.E = E;
   a.nfr_total = (int)((m + 7) / 8);
+  a.prof = ctx.q2_prof;
   const size_t smem = ((size_t)WPMAX * LDV + 32 * LDT + (size_t)QBN * LDE + (size_t)QBN * LDY) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                      "q2 attr"));
-    attr = true;
-  }
   const int grid = std::min(ctx.num_sms, a.nfr_total);
-  apply_q2_kernel<<<grid, QT, smem, ctx.stream>>>(a);
+  const int per = (a.nfr_total + grid - 1) / grid;        // fragments of the longest CTA range
+  const int nslab = (per + NFMAX - 1) / NFMAX;
+  const int nf = (per + nslab - 1) / nslab;
+  static bool attr[NFMAX + 1] = {};
+#define Q2_CASE(K)                                                                                          \
+  case K:                                                                                                   \
+    if (!attr[K]) {                                                                                         \
+      EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)smem), "q2 attr"));                                       \
+      attr[K] = true;                                                                                       \
+    }                                                                                                       \
+    apply_q2_kernel<K><<<grid, QT, smem, ctx.stream>>>(a, nslab);                                           \
+    break;
+  switch (nf) {
+    Q2_CASE(1) Q2_CASE(2) Q2_CASE(3) Q2_CASE(4) Q2_CASE(5) Q2_CASE(6) Q2_CASE(7) Q2_CASE(8) Q2_CASE(9)
+    default: return EIG_ERR_NOTIMPL;
+  }
+#undef Q2_CASE
   return ctx.launched("apply_q2_kernel");
 }
 

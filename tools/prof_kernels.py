@@ -75,6 +75,10 @@ def main():
         E.copy_(torch.randn(m, n, dtype=torch.complex128, device=dev).t())
         ms = timeit(lambda: s.apply_q2(V2d, t2d, E), a.reps)
         print(f"apply_q2 n={n} m={m} nb={a.nb} g={s.q2_group}: {ms:.3f} ms  {8.0 * n * n * m / ms / 1e9:.2f} TFLOP/s")
+        if os.environ.get("EIG_Q2_PROFILE"):
+            pr = s.q2_profile()
+            tot = sum(pr)
+            print("  CTA0 phase cycles (load, A, B, C, commit):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
     elif a.mode == "he2hb":
         A0 = colmajor(synth.rand_hermitian(n, 0), dev)
         A = A0.clone()
