@@ -135,10 +135,11 @@ int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void 
 int eig_zgemm(eig_handle h, char opa, char opb, int64_t M, int64_t N, int64_t K, double alpha, const void *A,
               int64_t lda, const void *B, int64_t ldb, double beta, void *C, int64_t ldc, int herm_a, int lower_c);
 
-/* Debug: cycles spent by CTA 0 of the last apply_q2 launches in its phases
- * (load, A, B, C, commit), accumulated; needs EIG_Q2_PROFILE set in the
- * environment at eig_init (else EIG_ERR_NOTIMPL).  out5: host array of 5. */
-int eig_debug_q2_profile(eig_handle h, unsigned long long *out5);
+/* Debug: cycles spent by CTA 0 of apply_q2 in its phases [0..4] (load, A,
+ * B, C, commit) and of panel_qr [8..13] (barrier, reduce, beta, update,
+ * partials, tail), accumulated since eig_init; needs EIG_Q2_PROFILE set in
+ * the environment at eig_init (else EIG_ERR_NOTIMPL).  out16: host array. */
+int eig_debug_q2_profile(eig_handle h, unsigned long long *out16);
 
 /* Generalized solver (Algorithm 1).  Needs the NEXT stages
  * (device hb2st, stedc, potrf/hegst); returns EIG_ERR_NOTIMPL in this build. */

@@ -153,8 +153,8 @@ class Solver:
         return int(lib().eig_launch_count(self.h))
 
     def q2_profile(self):
-        """Cycles of CTA 0 in apply_q2 phases (load, A, B, C, commit); needs EIG_Q2_PROFILE."""
-        out = (C.c_ulonglong * 5)()
+        """Cycles of CTA 0: apply_q2 phases [0:5], panel_qr phases [8:14]; needs EIG_Q2_PROFILE."""
+        out = (C.c_ulonglong * 16)()
         self._check(lib().eig_debug_q2_profile(self.h, C.cast(out, C.c_void_p)))
         return list(out)
 

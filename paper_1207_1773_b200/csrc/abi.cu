@@ -106,27 +106,70 @@ static int he2hb_run(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau, d
 }
 
 // ------------------------------------------------------------------ Q1
+// E <- Q1 E with Q1 = Q^(0) ... Q^(K-1), Q^(k) = I - V_k T_k V_k^H.
+// Panels are aggregated ga at a time (last group first):
+//   Q^(k0)...Q^(k0+ga-1) = I - V T V^H,  V = [V_k0 ... V_k0+ga-1] (unit lower
+//   trapezoidal from row (k0+1)nb),  T = [[T_a, -T_a (V_a^H V_b) T_b], [0, T_b]]
+// merged pairwise from the per-panel T_k with the Gram matrix V^H V, so each
+// pass over E is three GEMMs with K = ga*nb instead of nb.
 static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const double2 *T, double2 *E, int64_t lde,
                         int64_t m) {
   const int nb = c.nb;
   const int64_t K = num_panels(n, nb);
   if (K == 0 || m <= 0) return 0;
+  const int ga_max = std::max(1, 256 / nb);
+  const int kw = ga_max * nb;                       // aggregated width
   const int64_t ldv = n - nb;
-  double2 *Vb = (double2 *)c.ws(WS_V, (size_t)ldv * nb * sizeof(double2));
-  double2 *Y = (double2 *)c.ws(WS_Y, (size_t)nb * m * sizeof(double2));
-  double2 *Y2 = (double2 *)c.ws(WS_Y2, (size_t)nb * m * sizeof(double2));
-  if (!Vb || !Y || !Y2) return EIG_ERR_NOMEM;
-  for (int64_t k = K - 1; k >= 0; k--) {
-    const int64_t r0 = (k + 1) * nb, s = n - r0;
-    EIG_TRY(extract_v(c, A + r0 + k * nb * lda, lda, s, nb, Vb, ldv));
+  double2 *Vb = (double2 *)c.ws(WS_V, (size_t)ldv * kw * sizeof(double2));
+  double2 *Y = (double2 *)c.ws(WS_Y, (size_t)kw * m * sizeof(double2));
+  double2 *Y2 = (double2 *)c.ws(WS_Y2, (size_t)kw * m * sizeof(double2));
+  double2 *Tg = (double2 *)c.ws(WS_TAGG, (size_t)3 * kw * kw * sizeof(double2));
+  if (!Vb || !Y || !Y2 || !Tg) return EIG_ERR_NOMEM;
+  double2 *Gm = Tg + (size_t)kw * kw, *Tmp = Gm + (size_t)kw * kw;
+  const int64_t ngroups = (K + ga_max - 1) / ga_max;
+  for (int64_t gi = ngroups - 1; gi >= 0; gi--) {
+    const int64_t k0 = gi * ga_max;
+    const int ga = (int)std::min<int64_t>(ga_max, K - k0);
+    const int w = ga * nb;
+    const int64_t r0 = (k0 + 1) * nb, s = n - r0;
+    EIG_TRY(extract_v(c, A + r0 + k0 * nb * lda, lda, s, w, Vb, ldv));
     Zgemm g;
-    g.opa = OP_C; g.M = nb; g.N = m; g.K = s; g.A = Vb; g.lda = ldv; g.B = E + r0; g.ldb = lde; g.C = Y; g.ldc = nb;
+    const double2 *Tuse = T + k0 * nb * nb;
+    int ldt = nb;
+    if (ga > 1) {
+      // aggregated T: diagonal blocks T_k, off-diagonal blocks merged pairwise
+      EIG_TRY(c.check(cudaMemsetAsync(Tg, 0, (size_t)w * w * sizeof(double2), c.stream), "memset T"));
+      for (int p = 0; p < ga; p++)
+        EIG_TRY(c.check(cudaMemcpy2DAsync(Tg + (size_t)p * nb * w + p * nb, w * sizeof(double2),
+                                          T + (k0 + p) * nb * nb, nb * sizeof(double2), nb * sizeof(double2), nb,
+                                          cudaMemcpyDeviceToDevice, c.stream), "copy T"));
+      g = Zgemm();   // Gram = V^H V
+      g.opa = OP_C; g.M = w; g.N = w; g.K = s; g.A = Vb; g.lda = ldv; g.B = Vb; g.ldb = ldv; g.C = Gm; g.ldc = w;
+      EIG_TRY(zgemm(c, g));
+      for (int span = nb; span < w; span *= 2)
+        for (int p0 = 0; p0 + span < w; p0 += 2 * span) {
+          const int p1 = p0 + span, p2 = std::min(w, p1 + span);
+          // Tmp = T[p0:p1, p0:p1] G[p0:p1, p1:p2];  T[p0:p1, p1:p2] = -Tmp T[p1:p2, p1:p2]
+          g = Zgemm();
+          g.M = span; g.N = p2 - p1; g.K = span; g.A = Tg + (size_t)p0 * w + p0; g.lda = w;
+          g.B = Gm + (size_t)p1 * w + p0; g.ldb = w; g.C = Tmp; g.ldc = w;
+          EIG_TRY(zgemm(c, g));
+          g = Zgemm();
+          g.M = span; g.N = p2 - p1; g.K = p2 - p1; g.A = Tmp; g.lda = w; g.B = Tg + (size_t)p1 * w + p1; g.ldb = w;
+          g.C = Tg + (size_t)p1 * w + p0; g.ldc = w; g.alpha = -1.0;
+          EIG_TRY(zgemm(c, g));
+        }
+      Tuse = Tg;
+      ldt = w;
+    }
+    g = Zgemm();   // Y = V^H E
+    g.opa = OP_C; g.M = w; g.N = m; g.K = s; g.A = Vb; g.lda = ldv; g.B = E + r0; g.ldb = lde; g.C = Y; g.ldc = w;
     EIG_TRY(zgemm(c, g));
-    g = Zgemm();
-    g.M = nb; g.N = m; g.K = nb; g.A = T + k * nb * nb; g.lda = nb; g.B = Y; g.ldb = nb; g.C = Y2; g.ldc = nb;
+    g = Zgemm();   // Y2 = T Y
+    g.M = w; g.N = m; g.K = w; g.A = Tuse; g.lda = ldt; g.B = Y; g.ldb = w; g.C = Y2; g.ldc = w;
     EIG_TRY(zgemm(c, g));
-    g = Zgemm();
-    g.M = s; g.N = m; g.K = nb; g.A = Vb; g.lda = ldv; g.B = Y2; g.ldb = nb; g.C = E + r0; g.ldc = lde;
+    g = Zgemm();   // E -= V Y2
+    g.M = s; g.N = m; g.K = w; g.A = Vb; g.lda = ldv; g.B = Y2; g.ldb = w; g.C = E + r0; g.ldc = lde;
     g.alpha = -1.0; g.beta = 1.0;
     EIG_TRY(zgemm(c, g));
   }
@@ -258,17 +301,17 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
   rc = x->c.check(cudaMemset(bar, 0, 64), "barrier init");
   if (rc) { delete x; return rc; }
   if (getenv("EIG_Q2_PROFILE")) {
-    x->c.q2_prof = (unsigned long long *)x->c.ws(WS_Q2PROF, 64);
-    if (x->c.q2_prof) cudaMemset(x->c.q2_prof, 0, 64);
+    x->c.q2_prof = (unsigned long long *)x->c.ws(WS_Q2PROF, 256);
+    if (x->c.q2_prof) cudaMemset(x->c.q2_prof, 0, 256);
   }
   *h = x;
   return 0;
 }
 
-int eig_debug_q2_profile(eig_handle h, unsigned long long *out5) {
+int eig_debug_q2_profile(eig_handle h, unsigned long long *out16) {
   if (!h) return EIG_ERR_STATE;
   if (!h->c.q2_prof) return EIG_ERR_NOTIMPL;
-  return h->c.check(cudaMemcpy(out5, h->c.q2_prof, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "prof");
+  return h->c.check(cudaMemcpy(out16, h->c.q2_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "prof");
 }
 
 int eig_finalize(eig_handle h) {

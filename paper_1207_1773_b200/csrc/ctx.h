@@ -15,11 +15,11 @@ enum WsId {
   WS_PART,        // split-K partials
   WS_SMALL,       // nb x nb scratch (Mh, M)
   WS_PANEL_REC,   // panel reduction records
-  WS_PANEL_GRAM,  // panel Gram partials
   WS_BARRIER,     // grid barrier words
   WS_V,           // BT: explicit V_k
   WS_Y,           // BT: nb x m
   WS_Y2,          // BT: nb x m
+  WS_TAGG,        // BT: aggregated T (ga*nb)^2 + Gram + temp
   WS_LINV,        // trsm: inverted diagonal blocks
   WS_T2,          // Q2 T factors
   WS_Q2PLAN,      // Q2 plan tables
@@ -35,6 +35,7 @@ struct Ctx {
   int q2g = 32;
   int num_sms = 148;
   int64_t launches = 0;
+  unsigned long long bar_epoch = 0;  // panel arrival counter value after the last launch
   unsigned long long *q2_prof = nullptr;  // debug: device counters for apply_q2 phases (EIG_Q2_PROFILE)
   std::string last_err;
   void *buf[WS_COUNT] = {};

@@ -34,93 +34,133 @@ struct PanelArgs {
   int nb, nref, R, G;
   double2 *tau, *T, *vout, *vout2;
   int64_t ldv;
-  double2 *rec;    // [2][G][recw]
-  double2 *gram;   // [G][nb*nb] partials, then [nb*nb] final
-  unsigned *bar;   // [0] count, [1] generation
+  double2 *rec;                  // [2][G][recw]: s_l (l != j), sumsq at l = j, then row j
+  unsigned long long *cnt;       // monotonic arrival counter (never reset)
+  unsigned long long epoch0;     // counter value when this launch starts
+  unsigned long long *prof;      // optional: CTA 0 phase cycles [8..13]
 };
 
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned *vgen = bar + 1;
-    const unsigned gen = *vgen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
+// One column step costs one exchange: every CTA publishes, for the next pivot
+// column a_j (rows below j that it owns), s_l = sum conj(a_j[r]) P[r, l] for
+// all l != j, sum |a_j[r]|^2 (in slot j) and, if it owns row j, row j itself;
+// then it increments a monotonic counter.  After all G arrivals every CTA
+// reduces the records in a fixed order (deterministic) and derives
+//   beta, tau, v = (1, a_j / (alpha - beta)),
+//   w_l = v^H P[:, l] = P[j, l] + conj(scale) s_l              (l > j),
+//   y_i = V[:, i]^H v  = conj(V[j, i]) + scale conj(s_i)       (i < j),
+// so the trailing-column update and the T column
+//   T[0:j, j] = -tau_j T[0:j, 0:j] y   (zlarft, forward/columnwise)
+// need no second reduction.
 __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double2 sm[];
   const int nb = a.nb, R = a.R, G = a.G;
-  const int recw = 1 + 2 * nb;
+  const int recw = 2 * nb;
   double2 *sTau = sm;               // [nb]
-  double2 *sRed = sTau + nb;        // [recw]
-  double2 *sW = sRed + recw;        // [nb]
-  double2 *sP = sW + nb;            // [nb][max(R, 2nb)], column l at sP + l*R
-  __shared__ double2 s_tau, s_scale, s_alpha;
+  double2 *sRow = sTau + nb;        // [nb]   row j (owner's record)
+  double2 *sS = sRow + nb;          // [nb]   reduced s_l
+  double2 *sW = sS + nb;            // [nb]   w_l / y_i
+  double2 *sY = sW + nb;            // [nb]   y_i (T column)
+  double2 *sPart = sY + nb;         // [4][64]
+  double2 *sT = sPart + 4 * 64;     // [nb][nb] (CTA 0)
+  double2 *sP = sT + nb * nb;       // [nb][R], column l at sP + l*R
+  __shared__ double2 s_tau, s_scale;
   __shared__ double s_beta;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int g = blockIdx.x;
   const int64_t row0 = (int64_t)g * R;
   const int64_t left = a.pn - row0;
   const int rows = left <= 0 ? 0 : (left < R ? (int)left : R);
+  const int cl = tid & 63, rq = tid >> 6;          // column / row-quarter of this thread
+  const int R4 = (rows + 3) >> 2;
+  const int rlo = min(rows, rq * R4), rhi = min(rows, (rq + 1) * R4);
 
-  for (int e = tid; e < R * nb; e += PT) {
-    const int r = e % R, l = e / R;
-    sP[l * R + r] = (r < rows) ? a.P[(row0 + r) + (int64_t)l * a.lda] : czero();
-  }
+  for (int l = 0; l < nb; l++)
+    for (int r = tid; r < R; r += PT) sP[l * R + r] = (r < rows) ? a.P[(row0 + r) + (int64_t)l * a.lda] : czero();
+  if (g == 0)
+    for (int e = tid; e < nb * nb; e += PT) sT[e] = czero();
   __syncthreads();
 
-  auto partials = [&](int j) {
-    double2 *out = a.rec + ((int64_t)(j & 1) * G + g) * recw;
-    for (int t = warp; t < nb - j; t += PT / 32) {
-      double2 acc = czero();
-      if (t == 0) {
-        for (int r = lane; r < rows; r += 32)
-          if (row0 + r > j) {
-            const double2 v = sP[j * R + r];
-            acc.x += v.x * v.x + v.y * v.y;
-          }
-      } else {
-        const int l = j + t;
-        for (int r = lane; r < rows; r += 32)
-          if (row0 + r >= j) acc = cadd(acc, cmulc(sP[j * R + r], sP[l * R + r]));
-      }
-      acc = warp_sum2(acc);
-      if (lane == 0) __stcg(&out[t == 0 ? 0 : 1 + j + t], acc);
+  const bool prof = a.prof != nullptr && g == 0 && tid == 0;
+  long long tm = prof ? clock64() : 0, tacc[6] = {0, 0, 0, 0, 0, 0};
+  auto mark = [&](int k) {
+    if (prof) {
+      const long long now = clock64();
+      tacc[k] += now - tm;
+      tm = now;
     }
-    if (j >= row0 && j < row0 + rows)
-      for (int l = j + tid; l < nb; l += PT) __stcg(&out[1 + nb + l], sP[l * R + (j - row0)]);
   };
 
-  if (a.nref > 0) partials(0);
-  for (int j = 0; j < a.nref; j++) {
-    grid_barrier(a.bar, G);
-    const double2 *recs = a.rec + (int64_t)(j & 1) * G * recw;
-    // reduce: warp per entry, lanes over CTAs, fixed order
-    for (int t = warp; t < nb - j; t += PT / 32) {
-      const int idx = (t == 0) ? 0 : 1 + j + t;
-      double2 s = czero();
-      for (int q = lane; q < G; q += 32) s = cadd(s, __ldcg(&recs[(int64_t)q * recw + idx]));
-      s = warp_sum2(s);
-      if (lane == 0) sRed[idx] = s;
+  // publish the record for pivot column jn and arrive.  With look-ahead, only
+  // column jn has been updated by the previous reflector (column jp = jn-1,
+  // holding v); columns l > jn are stale and their dots are corrected with
+  //   s_l = s_l(stale) - conj(tau) w_l (a^H v)   and   P[jn,l] -= conj(tau) v[jn] w_l.
+  auto publish = [&](int jn, bool corr, double2 ctau) {
+    double2 acc = czero();
+    if (cl < nb) {
+      const double2 *aj = sP + jn * R, *pl = sP + cl * R;
+      for (int r = rlo; r < rhi; r++) {
+        if (row0 + r <= jn) continue;
+        const double2 x = aj[r];
+        if (cl == jn) acc.x += x.x * x.x + x.y * x.y;
+        else acc = cadd(acc, cmulc(x, pl[r]));
+      }
     }
-    const int owner = j / R;
-    for (int l = j + tid; l < nb; l += PT) sRed[1 + nb + l] = __ldcg(&recs[(int64_t)owner * recw + 1 + nb + l]);
+    sPart[rq * 64 + cl] = acc;
     __syncthreads();
+    double2 *out = a.rec + ((int64_t)(jn & 1) * G + g) * recw;
+    if (tid < nb) {
+      double2 t = cadd(cadd(sPart[tid], sPart[64 + tid]), cadd(sPart[128 + tid], sPart[192 + tid]));
+      if (corr && tid > jn) {
+        const int jp = jn - 1;
+        const double2 c1 = cadd(cadd(sPart[jp], sPart[64 + jp]), cadd(sPart[128 + jp], sPart[192 + jp]));
+        t = csub(t, cmul(ctau, cmul(sW[tid], c1)));
+      }
+      __stcg(&out[tid], t);
+    }
+    if (jn >= row0 && jn < row0 + rows)
+      for (int l = tid; l < nb; l += PT) {
+        double2 pv = sP[l * R + (jn - row0)];
+        if (corr && l > jn) pv = csub(pv, cmul(ctau, cmul(sP[(jn - 1) * R + (jn - row0)], sW[l])));
+        __stcg(&out[nb + l], pv);
+      }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(a.cnt, 1ull);
+  };
+
+  if (a.nref > 0) publish(0, false, czero());
+  mark(4);
+  for (int j = 0; j < a.nref; j++) {
     if (tid == 0) {
-      const double2 alpha = sRed[1 + nb + j];
-      const double xnorm2 = sRed[0].x;
+      const unsigned long long target = a.epoch0 + (unsigned long long)G * (j + 1);
+      while (ld_acquire_u64(a.cnt) < target) {
+      }
+    }
+    __syncthreads();
+    mark(0);
+    const double2 *recs = a.rec + (int64_t)(j & 1) * G * recw;
+    {
+      double2 acc = czero();
+      if (cl < nb)
+        for (int q = rq; q < G; q += 4) acc = cadd(acc, __ldcg(&recs[(int64_t)q * recw + cl]));
+      sPart[rq * 64 + cl] = acc;
+      const int owner = j / R;
+      if (tid < nb) sRow[tid] = __ldcg(&recs[(int64_t)owner * recw + nb + tid]);
+    }
+    __syncthreads();
+    if (tid < nb) sS[tid] = cadd(cadd(sPart[tid], sPart[64 + tid]), cadd(sPart[128 + tid], sPart[192 + tid]));
+    __syncthreads();
+    mark(1);
+    if (tid == 0) {
+      const double2 alpha = sRow[j];
+      const double xnorm2 = sS[j].x;
       double2 tau, scale;
       double beta;
       if (xnorm2 == 0.0 && alpha.y == 0.0) {
@@ -137,98 +177,89 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       s_tau = tau;
       s_scale = scale;
       s_beta = beta;
-      s_alpha = alpha;
       sTau[j] = tau;
     }
     __syncthreads();
-    const double2 tau = s_tau, scale = s_scale, alpha = s_alpha;
-    const double beta = s_beta;
-    for (int l = j + 1 + tid; l < nb; l += PT) {
-      const double2 pj = sRed[1 + nb + l];
-      const double2 d = csub(sRed[1 + l], cmulc(alpha, pj));   // dot_l - conj(alpha) P[j,l]
-      sW[l] = cadd(pj, cmulc(scale, d));                       // v^H P[:, l]
+    mark(2);
+    const double2 tau = s_tau, scale = s_scale;
+    const double2 ctau = cconj(tau);
+    if (tid < nb) {
+      if (tid > j) sW[tid] = cadd(sRow[tid], cmulc(scale, sS[tid]));                  // w_l = v^H P[:,l]
+      else if (tid < j) sY[tid] = cadd(cconj(sRow[tid]), cmul(scale, cconj(sS[tid])));  // y_i = V_i^H v
     }
     for (int r = tid; r < rows; r += PT) {
       const int64_t grow = row0 + r;
       if (grow > j) sP[j * R + r] = cmul(sP[j * R + r], scale);
-      else if (grow == j) sP[j * R + r] = make_double2(beta, 0.0);
+      else if (grow == j) sP[j * R + r] = make_double2(s_beta, 0.0);
     }
     __syncthreads();
-    const int ncols = nb - j - 1;
-    const double2 ctau = cconj(tau);
-    for (int e = tid; e < rows * ncols; e += PT) {
-      const int r = e % rows, l = j + 1 + e / rows;
-      const int64_t grow = row0 + r;
-      if (grow < j) continue;
-      const double2 v = (grow == j) ? make_double2(1.0, 0.0) : sP[j * R + r];
-      sP[l * R + r] = csub(sP[l * R + r], cmul(ctau, cmul(v, sW[l])));
+    const double2 *vj = sP + j * R;
+    const bool la = (j + 1 < a.nref);
+    if (la) {
+      // look-ahead: the next pivot column first, then publish it
+      const double2 cw = cmul(ctau, sW[j + 1]);
+      double2 *pl = sP + (j + 1) * R;
+      for (int r = tid; r < rows; r += PT) {
+        const int64_t grow = row0 + r;
+        if (grow < j) continue;
+        const double2 v = (grow == j) ? make_double2(1.0, 0.0) : vj[r];
+        pl[r] = csub(pl[r], cmul(v, cw));
+      }
+      __syncthreads();
+      mark(3);
+      publish(j + 1, true, ctau);
+      mark(4);
+    }
+    // bulk update of the remaining trailing columns (overlaps the other CTAs' exchange)
+    {
+      const int lo = la ? j + 2 : j + 1;
+      const int c = nb - lo;
+      if (c > 0) {
+        const int tpc = PT / c;                         // threads per column
+        const int lc = tid / tpc, part = tid - lc * tpc;
+        if (lc < c) {
+          const int l = lo + lc;
+          const int rb = (int)((int64_t)rows * part / tpc), re = (int)((int64_t)rows * (part + 1) / tpc);
+          const double2 cw = cmul(ctau, sW[l]);
+          double2 *pl = sP + l * R;
+          for (int r = rb; r < re; r++) {
+            const int64_t grow = row0 + r;
+            if (grow < j) continue;
+            const double2 v = (grow == j) ? make_double2(1.0, 0.0) : vj[r];
+            pl[r] = csub(pl[r], cmul(v, cw));
+          }
+        }
+      }
+    }
+    if (g == 0) {
+      // T column j: T[0:j, j] = -tau_j T[0:j, 0:j] y
+      if (tid < j) {
+        double2 acc = czero();
+        for (int l = tid; l < j; l++) acc = cadd(acc, cmul(sT[tid + l * nb], sY[l]));
+        sT[tid + j * nb] = make_double2(-(tau.x * acc.x - tau.y * acc.y), -(tau.x * acc.y + tau.y * acc.x));
+      }
+      if (tid == 0) sT[j + j * nb] = tau;
     }
     __syncthreads();
-    if (j + 1 < a.nref) partials(j + 1);
+    mark(5);
   }
 
   // write back the factored rows and the explicit unit-lower V
-  for (int e = tid; e < rows * nb; e += PT) {
-    const int r = e % rows, l = e / rows;
-    const int64_t grow = row0 + r;
-    const double2 p = sP[l * R + r];
-    a.P[grow + (int64_t)l * a.lda] = p;
-    const double2 v = (grow > l) ? p : (grow == l ? make_double2(1.0, 0.0) : czero());
-    a.vout[grow + (int64_t)l * a.ldv] = v;
-    if (a.vout2) a.vout2[grow + (int64_t)l * a.ldv] = v;
-  }
-  // Gram partials G[x][y] = sum_r conj(V[r,x]) V[r,y], x < y
-  {
-    double2 *out = a.gram + (int64_t)g * nb * nb;
-    for (int pidx = tid; pidx < nb * nb; pidx += PT) {
-      const int x = pidx % nb, y = pidx / nb;
-      double2 s = czero();
-      if (x < y) {
-        for (int r = 0; r < rows; r++) {
-          const int64_t grow = row0 + r;
-          if (grow < y) continue;
-          const double2 vy = (grow == y) ? make_double2(1.0, 0.0) : sP[y * R + r];
-          const double2 vx = sP[x * R + r];   // grow >= y > x: strictly below the diagonal
-          s = cadd(s, cmulc(vx, vy));
-        }
-      }
-      __stcg(&out[pidx], s);
+  for (int l = 0; l < nb; l++)
+    for (int r = tid; r < rows; r += PT) {
+      const int64_t grow = row0 + r;
+      const double2 p = sP[l * R + r];
+      a.P[grow + (int64_t)l * a.lda] = p;
+      const double2 v = (grow > l) ? p : (grow == l ? make_double2(1.0, 0.0) : czero());
+      a.vout[grow + (int64_t)l * a.ldv] = v;
+      if (a.vout2) a.vout2[grow + (int64_t)l * a.ldv] = v;
     }
-  }
-  grid_barrier(a.bar, G);
-  {
-    double2 *fin = a.gram + (int64_t)G * nb * nb;
-    const int per = (nb * nb + G - 1) / G;
-    for (int pidx = g * per + tid; pidx < min(nb * nb, (g + 1) * per); pidx += PT) {
-      double2 s = czero();
-      for (int q = 0; q < G; q++) s = cadd(s, __ldcg(&a.gram[(int64_t)q * nb * nb + pidx]));
-      __stcg(&fin[pidx], s);
-    }
-  }
-  grid_barrier(a.bar, G);
   if (g == 0) {
-    double2 *sG = sP;                // reuse: [nb][nb]
-    double2 *sT = sP + nb * nb;      // [nb][nb]
-    const double2 *fin = a.gram + (int64_t)G * nb * nb;
-    for (int pidx = tid; pidx < nb * nb; pidx += PT) {
-      sG[pidx] = __ldcg(&fin[pidx]);
-      sT[pidx] = czero();
-    }
-    __syncthreads();
-    for (int j = 0; j < a.nref; j++) {
-      const double2 tj = sTau[j];
-      if (tid < j) {
-        const int i = tid;
-        double2 s = czero();
-        for (int l = i; l < j; l++) s = cadd(s, cmul(sT[i + l * nb], sG[l + j * nb]));
-        sT[i + j * nb] = make_double2(-(tj.x * s.x - tj.y * s.y), -(tj.x * s.y + tj.y * s.x));
-      }
-      if (tid == 0) sT[j + j * nb] = tj;
-      __syncthreads();
-    }
-    for (int pidx = tid; pidx < nb * nb; pidx += PT) a.T[pidx] = sT[pidx];
+    for (int e = tid; e < nb * nb; e += PT) a.T[e] = sT[e];
     for (int l = tid; l < nb; l += PT) a.tau[l] = (l < a.nref) ? sTau[l] : czero();
   }
+  if (prof)
+    for (int k = 0; k < 6; k++) atomicAdd(&a.prof[8 + k], (unsigned long long)tacc[k]);
 }
 
 // Explicit unit-lower V (s x nb) from the he2hb storage of one panel.
@@ -254,15 +285,16 @@ __global__ void real_diag_kernel(int64_t n, double2 *A, int64_t lda) {
 int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau, double2 *T, double2 *vout,
              double2 *vout2, int64_t ldv) {
   if (pn <= 0) return 0;
+  if (nb > 64) return EIG_ERR_NOTIMPL;
   const int nref = (int)std::min<int64_t>(pn, nb);
   int G = (int)std::min<int64_t>(ctx.num_sms, (pn + nb - 1) / nb);
   G = std::max(G, 1);
   int R = (int)((pn + G - 1) / G);
   R = std::max(R, nb);
   G = (int)((pn + R - 1) / R);
-  const int recw = 1 + 2 * nb;
-  const size_t smem = ((size_t)nb * std::max(R, 2 * nb) + recw + 2 * nb) * sizeof(double2);
-  if (smem > 220 * 1024) return EIG_ERR_NOTIMPL;  // panel too tall for on-chip residency (n > ~24000)
+  const int recw = 2 * nb;
+  const size_t smem = ((size_t)5 * nb + 4 * 64 + (size_t)nb * nb + (size_t)nb * R) * sizeof(double2);
+  if (smem > 220 * 1024) return EIG_ERR_NOTIMPL;  // panel too tall for on-chip residency (n > ~20000 at nb=64)
   PanelArgs a;
   a.P = P;
   a.lda = lda;
@@ -277,9 +309,10 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   a.vout2 = vout2;
   a.ldv = ldv;
   a.rec = (double2 *)ctx.ws(WS_PANEL_REC, (size_t)2 * G * recw * sizeof(double2));
-  a.gram = (double2 *)ctx.ws(WS_PANEL_GRAM, (size_t)(G + 1) * nb * nb * sizeof(double2));
-  a.bar = (unsigned *)ctx.buf[WS_BARRIER];
-  if (!a.rec || !a.gram || !a.bar) return EIG_ERR_NOMEM;
+  a.cnt = (unsigned long long *)ctx.buf[WS_BARRIER];
+  a.epoch0 = ctx.bar_epoch;
+  a.prof = ctx.q2_prof;
+  if (!a.rec || !a.cnt) return EIG_ERR_NOMEM;
   static bool attr = false;
   if (!attr) {
     EIG_TRY(ctx.check(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024),
@@ -289,6 +322,7 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   void *args[] = {&a};
   EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel, dim3(G), dim3(PT), args, smem, ctx.stream),
                     "panel_qr_kernel launch"));
+  ctx.bar_epoch += (unsigned long long)G * nref;   // arrivals this launch performs
   return ctx.launched("panel_qr_kernel");
 }
 

@@ -76,7 +76,7 @@ def main():
         ms = timeit(lambda: s.apply_q2(V2d, t2d, E), a.reps)
         print(f"apply_q2 n={n} m={m} nb={a.nb} g={s.q2_group}: {ms:.3f} ms  {8.0 * n * n * m / ms / 1e9:.2f} TFLOP/s")
         if os.environ.get("EIG_Q2_PROFILE"):
-            pr = s.q2_profile()
+            pr = s.q2_profile()[:5]
             tot = sum(pr)
             print("  CTA0 phase cycles (load, A, B, C, commit):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
     elif a.mode == "he2hb":
@@ -88,6 +88,11 @@ def main():
             s.he2hb(A)
         ms = timeit(run, a.reps)
         print(f"he2hb n={n} nb={a.nb}: {ms:.3f} ms  {16.0 / 3.0 * n ** 3 / ms / 1e9:.2f} TFLOP/s")
+        if os.environ.get("EIG_Q2_PROFILE"):
+            pr = s.q2_profile()[8:14]
+            tot = sum(pr)
+            print("  panel CTA0 cycles (wait, reduce, beta, lookahead-col, publish, bulk+T):",
+                  [f"{x / tot * 100:.1f}%" for x in pr], f"{tot / 1.965e6 / (a.reps + 1):.1f} ms/run")
     s.close()
 
 
