@@ -58,24 +58,37 @@ static int64_t v2_slots(int64_t n, int nb) {
 }
 
 // ------------------------------------------------------------------ he2hb
+// Step k (panel i = k nb, trailing A22 = A[r0:, r0:], r0 = i + nb, s = n - r0):
+//   a1+a2  panel QR + T of A[r0:, i:i+nb]          (panel_qr, cooperative)
+//   a3     W = A22 V T                              (Hermitian-A GEMM, split-K)
+//   a4     M = T^H (V^H W),  X = W - 1/2 V M
+//   a5     A22 -= V X^H + X V^H (lower)
+// Look-ahead (Fig. 1: "(a) can be overlapped with (c)"): a5 is split
+// into (i) the next panel's nb columns and (ii) the rest; panel k+1 runs on a
+// high-priority side stream right after (i), concurrently with (ii).  The
+// [V | X | V] workspace is double-buffered by step parity.
 static int he2hb_run(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau, double2 *T) {
   const int nb = c.nb;
   const int64_t K = num_panels(n, nb);
   EIG_TRY(real_diag(c, n, A, lda));
   if (K == 0) return 0;
   const int64_t ldw = n - nb;
-  double2 *VXV = (double2 *)c.ws(WS_VXV, (size_t)ldw * 3 * nb * sizeof(double2));
+  const size_t vxv_elems = (size_t)ldw * 3 * nb;
+  double2 *VXV = (double2 *)c.ws(WS_VXV, 2 * vxv_elems * sizeof(double2));
   double2 *Wb = (double2 *)c.ws(WS_W, (size_t)ldw * nb * sizeof(double2));
   double2 *Sm = (double2 *)c.ws(WS_SMALL, (size_t)2 * nb * nb * sizeof(double2));
   if (!VXV || !Wb || !Sm) return EIG_ERR_NOMEM;
-  double2 *V = VXV, *X = VXV + ldw * nb, *V2 = VXV + 2 * ldw * nb;
+  auto buf = [&](int64_t k) { return VXV + (k & 1) * vxv_elems; };
+  {
+    double2 *b0 = buf(0);
+    EIG_TRY(panel_qr(c, A + nb, lda, n - nb, nb, tau, T, b0, b0 + 2 * ldw * nb, ldw, c.stream));
+  }
   for (int64_t k = 0; k < K; k++) {
     const int64_t i = k * nb, r0 = i + nb, s = n - r0;
-    double2 *P = A + r0 + i * lda;
     double2 *A22 = A + r0 + r0 * lda;
     double2 *Tk = T + k * nb * nb;
-    // a1 + a2: panel QR and T
-    EIG_TRY(panel_qr(c, P, lda, s, nb, tau + k * nb, Tk, V, V2, ldw));
+    double2 *V = buf(k), *X = buf(k) + ldw * nb;
+    if (k > 0) EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_join, 0), "wait panel"));
     Zgemm g;
     // a3: W = A22 V T
     g = Zgemm();
@@ -97,10 +110,30 @@ static int he2hb_run(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau, d
     g.alpha = -0.5; g.beta = 1.0;
     EIG_TRY(zgemm(c, g));
     // a5: A22 -= [V X] [X V]^H   (lower triangle)
-    g = Zgemm();
-    g.opb = OP_C; g.lower_c = 1; g.M = s; g.N = s; g.K = 2 * nb; g.A = VXV; g.lda = ldw; g.B = X; g.ldb = ldw;
-    g.C = A22; g.ldc = lda; g.alpha = -1.0; g.beta = 1.0;
-    EIG_TRY(zgemm(c, g));
+    if (k + 1 < K) {
+      // (i) the next panel's columns (rectangular s x nb, lower part)
+      g = Zgemm();
+      g.opb = OP_C; g.lower_c = 2; g.M = s; g.N = nb; g.K = 2 * nb; g.A = V; g.lda = ldw; g.B = X; g.ldb = ldw;
+      g.C = A22; g.ldc = lda; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+      // panel k+1 on the side stream, concurrent with (ii)
+      EIG_TRY(c.check(cudaEventRecord(c.ev_fork, c.stream), "fork"));
+      EIG_TRY(c.check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "fork wait"));
+      double2 *bn = buf(k + 1);
+      EIG_TRY(panel_qr(c, A + r0 + nb + r0 * lda, lda, s - nb, nb, tau + (k + 1) * nb, T + (k + 1) * nb * nb, bn,
+                       bn + 2 * ldw * nb, ldw, c.side));
+      EIG_TRY(c.check(cudaEventRecord(c.ev_join, c.side), "join"));
+      // (ii) the remaining trailing lower triangle
+      g = Zgemm();
+      g.opb = OP_C; g.lower_c = 1; g.M = s - nb; g.N = s - nb; g.K = 2 * nb; g.A = V + nb; g.lda = ldw;
+      g.B = X + nb; g.ldb = ldw; g.C = A22 + nb + nb * lda; g.ldc = lda; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+    } else {
+      g = Zgemm();
+      g.opb = OP_C; g.lower_c = 1; g.M = s; g.N = s; g.K = 2 * nb; g.A = V; g.lda = ldw; g.B = X; g.ldb = ldw;
+      g.C = A22; g.ldc = lda; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+    }
   }
   return 0;
 }
@@ -177,27 +210,40 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
 }
 
 // ------------------------------------------------------------------ trsm
+// E <- L^-H E, left-looking and two-level: outer 256-row blocks take
+// the bulk of the flops in one GEMM each (M = 256, K = n - I1), the 256 x 256
+// diagonal block is solved with 64-row steps using precomputed inverses of
+// the 64 x 64 diagonal blocks of L.
 static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2 *E, int64_t lde, int64_t m) {
   if (n <= 0 || m <= 0) return 0;
-  const int bs = 64;
+  const int bs = 64, BS = 256;
   const int64_t nblk = (n + bs - 1) / bs;
   double2 *Linv = (double2 *)c.ws(WS_LINV, (size_t)nblk * bs * bs * sizeof(double2));
   if (!Linv) return EIG_ERR_NOMEM;
   EIG_TRY(trinv_blocks(c, n, bs, L, ldl, Linv));
-  for (int64_t I = nblk - 1; I >= 0; I--) {
-    const int64_t I0 = I * bs, b = std::min<int64_t>(bs, n - I0), I1 = I0 + b;
+  for (int64_t I = (n + BS - 1) / BS - 1; I >= 0; I--) {
+    const int64_t I0 = I * BS, I1 = std::min<int64_t>(n, I0 + BS);
     Zgemm g;
     if (I1 < n) {
-      g.opa = OP_C; g.M = b; g.N = m; g.K = n - I1; g.A = L + I1 + I0 * ldl; g.lda = ldl; g.B = E + I1; g.ldb = lde;
-      g.C = E + I0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0;
+      g.opa = OP_C; g.M = I1 - I0; g.N = m; g.K = n - I1; g.A = L + I1 + I0 * ldl; g.lda = ldl; g.B = E + I1;
+      g.ldb = lde; g.C = E + I0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0;
       EIG_TRY(zgemm(c, g));
     }
-    // in place: one 64-row M tile per column tile, no split-K -> every CTA reads
-    // its whole K range before its epilogue writes
-    g = Zgemm();
-    g.opa = OP_C; g.M = b; g.N = m; g.K = b; g.A = Linv + I * bs * bs; g.lda = bs; g.B = E + I0; g.ldb = lde;
-    g.C = E + I0; g.ldc = lde; g.alpha = 1.0; g.beta = 0.0; g.splitk = 1;
-    EIG_TRY(zgemm(c, g));
+    for (int64_t i0 = I0 + ((I1 - I0 - 1) / bs) * bs; i0 >= I0; i0 -= bs) {
+      const int64_t i1 = std::min<int64_t>(I1, i0 + bs), bi = i1 - i0;
+      if (i1 < I1) {
+        g = Zgemm();
+        g.opa = OP_C; g.M = bi; g.N = m; g.K = I1 - i1; g.A = L + i1 + i0 * ldl; g.lda = ldl; g.B = E + i1;
+        g.ldb = lde; g.C = E + i0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0;
+        EIG_TRY(zgemm(c, g));
+      }
+      // in place: one 64-row M tile per column tile, no split-K -> every CTA reads
+      // its whole K range before its epilogue writes
+      g = Zgemm();
+      g.opa = OP_C; g.M = bi; g.N = m; g.K = bi; g.A = Linv + (i0 / bs) * bs * bs; g.lda = bs; g.B = E + i0;
+      g.ldb = lde; g.C = E + i0; g.ldc = lde; g.alpha = 1.0; g.beta = 0.0; g.splitk = 1;
+      EIG_TRY(zgemm(c, g));
+    }
   }
   return 0;
 }
@@ -296,6 +342,12 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, x->c.device);
   if (sms > 0) x->c.num_sms = sms;
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  rc = x->c.check(cudaStreamCreateWithPriority(&x->c.side, cudaStreamNonBlocking, hi_prio), "side stream");
+  if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_fork, cudaEventDisableTiming), "event");
+  if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_join, cudaEventDisableTiming), "event");
+  if (rc) { delete x; return rc; }
   void *bar = x->c.ws(WS_BARRIER, 64);
   if (!bar) { delete x; return EIG_ERR_NOMEM; }
   rc = x->c.check(cudaMemset(bar, 0, 64), "barrier init");
@@ -318,6 +370,9 @@ int eig_finalize(eig_handle h) {
   if (!h) return EIG_ERR_STATE;
   cudaSetDevice(h->c.device);
   cudaStreamSynchronize(h->c.stream);
+  if (h->c.side) { cudaStreamSynchronize(h->c.side); cudaStreamDestroy(h->c.side); }
+  if (h->c.ev_fork) cudaEventDestroy(h->c.ev_fork);
+  if (h->c.ev_join) cudaEventDestroy(h->c.ev_join);
   for (int i = 0; i < WS_COUNT; i++) {
     if (h->c.buf[i]) cudaFree(h->c.buf[i]);
   }

@@ -31,6 +31,8 @@ enum WsId {
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;        // high-priority stream for the he2hb panels (look-ahead)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int nb = 64;
   int q2g = 32;
   int num_sms = 148;

@@ -13,7 +13,9 @@ enum Op { OP_N = 0, OP_C = 1 };
 struct Zgemm {
   int opa = OP_N, opb = OP_N;
   int herm_a = 0;   // A Hermitian, lower stored (opa must be N)
-  int lower_c = 0;  // only lower triangle of C (M == N), imag(diag) = 0
+  int lower_c = 0;  // 1: only lower triangle of C (M == N, lower tiles only), imag(diag) = 0
+                    // 2: rectangular grid, writes only entries with row0 + gm >= gn, imag(diag) = 0
+  int64_t row0 = 0;  // lower modes: matrix row of C row 0
   int64_t M = 0, N = 0, K = 0;
   const double2 *A = nullptr;
   int64_t lda = 0;
@@ -33,7 +35,7 @@ int zgemm(Ctx &ctx, const Zgemm &g);
 // writes V (explicit, pn x nb, ldv) into vout (and vout2 if non-null),
 // tau[nb], T (nb x nb, ld nb).
 int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau, double2 *T, double2 *vout,
-             double2 *vout2, int64_t ldv);
+             double2 *vout2, int64_t ldv, cudaStream_t stream);
 
 // Copy the reflectors of panel k from the he2hb layout into an explicit
 // unit-lower s x nb matrix (ld ldv).

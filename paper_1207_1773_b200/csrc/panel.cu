@@ -57,7 +57,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // so the trailing-column update and the T column
 //   T[0:j, j] = -tau_j T[0:j, 0:j] y   (zlarft, forward/columnwise)
 // need no second reduction.
-__global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
+__global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double2 sm[];
   const int nb = a.nb, R = a.R, G = a.G;
   const int recw = 2 * nb;
@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   double2 *sW = sS + nb;            // [nb]   w_l / y_i
   double2 *sY = sW + nb;            // [nb]   y_i (T column)
   double2 *sPart = sY + nb;         // [4][64]
-  double2 *sT = sPart + 4 * 64;     // [nb][nb] (CTA 0)
-  double2 *sP = sT + nb * nb;       // [nb][R], column l at sP + l*R
+  double2 *sP = sPart + 4 * 64;     // [nb][R], column l at sP + l*R
+  double2 *gT = a.T;                // T is built in place in global memory by CTA 0 (off the critical path)
   __shared__ double2 s_tau, s_scale;
   __shared__ double s_beta;
 
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   for (int l = 0; l < nb; l++)
     for (int r = tid; r < R; r += PT) sP[l * R + r] = (r < rows) ? a.P[(row0 + r) + (int64_t)l * a.lda] : czero();
   if (g == 0)
-    for (int e = tid; e < nb * nb; e += PT) sT[e] = czero();
+    for (int e = tid; e < nb * nb; e += PT) gT[e] = czero();
   __syncthreads();
 
   const bool prof = a.prof != nullptr && g == 0 && tid == 0;
@@ -235,10 +235,10 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       // T column j: T[0:j, j] = -tau_j T[0:j, 0:j] y
       if (tid < j) {
         double2 acc = czero();
-        for (int l = tid; l < j; l++) acc = cadd(acc, cmul(sT[tid + l * nb], sY[l]));
-        sT[tid + j * nb] = make_double2(-(tau.x * acc.x - tau.y * acc.y), -(tau.x * acc.y + tau.y * acc.x));
+        for (int l = tid; l < j; l++) acc = cadd(acc, cmul(gT[tid + l * nb], sY[l]));
+        gT[tid + j * nb] = make_double2(-(tau.x * acc.x - tau.y * acc.y), -(tau.x * acc.y + tau.y * acc.x));
       }
-      if (tid == 0) sT[j + j * nb] = tau;
+      if (tid == 0) gT[j + j * nb] = tau;
     }
     __syncthreads();
     mark(5);
@@ -254,10 +254,8 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       a.vout[grow + (int64_t)l * a.ldv] = v;
       if (a.vout2) a.vout2[grow + (int64_t)l * a.ldv] = v;
     }
-  if (g == 0) {
-    for (int e = tid; e < nb * nb; e += PT) a.T[e] = sT[e];
+  if (g == 0)
     for (int l = tid; l < nb; l += PT) a.tau[l] = (l < a.nref) ? sTau[l] : czero();
-  }
   if (prof)
     for (int k = 0; k < 6; k++) atomicAdd(&a.prof[8 + k], (unsigned long long)tacc[k]);
 }
@@ -283,7 +281,7 @@ __global__ void real_diag_kernel(int64_t n, double2 *A, int64_t lda) {
 }  // namespace
 
 int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau, double2 *T, double2 *vout,
-             double2 *vout2, int64_t ldv) {
+             double2 *vout2, int64_t ldv, cudaStream_t stream) {
   if (pn <= 0) return 0;
   if (nb > 64) return EIG_ERR_NOTIMPL;
   const int nref = (int)std::min<int64_t>(pn, nb);
@@ -293,7 +291,7 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   R = std::max(R, nb);
   G = (int)((pn + R - 1) / R);
   const int recw = 2 * nb;
-  const size_t smem = ((size_t)5 * nb + 4 * 64 + (size_t)nb * nb + (size_t)nb * R) * sizeof(double2);
+  const size_t smem = ((size_t)5 * nb + 4 * 64 + (size_t)nb * R) * sizeof(double2);
   if (smem > 220 * 1024) return EIG_ERR_NOTIMPL;  // panel too tall for on-chip residency (n > ~20000 at nb=64)
   PanelArgs a;
   a.P = P;
@@ -320,7 +318,7 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
     attr = true;
   }
   void *args[] = {&a};
-  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel, dim3(G), dim3(PT), args, smem, ctx.stream),
+  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel, dim3(G), dim3(PT), args, smem, stream),
                     "panel_qr_kernel launch"));
   ctx.bar_epoch += (unsigned long long)G * nref;   // arrivals this launch performs
   return ctx.launched("panel_qr_kernel");

@@ -35,18 +35,19 @@ struct Params {
   int64_t ldc;
   double alpha, beta;
   double2 *part;   // split-K partials [split][M*N] (ld M), or nullptr
+  int64_t row0;    // lower modes: C row gm is matrix row row0 + gm (column gn is column gn)
   int64_t kchunk;  // K per split (multiple of BK)
   int tiles_m;
 };
 
-template <int OPA, int OPB, bool HERM, bool LOWER>
+template <int OPA, int OPB, bool HERM, int LOWER>
 __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
   extern __shared__ __align__(16) double2 smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2;
 
   int tm, tn;
-  if (LOWER) {
+  if (LOWER == 1) {
     const int64_t x = blockIdx.x;
     int64_t I = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
     while ((I + 1) * (I + 2) / 2 <= x) I++;
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
         if (p.part) {
           p.part[(int64_t)blockIdx.y * p.M * p.N + gm + gn * p.M] = v;
         } else {
-          if (LOWER && gm < gn) continue;
+          if (LOWER && p.row0 + gm < gn) continue;
           double2 out = make_double2(p.alpha * v.x, p.alpha * v.y);
           double2 *cp = p.C + gm + gn * p.ldc;
           if (p.beta != 0.0) {
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
             out.x += p.beta * c.x;
             out.y += p.beta * c.y;
           }
-          if (LOWER && gm == gn) out.y = 0.0;
+          if (LOWER && p.row0 + gm == gn) out.y = 0.0;
           *cp = out;
         }
       }
@@ -213,11 +214,11 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
 
 // C = alpha * sum_z part[z] + beta * C  (fixed summation order -> deterministic)
 __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int split, const double2 *__restrict__ part, double2 *C,
-                                     int64_t ldc, double alpha, double beta, int lower) {
+                                     int64_t ldc, double alpha, double beta, int lower, int64_t row0) {
   const int64_t total = M * N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t gm = e % M, gn = e / M;
-    if (lower && gm < gn) continue;
+    if (lower && row0 + gm < gn) continue;
     double2 s = part[e];
     for (int z = 1; z < split; z++) {
       const double2 t = part[(int64_t)z * total + e];
@@ -231,12 +232,12 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int split, const doub
       out.x += beta * c.x;
       out.y += beta * c.y;
     }
-    if (lower && gm == gn) out.y = 0.0;
+    if (lower && row0 + gm == gn) out.y = 0.0;
     *cp = out;
   }
 }
 
-template <int OPA, int OPB, bool HERM, bool LOWER>
+template <int OPA, int OPB, bool HERM, int LOWER>
 int launch_t(Ctx &ctx, const Params &p, dim3 grid) {
   static bool attr_done = false;
   if (!attr_done) {
@@ -255,19 +256,28 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   if (g.M <= 0 || g.N <= 0) return 0;
   if (g.K <= 0 && g.beta == 1.0) return 0;  // K = 0 otherwise runs the epilogue only: C = beta C
   if (g.herm_a && (g.opa != OP_N || g.M != g.K)) return -2;
-  if (g.lower_c && g.M != g.N) return -2;
+  if (g.lower_c == 1 && g.M != g.N) return -2;
 
   const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
-  const int64_t tiles = g.lower_c ? (int64_t)tiles_m * (tiles_m + 1) / 2 : (int64_t)tiles_m * tiles_n;
+  const int64_t tiles = g.lower_c == 1 ? (int64_t)tiles_m * (tiles_m + 1) / 2 : (int64_t)tiles_m * tiles_n;
   const int64_t ktiles = std::max<int64_t>(1, (g.K + BK - 1) / BK);
   int split = g.splitk;
   if (split <= 0) {
-    const int64_t target = 2LL * ctx.num_sms;
+    // pick the split that minimises (waves of 2 CTAs/SM) x (k-tiles per CTA + fixed per-CTA cost),
+    // plus the partial-sum traffic of the reduction (in k-tile units)
+    const int64_t cap = 2LL * ctx.num_sms;
+    const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(64, ktiles / 4));
+    double best = 1e300;
     split = 1;
-    if (tiles < target) {
-      int64_t want = (target + tiles - 1) / tiles;
-      int64_t maxs = std::max<int64_t>(1, ktiles / 4);
-      split = (int)std::min<int64_t>(want, maxs);
+    for (int64_t sp = 1; sp <= maxs; sp++) {
+      const int64_t kt = (ktiles + sp - 1) / sp;
+      const int64_t waves = (tiles * sp + cap - 1) / cap;
+      const double red = sp > 1 ? 0.02 * (double)sp * (double)g.M * (double)g.N / (double)(cap * 64 * 64) * 8.0 : 0.0;
+      const double t = (double)waves * (double)(kt + 3) + red;
+      if (t < best * 0.98) {
+        best = t;
+        split = (int)sp;
+      }
     }
   }
   int64_t kt_per = (ktiles + split - 1) / split;
@@ -288,6 +298,7 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   p.kchunk = kt_per * BK;
   p.tiles_m = tiles_m;
   p.part = nullptr;
+  p.row0 = g.row0;
   if (split > 1) {
     p.part = (double2 *)ctx.ws(WS_PART, (size_t)split * g.M * g.N * sizeof(double2));
     if (!p.part) return EIG_ERR_NOMEM;
@@ -295,25 +306,28 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   dim3 grid((unsigned)tiles, (unsigned)split);
   int rc;
   if (g.herm_a)
-    rc = launch_t<OP_N, OP_N, true, false>(ctx, p, grid);
-  else if (g.lower_c) {
-    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, true>(ctx, p, grid);
-    else if (g.opa == OP_N && g.opb == OP_N) rc = launch_t<OP_N, OP_N, false, true>(ctx, p, grid);
+    rc = launch_t<OP_N, OP_N, true, 0>(ctx, p, grid);
+  else if (g.lower_c == 1) {
+    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 1>(ctx, p, grid);
+    else if (g.opa == OP_N && g.opb == OP_N) rc = launch_t<OP_N, OP_N, false, 1>(ctx, p, grid);
+    else return -2;
+  } else if (g.lower_c == 2) {
+    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 2>(ctx, p, grid);
     else return -2;
   } else if (g.opa == OP_N && g.opb == OP_N)
-    rc = launch_t<OP_N, OP_N, false, false>(ctx, p, grid);
+    rc = launch_t<OP_N, OP_N, false, 0>(ctx, p, grid);
   else if (g.opa == OP_C && g.opb == OP_N)
-    rc = launch_t<OP_C, OP_N, false, false>(ctx, p, grid);
+    rc = launch_t<OP_C, OP_N, false, 0>(ctx, p, grid);
   else if (g.opa == OP_N && g.opb == OP_C)
-    rc = launch_t<OP_N, OP_C, false, false>(ctx, p, grid);
+    rc = launch_t<OP_N, OP_C, false, 0>(ctx, p, grid);
   else
-    rc = launch_t<OP_C, OP_C, false, false>(ctx, p, grid);
+    rc = launch_t<OP_C, OP_C, false, 0>(ctx, p, grid);
   if (rc) return rc;
   if (split > 1) {
     const int64_t total = g.M * g.N;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8LL * ctx.num_sms);
     splitk_reduce_kernel<<<blocks, 256, 0, ctx.stream>>>(g.M, g.N, split, p.part, g.C, g.ldc, g.alpha, g.beta,
-                                                          g.lower_c);
+                                                          g.lower_c, g.row0);
     EIG_TRY(ctx.launched("splitk_reduce_kernel"));
   }
   return 0;
