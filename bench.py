@@ -133,13 +133,13 @@ def cpu_sample(n, nb, seed, budget, pre=None):
     A = pre[0] if pre else synth.rand_hermitian(n, seed)
     Ah = oracle.full_hermitian(A)
     # he2hb sample
-    r = 4
+    r = 8
     t0 = time.perf_counter()
     oracle.he2hb_partial(Ah, nb, r)
     t_he = time.perf_counter() - t0
     fl_he = sum(16.0 * (n - nb - j) ** 2 for j in range(r))
     # BT sample
-    c = max(1, min(cores, 8))
+    c = max(1, min(cores, 16))
     V2, tau2 = (pre[1], pre[2]) if pre else synth.synthetic_v2(n, nb, seed)
     A1, tau1 = synth.synthetic_v1(n, nb, seed)
     L = pre[3] if pre else synth.unit_lower(n, seed)
