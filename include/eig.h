@@ -104,6 +104,16 @@ int eig_apply_q1(eig_handle h, int64_t n, const void *A, int64_t lda, const void
 int eig_apply_q2(eig_handle h, int64_t n, const void *V2, const void *tau2, const double *Z, int64_t ldz, void *E,
                  int64_t lde, int64_t m);
 
+/* ------------------------------------------------------------------ NEXT-1
+ * Band -> real symmetric tridiagonal by column-wise bulge chasing (P:L93,
+ * reading R5), on the device.  A: he2hb output (only the lower band
+ * 0 <= r-c <= nb is read; not modified).  d[n], e[n-1]: real diagonal and
+ * sub-diagonal (e_i = beta of sweep i, LAPACK zlarfg convention, so T is
+ * real without a phase diagonal).  V2 [slots*nb], tau2 [slots]: the chase
+ * reflectors in the V2 layout below, so that Band = Q2 T Q2^H.  Uses nb of
+ * the handle; library workspace holds a (2nb+2) x n band copy. */
+int eig_hb2st(eig_handle h, int64_t n, const void *A, int64_t lda, double *d, double *e, void *V2, void *tau2);
+
 /* ------------------------------------------------------------------ a8
  * E <- L^-H E (Algorithm 1 step 4): L n x n lower triangular
  * (non-unit; only the lower triangle read), E n x m. */

@@ -60,6 +60,7 @@ def lib():
             "eig_zgemm": (C.c_int, [h, C.c_char, C.c_char, I, I, I, D, P, I, P, I, D, P, I, C.c_int, C.c_int]),
             "eig_solve_gen": (C.c_int, [h, I, P, I, P, I, C.c_int, D, I, I, P, P, I, P]),
             "eig_debug_q2_profile": (C.c_int, [h, P]),
+            "eig_hb2st": (C.c_int, [h, I, P, I, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -72,7 +73,7 @@ def lib():
 def exported_symbols():
     return ["eig_init", "eig_finalize", "eig_strerror", "eig_last_cuda_error", "eig_launch_count", "eig_sync",
             "eig_num_panels", "eig_v2_slots", "eig_he2hb", "eig_apply_q1", "eig_apply_q2", "eig_trsm_lh",
-            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile"]
+            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile", "eig_hb2st"]
 
 
 def num_panels(n: int, nb: int) -> int:
@@ -171,6 +172,17 @@ class Solver:
         T = torch.zeros(max(K * self.nb * self.nb, 1), dtype=torch.complex128, device=A.device)
         self._check(lib().eig_he2hb(self.h, n, _ptr(A), _ld(A), _ptr(tau), _ptr(T)))
         return tau, T
+
+    def hb2st(self, A):
+        """NEXT-1: band (he2hb output A) -> (d, e, V2 [slots, nb], tau2 [slots])."""
+        n = A.shape[0]
+        slots = v2_slots(n, self.nb)
+        d = torch.zeros(max(n, 1), dtype=torch.float64, device=A.device)
+        e = torch.zeros(max(n, 1), dtype=torch.float64, device=A.device)
+        V2 = torch.zeros((max(slots, 1), self.nb), dtype=torch.complex128, device=A.device)
+        tau2 = torch.zeros(max(slots, 1), dtype=torch.complex128, device=A.device)
+        self._check(lib().eig_hb2st(self.h, n, _ptr(A), _ld(A), _ptr(d), _ptr(e), _ptr(V2), _ptr(tau2)))
+        return d[:n], e[:max(n - 1, 0)], V2[:slots], tau2[:slots]
 
     def apply_q1(self, A, T, E):
         n, m = E.shape

@@ -443,6 +443,31 @@ int eig_trsm_lh(eig_handle h, int64_t n, const void *L, int64_t ldl, void *E, in
   return trsm_lh_run(h->c, n, (const double2 *)L, ldl, (double2 *)E, lde, m);
 }
 
+int eig_hb2st(eig_handle h, int64_t n, const void *A, int64_t lda, double *d, double *e, void *V2, void *tau2) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (lda < std::max<int64_t>(1, n)) return -4;
+  Ctx &c = h->c;
+  cudaSetDevice(c.device);
+  if (n <= 1) {
+    if (n == 1) EIG_TRY(c.check(cudaMemcpy2DAsync(d, sizeof(double), A, sizeof(double2), sizeof(double), 1,
+                                                  cudaMemcpyDeviceToDevice, c.stream), "d"));
+    return 0;
+  }
+  std::vector<int64_t> off;
+  int64_t o = 0;
+  for (int64_t j = 0; 1 + j * c.nb <= n - 1; j++) {
+    off.push_back(o);
+    o += n - 1 - j * c.nb;
+  }
+  int64_t *d_off = (int64_t *)c.ws(WS_HBOFF, off.size() * sizeof(int64_t));
+  if (!d_off) return EIG_ERR_NOMEM;
+  EIG_TRY(c.check(cudaMemcpyAsync(d_off, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c.stream),
+                  "offsets"));
+  EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "offsets sync"));   // host vector goes out of scope
+  return hb2st(c, n, c.nb, (const double2 *)A, lda, d, e, (double2 *)V2, (double2 *)tau2, d_off);
+}
+
 int eig_zgemm(eig_handle h, char opa, char opb, int64_t M, int64_t N, int64_t K, double alpha, const void *A,
               int64_t lda, const void *B, int64_t ldb, double beta, void *C, int64_t ldc, int herm_a, int lower_c) {
   EIG_TRY(valid(h));

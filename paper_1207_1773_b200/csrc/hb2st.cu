@@ -1,0 +1,246 @@
+// hb2st.cu — second stage of the two-stage reduction on the device (NEXT-1):
+// Hermitian band (half-bandwidth nb) -> real symmetric tridiagonal by
+// column-wise bulge chasing ("we differ by using a column-wise
+// elimination"; reading R5), producing the Q2 reflectors in the V2
+// layout of include/eig.h.
+//
+// Task (i, j) (sweep i, step j): target column c = i (j = 0) or
+// i+1+(j-1)nb, rows R = [r0, r1] = [i+1+j nb, min(i+(j+1)nb, n-1)]:
+//   (beta, tau, v) = zlarfg(M[R, c]);  M[r0, c] = beta, M[r0+1:r1, c] = 0;
+//   (a) M[R, k] <- H^H M[R, k] for the rest of the previous bulge, c < k < r0;
+//   (b) M[R, R] <- H^H M[R, R] H            (p = tau D v, w = p - tau/2 (p^H v) v);
+//   (c) M[k, R] <- M[k, R] H for r1 < k <= min(r1 + nb, n-1)  (creates the next bulge).
+// Sequential order: sweep i-1 entirely before sweep i.  Task (i, j) touches
+// rows [r0, r1 + nb] x cols [c, r1]; of sweep i-1 only its steps <= j+2
+// overlap that region, so sweep i may run step j once sweep i-1 has finished
+// step j+2: a wavefront of ~J/3 concurrent sweeps.  One persistent
+// cooperative kernel: sweep i is owned by CTA i mod P, progress flags in
+// global memory (release/acquire), the band (2nb+1 diagonals, lower) lives in
+// L2 and is accessed with L1-bypassing loads.
+#include <algorithm>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "kernels.h"
+
+namespace eig {
+namespace {
+
+constexpr int HT = 256;
+
+struct HbArgs {
+  int64_t n;
+  int nb, ldab;
+  double2 *AB;            // band: M(r, c) = AB[(r - c) + c * ldab], 0 <= r - c <= 2nb
+  double2 *V2, *tau2;     // outputs (V2 layout)
+  const int64_t *off;     // slot offsets per step j
+  int *progress;          // [n] steps completed per sweep
+};
+
+__device__ __forceinline__ int ld_acquire_i32(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i32(int *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
+  __shared__ double2 sv[64];          // reflector
+  extern __shared__ __align__(16) double2 sD[];   // [64 * 65] diagonal block (full Hermitian), ld 65
+  __shared__ double2 sp[64];          // p, then w
+  __shared__ double2 s_tau, s_beta_scale;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n;
+  const int nb = a.nb, ldab = a.ldab;
+  double2 *AB = a.AB;
+  auto M = [&](int64_t r, int64_t c) -> double2 * { return AB + (r - c) + c * (int64_t)ldab; };
+
+  for (int64_t i = blockIdx.x; i + 1 < n; i += gridDim.x) {
+    for (int64_t j = 0;; j++) {
+      const int64_t c = (j == 0) ? i : i + 1 + (j - 1) * nb;
+      const int64_t r0 = i + 1 + j * nb;
+      if (r0 > n - 1) break;
+      const int64_t r1 = imin64(i + (j + 1) * nb, n - 1);
+      const int len = (int)(r1 - r0 + 1);
+      // wait for sweep i-1 to finish step j+2 (or to finish)
+      if (i > 0 && tid == 0) {
+        const int64_t prev = i - 1;
+        const int64_t jprev_max = (n - 2 - prev) / nb;   // last step index of sweep i-1
+        const int need = (int)imin64(j + 3, jprev_max + 1);
+        while (ld_acquire_i32(a.progress + prev) < need) {
+        }
+      }
+      __syncthreads();
+      // ---- reflector from M[R, c]
+      if (warp == 0) {
+        double2 x0 = czero(), x1 = czero();
+        if (lane < len) x0 = __ldcg(M(r0 + lane, c));
+        if (lane + 32 < len) x1 = __ldcg(M(r0 + lane + 32, c));
+        double nrm = 0.0;
+        if (lane >= 1) nrm += x0.x * x0.x + x0.y * x0.y;
+        nrm += x1.x * x1.x + x1.y * x1.y;
+        nrm = warp_sum(nrm);
+        double2 al = make_double2(__shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0));
+        double2 tau, scale;
+        double beta;
+        if (nrm == 0.0 && al.y == 0.0) {
+          tau = czero();
+          beta = al.x;
+          scale = czero();
+        } else {
+          beta = -copysign(sqrt(al.x * al.x + al.y * al.y + nrm), al.x);
+          tau = make_double2((beta - al.x) / beta, -al.y / beta);
+          const double2 d = make_double2(al.x - beta, al.y);
+          const double dd = d.x * d.x + d.y * d.y;
+          scale = make_double2(d.x / dd, -d.y / dd);
+        }
+        // v
+        sv[lane] = (lane == 0) ? make_double2(1.0, 0.0) : (lane < len ? cmul(x0, scale) : czero());
+        sv[lane + 32] = (lane + 32 < len) ? cmul(x1, scale) : czero();
+        if (lane == 0) {
+          s_tau = tau;
+          s_beta_scale = make_double2(beta, 0.0);
+        }
+      }
+      __syncthreads();
+      const double2 tau = s_tau, ctau = cconj(tau);
+      // outputs: V2 slot, tau2, the eliminated column
+      {
+        const int64_t slot = a.off[j] + i;
+        for (int t = tid; t < nb; t += HT) a.V2[slot * nb + t] = (t < len) ? sv[t] : czero();
+        if (tid == 0) a.tau2[slot] = tau;
+        for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta_scale : czero();
+      }
+      if (tau.x != 0.0 || tau.y != 0.0) {
+        // ---- (a) left application to columns c < k < r0 (rest of the previous bulge)
+        for (int64_t k = c + 1 + warp; k < r0; k += HT / 32) {
+          double2 y0 = czero(), y1 = czero();
+          if (lane < len) y0 = __ldcg(M(r0 + lane, k));
+          if (lane + 32 < len) y1 = __ldcg(M(r0 + lane + 32, k));
+          double2 sdot = cadd(cmulc(sv[lane], y0), cmulc(sv[lane + 32], y1));   // v^H y
+          sdot = warp_sum2(sdot);
+          const double2 f = cmul(ctau, sdot);
+          if (lane < len) *M(r0 + lane, k) = csub(y0, cmul(sv[lane], f));
+          if (lane + 32 < len) *M(r0 + lane + 32, k) = csub(y1, cmul(sv[lane + 32], f));
+        }
+        // ---- (b) two-sided on the diagonal block
+        for (int e = tid; e < len * len; e += HT) {
+          const int rr = e % len, cc = e / len;
+          if (rr >= cc) {
+            double2 d = __ldcg(M(r0 + rr, r0 + cc));
+            if (rr == cc) d.y = 0.0;
+            sD[rr + cc * 65] = d;
+            sD[cc + rr * 65] = cconj(d);
+          }
+        }
+        __syncthreads();
+        if (tid < len) {   // p = tau D v
+          double2 acc = czero();
+          for (int cc = 0; cc < len; cc++) acc = cadd(acc, cmul(sD[tid + cc * 65], sv[cc]));
+          sp[tid] = cmul(tau, acc);
+        }
+        __syncthreads();
+        if (warp == 0) {   // w = p - 1/2 tau (p^H v) v
+          double2 s = czero();
+          for (int t = lane; t < len; t += 32) s = cadd(s, cmulc(sp[t], sv[t]));
+          s = warp_sum2(s);
+          const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), s);
+          for (int t = lane; t < len; t += 32) sp[t] = cadd(sp[t], cmul(al, sv[t]));
+        }
+        __syncthreads();
+        for (int e = tid; e < len * len; e += HT) {
+          const int rr = e % len, cc = e / len;
+          if (rr >= cc) {
+            double2 d = sD[rr + cc * 65];
+            d = csub(d, cadd(cmul(sv[rr], cconj(sp[cc])), cmul(sp[rr], cconj(sv[cc]))));
+            if (rr == cc) d.y = 0.0;
+            *M(r0 + rr, r0 + cc) = d;
+          }
+        }
+        // ---- (c) right application to rows r1 < k <= min(r1 + nb, n-1)
+        const int64_t kend = imin64(r1 + nb, n - 1);
+        for (int64_t k = r1 + 1 + warp; k <= kend; k += HT / 32) {
+          double2 y0 = czero(), y1 = czero();
+          if (lane < len) y0 = __ldcg(M(k, r0 + lane));
+          if (lane + 32 < len) y1 = __ldcg(M(k, r0 + lane + 32));
+          double2 t = cadd(cmul(y0, sv[lane]), cmul(y1, sv[lane + 32]));   // y v
+          t = warp_sum2(t);
+          const double2 f = cmul(t, tau);
+          if (lane < len) *M(k, r0 + lane) = csub(y0, cmul(f, cconj(sv[lane])));
+          if (lane + 32 < len) *M(k, r0 + lane + 32) = csub(y1, cmul(f, cconj(sv[lane + 32])));
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release_i32(a.progress + i, (int)(j + 1));
+    }
+  }
+}
+
+__global__ void band_in_kernel(int64_t n, int nb, const double2 *A, int64_t lda, double2 *AB, int ldab) {
+  const int64_t total = n * (int64_t)ldab;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int)(e % ldab);
+    const int64_t c = e / ldab;
+    double2 v = czero();
+    if (d <= nb && c + d < n) {
+      v = A[(c + d) + c * lda];
+      if (d == 0) v.y = 0.0;
+    }
+    AB[e] = v;
+  }
+}
+
+__global__ void tridiag_out_kernel(int64_t n, const double2 *AB, int ldab, double *d, double *e) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    d[i] = AB[i * (int64_t)ldab].x;
+    if (i + 1 < n) e[i] = AB[1 + i * (int64_t)ldab].x;
+  }
+}
+
+}  // namespace
+
+int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d, double *e, double2 *V2,
+          double2 *tau2, const int64_t *d_off) {
+  if (n <= 0) return 0;
+  if (nb > 64) return EIG_ERR_NOTIMPL;
+  const int ldab = 2 * nb + 2;
+  double2 *AB = (double2 *)ctx.ws(WS_BAND, (size_t)ldab * n * sizeof(double2));
+  int *prog = (int *)ctx.ws(WS_HBPROG, (size_t)n * sizeof(int));
+  if (!AB || !prog) return EIG_ERR_NOMEM;
+  EIG_TRY(ctx.check(cudaMemsetAsync(prog, 0, (size_t)n * sizeof(int), ctx.stream), "memset progress"));
+  const int64_t total = n * (int64_t)ldab;
+  band_in_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 8LL * ctx.num_sms), 256, 0, ctx.stream>>>(
+      n, nb, A, lda, AB, ldab);
+  EIG_TRY(ctx.launched("band_in_kernel"));
+  if (n > 1) {
+    HbArgs a;
+    a.n = n;
+    a.nb = nb;
+    a.ldab = ldab;
+    a.AB = AB;
+    a.V2 = V2;
+    a.tau2 = tau2;
+    a.off = d_off;
+    a.progress = prog;
+    const int64_t J = (n - 2) / nb + 1;   // steps of sweep 0
+    const int P = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, std::min<int64_t>(n - 1, J / 3 + 2)));
+    void *args[] = {&a};
+    const size_t smem = (size_t)64 * 65 * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+      EIG_TRY(ctx.check(cudaFuncSetAttribute(hb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "hb2st attr"));
+      attr = true;
+    }
+    EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)hb2st_kernel, dim3(P), dim3(HT), args, smem, ctx.stream),
+                      "hb2st launch"));
+    EIG_TRY(ctx.launched("hb2st_kernel"));
+  }
+  tridiag_out_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, ctx.stream>>>(n, AB, ldab, d, e);
+  return ctx.launched("tridiag_out_kernel");
+}
+
+}  // namespace eig

@@ -50,6 +50,10 @@ int complexify(Ctx &ctx, int64_t n, int64_t m, const double *Z, int64_t ldz, dou
 // Zero the imaginary part of the diagonal of A (n x n).
 int real_diag(Ctx &ctx, int64_t n, double2 *A, int64_t lda);
 
+// Device bulge chase (NEXT-1): band from he2hb output A -> d, e and V2/tau2.
+int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d, double *e, double2 *V2,
+          double2 *tau2, const int64_t *d_off);
+
 // ------------------------------------------------------------- Q2
 struct Q2Plan {
   int64_t n = 0;

@@ -132,6 +132,19 @@ def pencil_known(n: int, seed: int = 0, kappa: float = 1e2, clustered: bool = Tr
     return A, B, D
 
 
+def known_hermitian(n: int, seed: int = 0, r: int = 8):
+    """Standard Hermitian matrix with an exactly known spectrum:
+    A = W^H diag(D) W, W a product of r random reflectors, D sorted U(-1, 1)
+    with 10% of the values in near-degenerate pairs (spacing 1e-9).
+    Returns (A full, D ascending)."""
+    D = np.sort(uniform(seed, 70, n) * 2.0 - 1.0)
+    k = n // 10
+    D[1:2 * k:2] = D[0:2 * k - 1:2] + 1e-9
+    D = np.sort(D)
+    W = random_reflectors(n, min(n, r), seed, 71)
+    return apply_reflectors_congruence(np.diag(D).astype(np.complex128), W), D
+
+
 def fem_pencil(n: int, seed: int = 0):
     """G4 (pin P6): K = tridiag(-1,2,-1), M = tridiag(1/6,2/3,1/6) under a
     unitary congruence; lambda_k = 6(1-cos t_k)/(2+cos t_k), t_k = k pi/(n+1)."""

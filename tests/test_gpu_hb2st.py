@@ -1,0 +1,81 @@
+"""NEXT-1 parity: device bulge chase (eig_hb2st) vs the oracle's dense
+column-wise chase (oracle.hb2st), elementwise on d, e, V2, tau2; and at full
+size the spectrum of the produced tridiagonal (oracle Sturm bisection) equals
+the exactly known spectrum of the input (marker: gpu)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+gpu = pytest.mark.gpu
+
+
+def _dev(x):
+    from paper_1207_1773_b200 import colmajor
+    return colmajor(x, torch.device("cuda:0"))
+
+
+def _band_full(A_out, nb):
+    n = A_out.shape[0]
+    r, c = np.indices((n, n))
+    Bl = np.where((r - c >= 0) & (r - c <= nb), A_out, 0)
+    B = np.tril(Bl) + np.tril(Bl, -1).conj().T
+    B[np.diag_indices(n)] = B.diagonal().real
+    return B
+
+
+@gpu
+@pytest.mark.parametrize("n,nb", [(40, 4), (150, 16), (300, 32), (517, 64), (65, 64), (64, 8), (2, 1)])
+def test_hb2st_parity_vs_oracle(n, nb):
+    from paper_1207_1773_b200 import Solver
+    s = Solver(0, nb=nb)
+    A = synth.rand_hermitian(n, n + nb)
+    A_o, _ = oracle.he2hb(A, nb)                    # band input from the oracle
+    d, e, V2, tau2 = s.hb2st(_dev(A_o))
+    d_o, e_o, V2_o, tau2_o = oracle.hb2st(_band_full(A_o, nb), nb)
+    scale = np.max(np.abs(A))
+    assert np.max(np.abs(d.cpu().numpy() - d_o)) < 1e-12 * scale * max(1, n / 100)
+    assert np.max(np.abs(e.cpu().numpy() - e_o)) < 1e-12 * scale * max(1, n / 100)
+    assert np.max(np.abs(tau2.cpu().numpy() - tau2_o)) < 1e-11 * max(1, n / 100)
+    assert np.max(np.abs(V2.cpu().numpy() - V2_o)) < 1e-10 * max(1, n / 100)
+
+
+@gpu
+def test_he2hb_hb2st_device_chain_known_spectrum():
+    """he2hb + hb2st both on the device; tridiagonal eigenvalues (oracle Sturm)
+    equal the known spectrum; Q2 from the device reflectors reproduces the band."""
+    from paper_1207_1773_b200 import Solver
+    n, nb = 400, 32
+    A, D = synth.known_hermitian(n, 3)
+    s = Solver(0, nb=nb)
+    dA = _dev(A)
+    s.he2hb(dA)
+    d, e, V2, tau2 = s.hb2st(dA)
+    w = oracle.sturm_values(d.cpu().numpy(), e.cpu().numpy())
+    assert np.max(np.abs(w - D)) < 1e-12
+    # Band = Q2 T Q2^H  (E <- Q2 E with the oracle's one-at-a-time application)
+    Band = _band_full(dA.cpu().numpy(), nb)
+    T = np.diag(d.cpu().numpy()) + np.diag(e.cpu().numpy(), 1) + np.diag(e.cpu().numpy(), -1)
+    Q2 = oracle.apply_q2(V2.cpu().numpy(), tau2.cpu().numpy(), nb, np.eye(n, dtype=complex))
+    assert np.linalg.norm(Q2 @ T @ Q2.conj().T - Band) < 1e-12 * np.linalg.norm(Band) * n / 10
+
+
+@gpu
+def test_full_size_hb2st_known_spectrum():
+    """n = 10000, nb = 64 (bench configuration): 64 sampled eigenvalues of the
+    device tridiagonal (oracle Sturm bisection) vs the exact spectrum."""
+    from paper_1207_1773_b200 import Solver
+    n, nb = 10000, 64
+    A, D = synth.known_hermitian(n, 5)
+    s = Solver(0, nb=nb)
+    dA = _dev(A)
+    del A
+    s.he2hb(dA)
+    d, e, V2, tau2 = s.hb2st(dA)
+    dd, ee = d.cpu().numpy(), e.cpu().numpy()
+    assert np.all(np.isfinite(dd)) and np.all(np.isfinite(ee))
+    idx = np.unique(np.linspace(1, n, 64).astype(int))
+    w = np.array([oracle.sturm_values(dd, ee, k, k)[0] for k in idx])
+    assert np.max(np.abs(w - D[idx - 1])) < 1e-10

@@ -79,6 +79,11 @@ def main():
             pr = s.q2_profile()[:5]
             tot = sum(pr)
             print("  CTA0 phase cycles (load, A, B, C, commit):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
+    elif a.mode == "hb2st":
+        A0 = colmajor(synth.rand_hermitian(n, 0), dev)
+        s.he2hb(A0)
+        ms = timeit(lambda: s.hb2st(A0), a.reps)
+        print(f"hb2st n={n} nb={a.nb}: {ms:.3f} ms  band bytes {n * (2 * a.nb + 2) * 16 / 1e6:.1f} MB")
     elif a.mode == "he2hb":
         A0 = colmajor(synth.rand_hermitian(n, 0), dev)
         A = A0.clone()
