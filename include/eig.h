@@ -147,8 +147,9 @@ int eig_zgemm(eig_handle h, char opa, char opb, int64_t M, int64_t N, int64_t K,
 
 /* Debug: cycles spent by CTA 0 of apply_q2 in its phases [0..4] (load, A,
  * B, C, commit) and of panel_qr [8..13] (barrier, reduce, beta, update,
- * partials, tail), accumulated since eig_init; needs EIG_Q2_PROFILE set in
- * the environment at eig_init (else EIG_ERR_NOTIMPL).  out16: host array. */
+ * partials, tail) and of hb2st [16..21] (wait, reflector, a, b, c, flag),
+ * accumulated since eig_init; needs EIG_Q2_PROFILE set in the environment at
+ * eig_init (else EIG_ERR_NOTIMPL).  out16: host array of 32. */
 int eig_debug_q2_profile(eig_handle h, unsigned long long *out16);
 
 /* Generalized solver (Algorithm 1).  Needs the NEXT stages

@@ -155,7 +155,7 @@ class Solver:
 
     def q2_profile(self):
         """Cycles of CTA 0: apply_q2 phases [0:5], panel_qr phases [8:14]; needs EIG_Q2_PROFILE."""
-        out = (C.c_ulonglong * 16)()
+        out = (C.c_ulonglong * 32)()
         self._check(lib().eig_debug_q2_profile(self.h, C.cast(out, C.c_void_p)))
         return list(out)
 

@@ -363,7 +363,7 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
 int eig_debug_q2_profile(eig_handle h, unsigned long long *out16) {
   if (!h) return EIG_ERR_STATE;
   if (!h->c.q2_prof) return EIG_ERR_NOTIMPL;
-  return h->c.check(cudaMemcpy(out16, h->c.q2_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "prof");
+  return h->c.check(cudaMemcpy(out16, h->c.q2_prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "prof");
 }
 
 int eig_finalize(eig_handle h) {

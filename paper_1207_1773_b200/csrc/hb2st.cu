@@ -35,6 +35,7 @@ struct HbArgs {
   double2 *V2, *tau2;     // outputs (V2 layout)
   const int64_t *off;     // slot offsets per step j
   int *progress;          // [n] steps completed per sweep
+  unsigned long long *prof;  // optional: CTA 0 phase cycles [16..21] (wait, refl, a, b, c, flag)
 };
 
 __device__ __forceinline__ int ld_acquire_i32(const int *p) {
@@ -56,6 +57,15 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
   const int nb = a.nb, ldab = a.ldab;
   double2 *AB = a.AB;
   auto M = [&](int64_t r, int64_t c) -> double2 * { return AB + (r - c) + c * (int64_t)ldab; };
+  const bool prof = a.prof != nullptr && blockIdx.x == 0 && tid == 0;
+  long long tm = 0, tacc[6] = {0, 0, 0, 0, 0, 0};
+  auto mark = [&](int k) {
+    if (prof) {
+      const long long now = clock64();
+      if (k >= 0) tacc[k] += now - tm;
+      tm = now;
+    }
+  };
 
   for (int64_t i = blockIdx.x; i + 1 < n; i += gridDim.x) {
     for (int64_t j = 0;; j++) {
@@ -64,6 +74,7 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       if (r0 > n - 1) break;
       const int64_t r1 = imin64(i + (j + 1) * nb, n - 1);
       const int len = (int)(r1 - r0 + 1);
+      mark(-1);
       // wait for sweep i-1 to finish step j+2 (or to finish)
       if (i > 0 && tid == 0) {
         const int64_t prev = i - 1;
@@ -73,6 +84,7 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
         }
       }
       __syncthreads();
+      mark(0);
       // ---- reflector from M[R, c]
       if (warp == 0) {
         double2 x0 = czero(), x1 = czero();
@@ -113,26 +125,51 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
         if (tid == 0) a.tau2[slot] = tau;
         for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta_scale : czero();
       }
+      mark(1);
       if (tau.x != 0.0 || tau.y != 0.0) {
-        // ---- (a) left application to columns c < k < r0 (rest of the previous bulge)
-        for (int64_t k = c + 1 + warp; k < r0; k += HT / 32) {
-          double2 y0 = czero(), y1 = czero();
-          if (lane < len) y0 = __ldcg(M(r0 + lane, k));
-          if (lane + 32 < len) y1 = __ldcg(M(r0 + lane + 32, k));
-          double2 sdot = cadd(cmulc(sv[lane], y0), cmulc(sv[lane + 32], y1));   // v^H y
-          sdot = warp_sum2(sdot);
-          const double2 f = cmul(ctau, sdot);
-          if (lane < len) *M(r0 + lane, k) = csub(y0, cmul(sv[lane], f));
-          if (lane + 32 < len) *M(r0 + lane + 32, k) = csub(y1, cmul(sv[lane + 32], f));
+        // ---- (a) left application to columns c < k < r0 (rest of the previous bulge),
+        //      4 columns per warp in flight (loads first, then the reductions)
+        for (int64_t k0 = c + 1 + 4 * warp; k0 < r0; k0 += 4 * (HT / 32)) {
+          double2 y0[4], y1[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int64_t k = k0 + u;
+            y0[u] = (k < r0 && lane < len) ? __ldcg(M(r0 + lane, k)) : czero();
+            y1[u] = (k < r0 && lane + 32 < len) ? __ldcg(M(r0 + lane + 32, k)) : czero();
+          }
+          const double2 va = sv[lane], vb = sv[lane + 32];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int64_t k = k0 + u;
+            double2 sdot = cadd(cmulc(va, y0[u]), cmulc(vb, y1[u]));   // v^H y
+            sdot = warp_sum2(sdot);
+            const double2 f = cmul(ctau, sdot);
+            if (k < r0) {
+              if (lane < len) *M(r0 + lane, k) = csub(y0[u], cmul(va, f));
+              if (lane + 32 < len) *M(r0 + lane + 32, k) = csub(y1[u], cmul(vb, f));
+            }
+          }
         }
+        mark(2);
         // ---- (b) two-sided on the diagonal block
-        for (int e = tid; e < len * len; e += HT) {
-          const int rr = e % len, cc = e / len;
-          if (rr >= cc) {
-            double2 d = __ldcg(M(r0 + rr, r0 + cc));
-            if (rr == cc) d.y = 0.0;
-            sD[rr + cc * 65] = d;
-            sD[cc + rr * 65] = cconj(d);
+        {
+          // thread (rr, cq): rows rr, columns cq, cq+4, ... ; all 16 loads in flight at once
+          const int rr = tid & 63, cq = tid >> 6;
+          double2 dv[16];
+#pragma unroll
+          for (int u = 0; u < 16; u++) {
+            const int cc = cq + 4 * u;
+            dv[u] = (rr < len && cc <= rr) ? __ldcg(M(r0 + rr, r0 + cc)) : czero();
+          }
+#pragma unroll
+          for (int u = 0; u < 16; u++) {
+            const int cc = cq + 4 * u;
+            if (rr < len && cc <= rr) {
+              double2 d = dv[u];
+              if (rr == cc) d.y = 0.0;
+              sD[rr + cc * 65] = d;
+              sD[cc + rr * 65] = cconj(d);
+            }
           }
         }
         __syncthreads();
@@ -150,33 +187,54 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
           for (int t = lane; t < len; t += 32) sp[t] = cadd(sp[t], cmul(al, sv[t]));
         }
         __syncthreads();
-        for (int e = tid; e < len * len; e += HT) {
-          const int rr = e % len, cc = e / len;
-          if (rr >= cc) {
-            double2 d = sD[rr + cc * 65];
-            d = csub(d, cadd(cmul(sv[rr], cconj(sp[cc])), cmul(sp[rr], cconj(sv[cc]))));
-            if (rr == cc) d.y = 0.0;
-            *M(r0 + rr, r0 + cc) = d;
+        {
+          const int rr = tid & 63, cq = tid >> 6;
+          const double2 vr = sv[rr], pr = sp[rr];
+#pragma unroll
+          for (int u = 0; u < 16; u++) {
+            const int cc = cq + 4 * u;
+            if (rr < len && cc <= rr) {
+              double2 d = sD[rr + cc * 65];
+              d = csub(d, cadd(cmul(vr, cconj(sp[cc])), cmul(pr, cconj(sv[cc]))));
+              if (rr == cc) d.y = 0.0;
+              *M(r0 + rr, r0 + cc) = d;
+            }
           }
         }
+        mark(3);
         // ---- (c) right application to rows r1 < k <= min(r1 + nb, n-1)
         const int64_t kend = imin64(r1 + nb, n - 1);
-        for (int64_t k = r1 + 1 + warp; k <= kend; k += HT / 32) {
-          double2 y0 = czero(), y1 = czero();
-          if (lane < len) y0 = __ldcg(M(k, r0 + lane));
-          if (lane + 32 < len) y1 = __ldcg(M(k, r0 + lane + 32));
-          double2 t = cadd(cmul(y0, sv[lane]), cmul(y1, sv[lane + 32]));   // y v
-          t = warp_sum2(t);
-          const double2 f = cmul(t, tau);
-          if (lane < len) *M(k, r0 + lane) = csub(y0, cmul(f, cconj(sv[lane])));
-          if (lane + 32 < len) *M(k, r0 + lane + 32) = csub(y1, cmul(f, cconj(sv[lane + 32])));
+        for (int64_t k0 = r1 + 1 + 4 * warp; k0 <= kend; k0 += 4 * (HT / 32)) {
+          double2 y0[4], y1[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int64_t k = k0 + u;
+            y0[u] = (k <= kend && lane < len) ? __ldcg(M(k, r0 + lane)) : czero();
+            y1[u] = (k <= kend && lane + 32 < len) ? __ldcg(M(k, r0 + lane + 32)) : czero();
+          }
+          const double2 va = sv[lane], vb = sv[lane + 32];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int64_t k = k0 + u;
+            double2 t = cadd(cmul(y0[u], va), cmul(y1[u], vb));   // y v
+            t = warp_sum2(t);
+            const double2 f = cmul(t, tau);
+            if (k <= kend) {
+              if (lane < len) *M(k, r0 + lane) = csub(y0[u], cmul(f, cconj(va)));
+              if (lane + 32 < len) *M(k, r0 + lane + 32) = csub(y1[u], cmul(f, cconj(vb)));
+            }
+          }
         }
       }
+      mark(4);
       __threadfence();
       __syncthreads();
       if (tid == 0) st_release_i32(a.progress + i, (int)(j + 1));
+      mark(5);
     }
   }
+  if (prof)
+    for (int k = 0; k < 6; k++) atomicAdd(&a.prof[16 + k], (unsigned long long)tacc[k]);
 }
 
 __global__ void band_in_kernel(int64_t n, int nb, const double2 *A, int64_t lda, double2 *AB, int ldab) {
@@ -225,6 +283,7 @@ int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d,
     a.tau2 = tau2;
     a.off = d_off;
     a.progress = prog;
+    a.prof = ctx.q2_prof;
     const int64_t J = (n - 2) / nb + 1;   // steps of sweep 0
     const int P = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, std::min<int64_t>(n - 1, J / 3 + 2)));
     void *args[] = {&a};

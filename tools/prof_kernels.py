@@ -84,6 +84,10 @@ def main():
         s.he2hb(A0)
         ms = timeit(lambda: s.hb2st(A0), a.reps)
         print(f"hb2st n={n} nb={a.nb}: {ms:.3f} ms  band bytes {n * (2 * a.nb + 2) * 16 / 1e6:.1f} MB")
+        if os.environ.get("EIG_Q2_PROFILE"):
+            pr = s.q2_profile()[16:22]
+            tot = sum(pr)
+            print("  hb2st CTA0 (wait, refl, a, b, c, flag):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
     elif a.mode == "he2hb":
         A0 = colmajor(synth.rand_hermitian(n, 0), dev)
         A = A0.clone()
