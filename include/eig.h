@@ -114,6 +114,15 @@ int eig_apply_q2(eig_handle h, int64_t n, const void *V2, const void *tau2, cons
  * the handle; library workspace holds a (2nb+2) x n band copy. */
 int eig_hb2st(eig_handle h, int64_t n, const void *A, int64_t lda, double *d, double *e, void *V2, void *tau2);
 
+/* ------------------------------------------------------------------ NEXT-2
+ * Real symmetric tridiagonal eigensolver by divide and conquer:
+ * d[n] diagonal, e[n-1] sub-diagonal (device, not modified).  w[n] receives
+ * all eigenvalues ascending; Z (n x (iu-il+1), ldz >= n, real binary64)
+ * the orthonormal eigenvectors of eigenvalues il..iu (1-based); only those
+ * are formed at the last merge.  Library workspace ~5 n^2 doubles. */
+int eig_stedc(eig_handle h, int64_t n, const double *d, const double *e, int64_t il, int64_t iu, double *w, double *Z,
+              int64_t ldz);
+
 /* ------------------------------------------------------------------ a8
  * E <- L^-H E (Algorithm 1 step 4): L n x n lower triangular
  * (non-unit; only the lower triangle read), E n x m. */

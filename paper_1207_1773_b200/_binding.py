@@ -61,6 +61,7 @@ def lib():
             "eig_solve_gen": (C.c_int, [h, I, P, I, P, I, C.c_int, D, I, I, P, P, I, P]),
             "eig_debug_q2_profile": (C.c_int, [h, P]),
             "eig_hb2st": (C.c_int, [h, I, P, I, P, P, P, P]),
+            "eig_stedc": (C.c_int, [h, I, P, P, I, I, P, P, I]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -73,7 +74,7 @@ def lib():
 def exported_symbols():
     return ["eig_init", "eig_finalize", "eig_strerror", "eig_last_cuda_error", "eig_launch_count", "eig_sync",
             "eig_num_panels", "eig_v2_slots", "eig_he2hb", "eig_apply_q1", "eig_apply_q2", "eig_trsm_lh",
-            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile", "eig_hb2st"]
+            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile", "eig_hb2st", "eig_stedc"]
 
 
 def num_panels(n: int, nb: int) -> int:
@@ -183,6 +184,16 @@ class Solver:
         tau2 = torch.zeros(max(slots, 1), dtype=torch.complex128, device=A.device)
         self._check(lib().eig_hb2st(self.h, n, _ptr(A), _ld(A), _ptr(d), _ptr(e), _ptr(V2), _ptr(tau2)))
         return d[:n], e[:max(n - 1, 0)], V2[:slots], tau2[:slots]
+
+    def stedc(self, d, e, il=1, iu=None):
+        """NEXT-2: tridiagonal D&C.  Returns (w [n] all eigenvalues, Z [n, iu-il+1] real)."""
+        n = d.shape[0]
+        iu = n if iu is None else iu
+        w = torch.zeros(max(n, 1), dtype=torch.float64, device=d.device)
+        Z = empty_colmajor(n, iu - il + 1, dtype=torch.float64, device=d.device)
+        e_ = e if e.numel() > 0 else torch.zeros(1, dtype=torch.float64, device=d.device)
+        self._check(lib().eig_stedc(self.h, n, _ptr(d), _ptr(e_), il, iu, _ptr(w), _ptr(Z), _ld(Z)))
+        return w[:n], Z
 
     def apply_q1(self, A, T, E):
         n, m = E.shape

@@ -468,6 +468,16 @@ int eig_hb2st(eig_handle h, int64_t n, const void *A, int64_t lda, double *d, do
   return hb2st(c, n, c.nb, (const double2 *)A, lda, d, e, (double2 *)V2, (double2 *)tau2, d_off);
 }
 
+int eig_stedc(eig_handle h, int64_t n, const double *d, const double *e, int64_t il, int64_t iu, double *w, double *Z,
+              int64_t ldz) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (n > 0 && (il < 1 || iu > n || il > iu)) return -5;
+  if (ldz < std::max<int64_t>(1, n)) return -9;
+  cudaSetDevice(h->c.device);
+  return stedc(h->c, n, d, e, il, iu, w, Z, ldz);
+}
+
 int eig_zgemm(eig_handle h, char opa, char opb, int64_t M, int64_t N, int64_t K, double alpha, const void *A,
               int64_t lda, const void *B, int64_t ldb, double beta, void *C, int64_t ldc, int herm_a, int lower_c) {
   EIG_TRY(valid(h));

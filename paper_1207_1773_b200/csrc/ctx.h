@@ -27,6 +27,8 @@ enum WsId {
   WS_BAND,        // hb2st band buffer (2nb+2 diagonals)
   WS_HBPROG,      // hb2st sweep progress flags
   WS_HBOFF,       // hb2st V2 slot offsets
+  WS_DC,          // stedc buffers
+  WS_DC_SMALL,    // stedc per-level node tables
   WS_HOST_A, WS_HOST_V2, WS_HOST_TAU2, WS_HOST_L, WS_HOST_Z, WS_HOST_E, WS_HOST_TAU1, WS_HOST_T1,
   WS_COUNT
 };

@@ -54,6 +54,28 @@ int real_diag(Ctx &ctx, int64_t n, double2 *A, int64_t lda);
 int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d, double *e, double2 *V2,
           double2 *tau2, const int64_t *d_off);
 
+// ------------------------------------------------------------- real grouped GEMM
+struct DgemmProb {
+  int64_t M, N, K;
+  const double *A;
+  int64_t lda;
+  const double *B;
+  int64_t ldb;
+  double *C;
+  int64_t ldc;
+};
+// C_p = A_p B_p for each problem of the device array d_probs; max_tiles =
+// max over p of dgemm_tiles(M_p, N_p).
+int dgemm_group(Ctx &ctx, const DgemmProb *d_probs, int nprob, int max_tiles);
+int dgemm_tiles(int64_t M, int64_t N);
+
+// ------------------------------------------------------------- stedc (NEXT-2)
+// Divide and conquer for the real symmetric tridiagonal (d, e): all
+// eigenvalues ascending into w[n]; eigenvectors of indices il..iu (1-based)
+// into Z (n x (iu-il+1), ldz).  d, e are device arrays (not modified).
+int stedc(Ctx &ctx, int64_t n, const double *d, const double *e, int64_t il, int64_t iu, double *w, double *Z,
+          int64_t ldz);
+
 // ------------------------------------------------------------- Q2
 struct Q2Plan {
   int64_t n = 0;
