@@ -39,6 +39,11 @@ extern "C" {
 #define EIG_ERR_STATE   (-1004)
 #define EIG_ERR_NOTIMPL (-1005)
 
+/* eig_solve_gen ranges (reading R12: "fraction" = the lowest ceil(f n)) */
+#define EIG_RANGE_ALL      0
+#define EIG_RANGE_FRACTION 1
+#define EIG_RANGE_INDEX    2
+
 /* eig_hotpath flags */
 #define EIG_HOST_BUFFERS 1u  /* pointers are host memory: copy in, run, copy E out (synchronous) */
 #define EIG_SKIP_HE2HB   2u  /* back-transform only (A already holds he2hb output + T1)        */
@@ -161,8 +166,33 @@ int eig_zgemm(eig_handle h, char opa, char opb, int64_t M, int64_t N, int64_t K,
  * eig_init (else EIG_ERR_NOTIMPL).  out16: host array of 32. */
 int eig_debug_q2_profile(eig_handle h, unsigned long long *out16);
 
-/* Generalized solver (Algorithm 1).  Needs the NEXT stages
- * (device hb2st, stedc, potrf/hegst); returns EIG_ERR_NOTIMPL in this build. */
+/* ------------------------------------------------------------------ NEXT-3
+ * Cholesky B = L L^H (Algorithm 1 step 1), blocked, in place: the
+ * lower triangle of B (n x n, ldb) is replaced by L (strict upper not
+ * referenced).  Synchronous.  Returns 0, or n + j if the leading minor of
+ * order j is not positive definite (LAPACK zhegv INFO convention, R11). */
+int eig_potrf(eig_handle h, int64_t n, void *B, int64_t ldb);
+
+/* Standard form A' = L^-1 A L^-H (Algorithm 1 step 2): A (lower
+ * read) is overwritten by A' (full Hermitian storage, imag(diag) = 0);
+ * L lower from eig_potrf.  Library workspace: n^2 complex128. */
+int eig_hegst(eig_handle h, int64_t n, void *A, int64_t lda, const void *L, int64_t ldl);
+
+/* ------------------------------------------------------------------ Algorithm 1
+ * Generalized solver A x = lambda B x (Algorithm 1, with the
+ * two-stage Algorithm 2, and the D&C tridiagonal solver, §4.3):
+ * potrf -> hegst -> he2hb -> hb2st -> stedc (last merge restricted to il..iu)
+ * -> Z = L^-H Q1 Q2 Z'.
+ *   A   [in/destroyed] n x n (lda), Hermitian, lower read.
+ *   B   [in/out] n x n (ldb), HPD, lower read; overwritten by L.
+ *   range EIG_RANGE_ALL | EIG_RANGE_FRACTION (0 < fraction <= 1: il = 1,
+ *       iu = ceil(fraction n)) | EIG_RANGE_INDEX (1 <= il <= iu <= n).
+ *   w   [out, device] n binary64: all eigenvalues ascending.
+ *   Z   [out, device] n x m complex128 (ldz >= n), m = iu - il + 1, the
+ *       B-orthonormal eigenvectors of eigenvalues il..iu.
+ *   m_out [out, host, nullable] m.
+ * Synchronous.  Returns 0, -i (illegal argument i), n + j (B not PD), or a
+ * library error code. */
 int eig_solve_gen(eig_handle h, int64_t n, void *A, int64_t lda, void *B, int64_t ldb, int range, double fraction,
                   int64_t il, int64_t iu, double *w, void *Z, int64_t ldz, int64_t *m_out);
 

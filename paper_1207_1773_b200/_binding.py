@@ -19,6 +19,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libeigb200.so")
 
+EIG_RANGE_ALL, EIG_RANGE_FRACTION, EIG_RANGE_INDEX = 0, 1, 2
 EIG_HOST_BUFFERS = 1
 EIG_SKIP_HE2HB = 2
 EIG_SKIP_BT = 4
@@ -62,6 +63,8 @@ def lib():
             "eig_debug_q2_profile": (C.c_int, [h, P]),
             "eig_hb2st": (C.c_int, [h, I, P, I, P, P, P, P]),
             "eig_stedc": (C.c_int, [h, I, P, P, I, I, P, P, I]),
+            "eig_potrf": (C.c_int, [h, I, P, I]),
+            "eig_hegst": (C.c_int, [h, I, P, I, P, I]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -74,7 +77,7 @@ def lib():
 def exported_symbols():
     return ["eig_init", "eig_finalize", "eig_strerror", "eig_last_cuda_error", "eig_launch_count", "eig_sync",
             "eig_num_panels", "eig_v2_slots", "eig_he2hb", "eig_apply_q1", "eig_apply_q2", "eig_trsm_lh",
-            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile", "eig_hb2st", "eig_stedc"]
+            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile", "eig_hb2st", "eig_stedc", "eig_potrf", "eig_hegst"]
 
 
 def num_panels(n: int, nb: int) -> int:
@@ -194,6 +197,42 @@ class Solver:
         e_ = e if e.numel() > 0 else torch.zeros(1, dtype=torch.float64, device=d.device)
         self._check(lib().eig_stedc(self.h, n, _ptr(d), _ptr(e_), il, iu, _ptr(w), _ptr(Z), _ld(Z)))
         return w[:n], Z
+
+    def potrf(self, B):
+        """NEXT-3: B <- L (lower) in place.  Returns LAPACK-style info (0 or n + j)."""
+        n = B.shape[0]
+        rc = lib().eig_potrf(self.h, n, _ptr(B), _ld(B))
+        if rc < 0:
+            self._check(rc)
+        return rc
+
+    def hegst(self, A, L):
+        """NEXT-3: A <- L^-1 A L^-H (full Hermitian storage)."""
+        n = A.shape[0]
+        self._check(lib().eig_hegst(self.h, n, _ptr(A), _ld(A), _ptr(L), _ld(L)))
+        return A
+
+    def solve_gen(self, A, B, fraction=None, il=None, iu=None):
+        """Algorithm 1: A x = lambda B x.  A, B device column-major complex128
+        (lower read; both destroyed, B <- L).  Returns (w [n], Z [n, m]).
+        Raises EigError on failure (info n + j: B not positive definite)."""
+        n = A.shape[0]
+        if fraction is not None:
+            rng, f, a, b = EIG_RANGE_FRACTION, float(fraction), 0, 0
+            m = max(1, min(n, int(np.ceil(fraction * n))))
+        elif il is not None:
+            rng, f, a, b = EIG_RANGE_INDEX, 0.0, il, iu
+            m = iu - il + 1
+        else:
+            rng, f, a, b = EIG_RANGE_ALL, 0.0, 0, 0
+            m = n
+        w = torch.zeros(max(n, 1), dtype=torch.float64, device=A.device)
+        Z = empty_colmajor(n, m, device=A.device)
+        mo = C.c_int64(0)
+        rc = lib().eig_solve_gen(self.h, n, _ptr(A), _ld(A), _ptr(B), _ld(B), rng, f, a, b, _ptr(w), _ptr(Z), _ld(Z),
+                                 C.byref(mo))
+        self._check(rc)
+        return w[:n], Z[:, :mo.value]
 
     def apply_q1(self, A, T, E):
         n, m = E.shape

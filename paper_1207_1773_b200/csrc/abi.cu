@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -246,6 +247,53 @@ static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2
     }
   }
   return 0;
+}
+
+// E <- L^-1 E (forward substitution, left, lower, no transpose), two-level like trsm_lh.
+static int trsm_ln_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2 *E, int64_t lde, int64_t m) {
+  if (n <= 0 || m <= 0) return 0;
+  const int bs = 64, BS = 256;
+  const int64_t nblk = (n + bs - 1) / bs;
+  double2 *Linv = (double2 *)c.ws(WS_LINV, (size_t)nblk * bs * bs * sizeof(double2));
+  if (!Linv) return EIG_ERR_NOMEM;
+  EIG_TRY(trinv_blocks(c, n, bs, L, ldl, Linv));
+  for (int64_t I0 = 0; I0 < n; I0 += BS) {
+    const int64_t I1 = std::min<int64_t>(n, I0 + BS);
+    Zgemm g;
+    if (I0 > 0) {
+      g.M = I1 - I0; g.N = m; g.K = I0; g.A = L + I0; g.lda = ldl; g.B = E; g.ldb = lde; g.C = E + I0; g.ldc = lde;
+      g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+    }
+    for (int64_t i0 = I0; i0 < I1; i0 += bs) {
+      const int64_t i1 = std::min<int64_t>(I1, i0 + bs), bi = i1 - i0;
+      if (i0 > I0) {
+        g = Zgemm();
+        g.M = bi; g.N = m; g.K = i0 - I0; g.A = L + i0 + I0 * ldl; g.lda = ldl; g.B = E + I0; g.ldb = lde;
+        g.C = E + i0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0;
+        EIG_TRY(zgemm(c, g));
+      }
+      g = Zgemm();   // in place: single 64-row M tile, no split-K
+      g.M = bi; g.N = m; g.K = bi; g.A = Linv + (i0 / bs) * bs * bs; g.lda = bs; g.B = E + i0; g.ldb = lde;
+      g.C = E + i0; g.ldc = lde; g.splitk = 1;
+      EIG_TRY(zgemm(c, g));
+    }
+  }
+  return 0;
+}
+
+// A' = L^-1 A L^-H = L^-1 (L^-1 A)^H  (A' Hermitian), Algorithm 1 step 2.
+static int hegst_run(Ctx &c, int64_t n, double2 *A, int64_t lda, const double2 *L, int64_t ldl) {
+  if (n <= 0) return 0;
+  double2 *Y = (double2 *)c.ws(WS_GST, (size_t)n * n * sizeof(double2));
+  if (!Y) return EIG_ERR_NOMEM;
+  EIG_TRY(herm_full(c, n, A, lda));
+  EIG_TRY(trsm_ln_run(c, n, L, ldl, A, lda, n));        // X = L^-1 A
+  EIG_TRY(conj_transpose(c, n, A, lda, Y, n));          // Y = X^H
+  EIG_TRY(trsm_ln_run(c, n, L, ldl, Y, n, n));          // A' = L^-1 X^H
+  EIG_TRY(c.check(cudaMemcpy2DAsync(A, lda * sizeof(double2), Y, n * sizeof(double2), n * sizeof(double2), n,
+                                    cudaMemcpyDeviceToDevice, c.stream), "copy A'"));
+  return real_diag(c, n, A, lda);
 }
 
 // ------------------------------------------------------------------ Q2
@@ -558,12 +606,87 @@ int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void 
   return 0;
 }
 
+int eig_potrf(eig_handle h, int64_t n, void *B, int64_t ldb) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (ldb < std::max<int64_t>(1, n)) return -4;
+  Ctx &c = h->c;
+  cudaSetDevice(c.device);
+  int64_t *d_info = (int64_t *)c.ws(WS_INFO, 64);
+  if (!d_info) return EIG_ERR_NOMEM;
+  EIG_TRY(c.check(cudaMemsetAsync(d_info, 0, sizeof(int64_t), c.stream), "info"));
+  EIG_TRY(potrf_lower(c, n, (double2 *)B, ldb, d_info));
+  int64_t info = 0;
+  EIG_TRY(c.check(cudaMemcpyAsync(&info, d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream), "info"));
+  EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync"));
+  return (int)info;
+}
+
+int eig_hegst(eig_handle h, int64_t n, void *A, int64_t lda, const void *L, int64_t ldl) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (lda < std::max<int64_t>(1, n)) return -4;
+  if (ldl < std::max<int64_t>(1, n)) return -6;
+  cudaSetDevice(h->c.device);
+  return hegst_run(h->c, n, (double2 *)A, lda, (const double2 *)L, ldl);
+}
+
 int eig_solve_gen(eig_handle h, int64_t n, void *A, int64_t lda, void *B, int64_t ldb, int range, double fraction,
                   int64_t il, int64_t iu, double *w, void *Z, int64_t ldz, int64_t *m_out) {
-  (void)n; (void)A; (void)lda; (void)B; (void)ldb; (void)range; (void)fraction; (void)il; (void)iu; (void)w; (void)Z;
-  (void)ldz; (void)m_out;
   EIG_TRY(valid(h));
-  return EIG_ERR_NOTIMPL;
+  Ctx &c = h->c;
+  if (n < 0) return -2;
+  if (lda < std::max<int64_t>(1, n)) return -4;
+  if (ldb < std::max<int64_t>(1, n)) return -6;
+  if (range == EIG_RANGE_ALL) {
+    il = 1;
+    iu = n;
+  } else if (range == EIG_RANGE_FRACTION) {
+    if (!(fraction > 0.0 && fraction <= 1.0)) return -8;
+    il = 1;
+    iu = (int64_t)std::ceil(fraction * (double)n);
+    iu = std::max<int64_t>(1, std::min<int64_t>(n, iu));
+  } else if (range == EIG_RANGE_INDEX) {
+    if (il < 1 || il > std::max<int64_t>(1, n)) return -9;
+    if (iu < il || iu > n) return -10;
+  } else {
+    return -7;
+  }
+  if (ldz < std::max<int64_t>(1, n)) return -13;
+  if (n == 0) {
+    if (m_out) *m_out = 0;
+    return 0;
+  }
+  cudaSetDevice(c.device);
+  const int64_t m = iu - il + 1;
+  const int nb = c.nb;
+  // step 1: B = L L^H
+  int rc = eig_potrf(h, n, B, ldb);
+  if (rc) return rc;
+  double2 *dA = (double2 *)A, *dL = (double2 *)B;
+  // step 2: A' = L^-1 A L^-H
+  EIG_TRY(hegst_run(c, n, dA, lda, dL, ldb));
+  // step 3: two-stage standard eigensolver
+  const int64_t K = num_panels(n, nb), slots = v2_slots(n, nb);
+  double2 *tau1 = (double2 *)c.ws(WS_SG_TAU1, (size_t)std::max<int64_t>(K, 1) * nb * sizeof(double2));
+  double2 *T1 = (double2 *)c.ws(WS_SG_T1, (size_t)std::max<int64_t>(K, 1) * nb * nb * sizeof(double2));
+  double *dd = (double *)c.ws(WS_SG_D, (size_t)n * sizeof(double));
+  double *de = (double *)c.ws(WS_SG_E, (size_t)n * sizeof(double));
+  double2 *V2 = (double2 *)c.ws(WS_SG_V2, (size_t)std::max<int64_t>(slots, 1) * nb * sizeof(double2));
+  double2 *tau2 = (double2 *)c.ws(WS_SG_TAU2, (size_t)std::max<int64_t>(slots, 1) * sizeof(double2));
+  double *Zr = (double *)c.ws(WS_SG_Z, (size_t)n * m * sizeof(double));
+  if (!tau1 || !T1 || !dd || !de || !V2 || !tau2 || !Zr) return EIG_ERR_NOMEM;
+  EIG_TRY(he2hb_run(c, n, dA, lda, tau1, T1));
+  EIG_TRY(eig_hb2st(h, n, dA, lda, dd, de, V2, tau2));
+  EIG_TRY(stedc(c, n, dd, de, il, iu, w, Zr, n));
+  // step 3 back-transform and step 4: Z = L^-H Q1 Q2 complex(Zr)
+  EIG_TRY(complexify(c, n, m, Zr, n, (double2 *)Z, ldz));
+  if (c.q2g >= 4) EIG_TRY(apply_q2_run(c, n, V2, tau2, (double2 *)Z, ldz, m));
+  else if (n > 1) return EIG_ERR_NOTIMPL;
+  EIG_TRY(apply_q1_run(c, n, dA, lda, T1, (double2 *)Z, ldz, m));
+  EIG_TRY(trsm_lh_run(c, n, dL, ldb, (double2 *)Z, ldz, m));
+  if (m_out) *m_out = m;
+  return c.check(cudaStreamSynchronize(c.stream), "sync");
 }
 
 }  // extern "C"

@@ -29,6 +29,10 @@ enum WsId {
   WS_HBOFF,       // hb2st V2 slot offsets
   WS_DC,          // stedc buffers
   WS_DC_SMALL,    // stedc per-level node tables
+  WS_FRONT,       // potrf diagonal-block inverse
+  WS_GST,         // hegst n x n scratch
+  WS_INFO,        // device info word
+  WS_SG_TAU1, WS_SG_T1, WS_SG_D, WS_SG_E, WS_SG_V2, WS_SG_TAU2, WS_SG_Z,   // solve_gen stage buffers
   WS_HOST_A, WS_HOST_V2, WS_HOST_TAU2, WS_HOST_L, WS_HOST_Z, WS_HOST_E, WS_HOST_TAU1, WS_HOST_T1,
   WS_COUNT
 };

@@ -1,0 +1,159 @@
+// frontend.cu — NEXT-3 front end: Cholesky B = L L^H (Algorithm 1 step 1,
+// P:L66) and the standard-form transform A' = L^-1 A L^-H (step 2),
+// plus the forward triangular solve they need.
+//
+// potrf: blocked right-looking, 64-column panels: the diagonal block is
+// factored (and inverted) by one CTA in shared memory, the panel below it is
+// L21 = A21 L11^-H (one DMMA GEMM with the inverse), the trailing matrix gets
+// the Hermitian rank-64 update on the lower triangle.
+// hegst: A' = L^-1 (L^-1 A)^H, which is Hermitian, computed as two blocked
+// forward solves with n right-hand sides (GEMM-rich and fully parallel; twice
+// the flops of LAPACK's zhegst but no sequential trailing solves).
+#include <algorithm>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "kernels.h"
+
+namespace eig {
+namespace {
+
+constexpr int FB = 64;
+
+// Factor the b x b Hermitian diagonal block (lower) in place and write its
+// inverse (lower, zeros above) to Linv (ld 64).  info (1-based global pivot
+// index, + n) is set on the first non-positive pivot.
+__global__ void __launch_bounds__(256) potrf_diag_kernel(double2 *A11, int64_t lda, int b, double2 *Linv,
+                                                         int64_t gofs, int64_t n, int64_t *info) {
+  extern __shared__ __align__(16) double2 fsm[];
+  double2 *L = fsm;                  // [64][65]
+  double2 *X = fsm + 64 * 65;        // [64][65]
+  __shared__ double s_piv;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < b * b; e += 256) {
+    const int r = e % b, c = e / b;
+    L[r + c * 65] = (r >= c) ? A11[r + c * lda] : czero();
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int j = 0; j < b; j++) {
+    if (tid == 0) {
+      const double d = L[j + j * 65].x;
+      if (!(d > 0.0) || !isfinite(d)) {
+        if (!s_bad) {
+          s_bad = 1;
+          atomicCAS(reinterpret_cast<unsigned long long *>(info), 0ull, (unsigned long long)(n + gofs + j + 1));
+        }
+        s_piv = 1.0;
+      } else {
+        s_piv = sqrt(d);
+      }
+      L[j + j * 65] = make_double2(s_piv, 0.0);
+    }
+    __syncthreads();
+    const double inv = 1.0 / s_piv;
+    for (int i = j + 1 + tid; i < b; i += 256) L[i + j * 65] = cscale(inv, L[i + j * 65]);
+    __syncthreads();
+    const int m = b - j - 1;
+    for (int e = tid; e < m * m; e += 256) {
+      const int i = j + 1 + e % m, k = j + 1 + e / m;
+      if (i >= k) L[i + k * 65] = csub(L[i + k * 65], cmul(L[i + j * 65], cconj(L[k + j * 65])));
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += 256) {
+    const int r = e % b, c = e / b;
+    if (r >= c) A11[r + c * lda] = L[r + c * 65];
+  }
+  // inverse: column c by forward substitution
+  if (tid < b) {
+    const int c = tid;
+    for (int r = 0; r < b; r++) {
+      double2 s = (r == c) ? make_double2(1.0, 0.0) : czero();
+      if (r >= c) {
+        for (int k = c; k < r; k++) s = csub(s, cmul(L[r + k * 65], X[k + c * 65]));
+        const double2 d = L[r + r * 65];
+        s = make_double2(s.x / d.x, s.y / d.x);   // diagonal is real positive
+      } else {
+        s = czero();
+      }
+      X[r + c * 65] = s;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < FB * FB; e += 256) {
+    const int r = e % FB, c = e / FB;
+    Linv[r + c * FB] = (r < b && c < b) ? X[r + c * 65] : czero();
+  }
+}
+
+// Full Hermitian from the lower triangle (imag(diag) = 0): upper <- conj(lower)^T.
+__global__ void herm_full_kernel(int64_t n, double2 *A, int64_t lda) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % n, c = e / n;
+    if (r < c) A[r + c * lda] = cconj(A[c + r * lda]);
+    else if (r == c) A[r + c * lda].y = 0.0;
+  }
+}
+
+// Y = X^H (n x n, tiled transpose through shared memory)
+__global__ void conj_transpose_kernel(int64_t n, const double2 *X, int64_t ldx, double2 *Y, int64_t ldy) {
+  __shared__ double2 t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + k;
+    if (r < n && c < n) t[k][threadIdx.x] = X[r + c * ldx];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = c0 + threadIdx.x, c = r0 + k;   // Y[r, c] = conj(X[c, r])
+    if (r < n && c < n) Y[r + c * ldy] = cconj(t[threadIdx.x][k]);
+  }
+}
+
+}  // namespace
+
+int potrf_lower(Ctx &c, int64_t n, double2 *B, int64_t ldb, int64_t *d_info) {
+  double2 *Linv = (double2 *)c.ws(WS_FRONT, (size_t)FB * FB * sizeof(double2));
+  if (!Linv) return EIG_ERR_NOMEM;
+  static bool attr = false;
+  const size_t smem = (size_t)2 * 64 * 65 * sizeof(double2);
+  if (!attr) {
+    EIG_TRY(c.check(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                    "potrf attr"));
+    attr = true;
+  }
+  for (int64_t k = 0; k < n; k += FB) {
+    const int b = (int)std::min<int64_t>(FB, n - k);
+    double2 *A11 = B + k + k * ldb;
+    potrf_diag_kernel<<<1, 256, smem, c.stream>>>(A11, ldb, b, Linv, k, n, d_info);
+    EIG_TRY(c.launched("potrf_diag_kernel"));
+    const int64_t s = n - k - b;
+    if (s <= 0) break;
+    Zgemm g;   // L21 = A21 L11^-H   (in place: one 64-col N tile, no split-K)
+    g.opb = OP_C; g.M = s; g.N = b; g.K = b; g.A = A11 + b; g.lda = ldb; g.B = Linv; g.ldb = FB; g.C = A11 + b;
+    g.ldc = ldb; g.splitk = 1;
+    EIG_TRY(zgemm(c, g));
+    g = Zgemm();   // A22 -= L21 L21^H (lower)
+    g.opb = OP_C; g.lower_c = 1; g.M = s; g.N = s; g.K = b; g.A = A11 + b; g.lda = ldb; g.B = A11 + b; g.ldb = ldb;
+    g.C = A11 + b + b * ldb; g.ldc = ldb; g.alpha = -1.0; g.beta = 1.0;
+    EIG_TRY(zgemm(c, g));
+  }
+  return 0;
+}
+
+int herm_full(Ctx &c, int64_t n, double2 *A, int64_t lda) {
+  const int64_t total = n * n;
+  herm_full_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 16LL * c.num_sms), 256, 0, c.stream>>>(n, A, lda);
+  return c.launched("herm_full_kernel");
+}
+
+int conj_transpose(Ctx &c, int64_t n, const double2 *X, int64_t ldx, double2 *Y, int64_t ldy) {
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+  conj_transpose_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(n, X, ldx, Y, ldy);
+  return c.launched("conj_transpose_kernel");
+}
+
+}  // namespace eig

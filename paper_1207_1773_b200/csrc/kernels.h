@@ -76,6 +76,11 @@ int dgemm_tiles(int64_t M, int64_t N);
 int stedc(Ctx &ctx, int64_t n, const double *d, const double *e, int64_t il, int64_t iu, double *w, double *Z,
           int64_t ldz);
 
+// ------------------------------------------------------------- front end (NEXT-3)
+int potrf_lower(Ctx &ctx, int64_t n, double2 *B, int64_t ldb, int64_t *d_info);
+int herm_full(Ctx &ctx, int64_t n, double2 *A, int64_t lda);
+int conj_transpose(Ctx &ctx, int64_t n, const double2 *X, int64_t ldx, double2 *Y, int64_t ldy);
+
 // ------------------------------------------------------------- Q2
 struct Q2Plan {
   int64_t n = 0;
