@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-zhegv", action="store_true", help="skip the end-to-end generalized solve timing")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
     a = p.parse_args()
     if a.m is None:
@@ -180,6 +181,66 @@ def run_reference(a, rank, world):
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ------------------------------------------------------------------ zhegv (Algorithm 1 end to end)
+def hpd_on_device(n, kappa, seed, dev, r=8):
+    """G1 B = U^H diag(kappa^(k/(n-1))) U built with torch on the device from
+    synth's seeded reflectors (same recipe as synth.hpd_with_condition)."""
+    import torch
+
+    import synth
+    U = torch.from_numpy(synth.random_reflectors(n, r, seed, 2)).to(dev)
+    d = torch.as_tensor(kappa ** (np.arange(n) / max(n - 1, 1)), dtype=torch.complex128, device=dev)
+    M = torch.diag(d)
+    for t in range(r):
+        u = U[:, t:t + 1]
+        M = M - 2.0 * u @ (u.conj().T @ M)
+        M = M - 2.0 * (M @ u) @ u.conj().T
+    M = 0.5 * (M + M.conj().T)
+    return M.t().contiguous().t()
+
+
+def zhegv_timing(solver, A0, B0, stream):
+    """Seconds of one eig_solve_gen (all eigenvectors) after a warm-up call, plus
+    a per-stage breakdown from the stage entry points (CUDA events)."""
+    import torch
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    A, B = A0.clone(), B0.clone()
+    solver.solve_gen(A, B)
+    A.copy_(A0)
+    B.copy_(B0)
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    w, Z = solver.solve_gen(A, B)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    total = e0.elapsed_time(e1) * 1e-3
+    # stage breakdown (same work through the stage entry points)
+    A.copy_(A0)
+    B.copy_(B0)
+    torch.cuda.synchronize()
+    evs = [ev() for _ in range(7)]
+    evs[0].record(stream)
+    solver.potrf(B)
+    evs[1].record(stream)
+    solver.hegst(A, B)
+    evs[2].record(stream)
+    tau1, T1 = solver.he2hb(A)
+    evs[3].record(stream)
+    d, e, V2, tau2 = solver.hb2st(A)
+    evs[4].record(stream)
+    w2, Zr = solver.stedc(d, e)
+    evs[5].record(stream)
+    solver.apply_q2(V2, tau2, Z, Z=Zr)
+    solver.apply_q1(A, T1, Z)
+    solver.trsm_lh(B, Z)
+    evs[6].record(stream)
+    torch.cuda.synchronize()
+    names = ["potrf", "hegst", "he2hb", "hb2st", "stedc", "backtransform"]
+    stages = {nm: evs[i].elapsed_time(evs[i + 1]) for i, nm in enumerate(names)}
+    return total, stages
 
 
 # ------------------------------------------------------------------ B200 arm
@@ -336,6 +397,17 @@ def run_b200(a, rank, world, local_rank):
         e2e = {"value": flops / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": dt * 1e3, "steps": e_steps}
 
+    zhegv = None
+    if rank == 0 and world == 1 and not a.no_zhegv:
+        del E
+        torch.cuda.empty_cache()
+        B0 = hpd_on_device(n, 1e2, a.seed, dev)
+        zs, zst = zhegv_timing(solver, A0, B0, stream)
+        zhegv = {"seconds": zs, "stages_ms": zst, "n": n, "m": n, "kappa_B": 1e2,
+                 "note": "eig_solve_gen (potrf, hegst, he2hb, hb2st, stedc, Q2, Q1, L^-H), all eigenvectors, "
+                         "one call after a warm-up; stage breakdown from the stage entry points"}
+        del B0
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         v, cores, desc, secs = cpu_sample(n, nb, a.seed, a.cpu_budget, pre=(A_h, V2_h, tau2_h, L_h))
@@ -353,7 +425,7 @@ def run_b200(a, rank, world, local_rank):
                            "input_gen_s": round(t_gen, 1)},
                 "stages_ms": stages, "gpu_launches": launches,
                 "gpu_launches_per_step": launches / max(a.steps, 1), "roofline": roof, "clocks": clk,
-                "e2e": e2e, "cpu_baseline": cpu}
+                "e2e": e2e, "cpu_baseline": cpu, "zhegv": zhegv}
         print(json.dumps(line), flush=True)
     solver.close()
     return 0
