@@ -398,6 +398,29 @@ def run_b200(a, rank, world, local_rank):
                "ms_per_step": dt * 1e3, "steps": e_steps}
 
     zhegv = None
+    if world > 1 and not a.no_zhegv:
+        from paper_1207_1773_b200.dist import solve_gen_sharded
+        del E
+        torch.cuda.empty_cache()
+        B0 = hpd_on_device(n, 1e2, a.seed, dev) if rank == 0 else empty_colmajor(n, n, device=dev)
+        Aw, Bw = A0.clone(), B0.clone()
+        solve_gen_sharded(solver, Aw, Bw, nb)          # warm-up
+        Aw.copy_(A0)
+        Bw.copy_(B0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        z0, z1 = ev(), ev()
+        z0.record(stream)
+        solve_gen_sharded(solver, Aw, Bw, nb)
+        z1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        tt = torch.tensor([z0.elapsed_time(z1) * 1e-3], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        zhegv = {"seconds": float(tt.item()), "n": n, "m": n, "kappa_B": 1e2, "ranks": world,
+                 "note": "rank 0: potrf, hegst, he2hb, hb2st, stedc; NCCL broadcast of the factors; "
+                         "back-transform sharded by eigenvector columns; max over ranks"}
+        del Aw, Bw, B0
     if rank == 0 and world == 1 and not a.no_zhegv:
         del E
         torch.cuda.empty_cache()

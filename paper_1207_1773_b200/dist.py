@@ -46,6 +46,50 @@ def hotpath_sharded(solver, A, tau1, T1, V2, tau2, L, Z_slice, E_slice, group=No
     return E_slice
 
 
+def solve_gen_sharded(solver, A, B, nb: int, group=None):
+    """Algorithm 1 with the back-transform sharded by eigenvector columns
+    (SURVEY.md §8(e), CS2): rank 0 runs potrf, hegst, he2hb, hb2st and stedc;
+    A (band + V1), T1, V2/tau2, L (in B), w and the tridiagonal eigenvectors
+    Z' are broadcast; every rank forms E = L^-H Q1 Q2 Z'[:, slice] for its
+    contiguous column slice.  A, B (n x n column-major) must exist on every
+    rank (contents only matter on rank 0).  Returns (w [n], E_slice, (lo, hi))."""
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    n = A.shape[0]
+    dev = A.device
+    K = 0 if n <= nb else (n - nb - 1) // nb + 1
+    slots = 0
+    j = 0
+    while 1 + j * nb <= n - 1:
+        slots += n - 1 - j * nb
+        j += 1
+    if rank == 0:
+        info = solver.potrf(B)
+        if info:
+            raise RuntimeError(f"B not positive definite (info {info})")
+        solver.hegst(A, B)
+        tau1, T1 = solver.he2hb(A)
+        d, e, V2, tau2 = solver.hb2st(A)
+        w, Zr = solver.stedc(d, e)
+        T1 = T1.contiguous()
+        V2 = V2.contiguous()
+        tau2 = tau2.contiguous()
+        w = w.contiguous()
+    else:
+        T1 = torch.zeros(max(K * nb * nb, 1), dtype=torch.complex128, device=dev)
+        V2 = torch.zeros((slots, nb), dtype=torch.complex128, device=dev)
+        tau2 = torch.zeros(slots, dtype=torch.complex128, device=dev)
+        w = torch.zeros(n, dtype=torch.float64, device=dev)
+        Zr = torch.zeros((n, n), dtype=torch.float64, device=dev).t()
+    broadcast_factors([A, T1, V2, tau2, B, w, Zr], src=0, group=group)
+    lo, hi = column_slice(n, rank, world)
+    E = torch.empty((hi - lo, n), dtype=torch.complex128, device=dev).t()
+    solver.apply_q2(V2, tau2, E, Z=Zr[:, lo:hi])
+    solver.apply_q1(A, T1, E)
+    solver.trsm_lh(B, E)
+    return w, E, (lo, hi)
+
+
 def gather_columns(E_slice: torch.Tensor, m: int, group=None):
     """Gather the column slices to every rank (column-major n x m result)."""
     world = dist.get_world_size(group)

@@ -58,7 +58,31 @@ class OracleSolver:
         E.copy_(torch.from_numpy(oracle.apply_q1(A.numpy(), tau, self.nb, E.numpy())))
 
     def trsm_lh(self, L, E):
-        E.copy_(torch.from_numpy(oracle.backsub_lh(L.numpy(), E.numpy())))
+        E.copy_(torch.from_numpy(oracle.backsub_lh(np.tril(L.numpy()), E.numpy())))
+
+    # front end / tridiagonal stages (for the sharded Algorithm 1)
+    def potrf(self, B):
+        L, info = oracle.potrf(oracle.full_hermitian(B.numpy()))
+        B.copy_(_cm(L))
+        return info
+
+    def hegst(self, A, L):
+        A.copy_(_cm(oracle.std_form(A.numpy(), np.tril(L.numpy()))))
+
+    def hb2st(self, A):
+        n = A.shape[0]
+        Ao = A.numpy()
+        r, c = np.indices((n, n))
+        Bl = np.where((r - c >= 0) & (r - c <= self.nb), Ao, 0)
+        Band = np.tril(Bl) + np.tril(Bl, -1).conj().T
+        Band[np.diag_indices(n)] = Band.diagonal().real
+        d, e, V2, tau2 = oracle.hb2st(Band, self.nb)
+        return torch.from_numpy(d), torch.from_numpy(e.copy()), torch.from_numpy(V2.copy()), torch.from_numpy(tau2.copy())
+
+    def stedc(self, d, e):
+        w, Z, info = oracle.tql2(d.numpy(), e.numpy())
+        assert info == 0
+        return torch.from_numpy(w), _cm(Z)
 
 
 def _cm(x):
@@ -107,6 +131,58 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+def _worker_gen(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1207_1773_b200.dist import gather_columns, solve_gen_sharded
+    A, B = synth.pencil_rand(N, seed=9, kappa=10.0)
+    if rank == 0:
+        tA, tB = _cm(A), _cm(B)
+    else:
+        tA = torch.zeros((N, N), dtype=torch.complex128).t().contiguous().t()
+        tB = torch.zeros((N, N), dtype=torch.complex128).t().contiguous().t()
+    w, Es, _ = solve_gen_sharded(OracleSolver(NB), tA, tB, NB)
+    Eall = gather_columns(Es, N)
+    if rank == 0:
+        out.put((w.numpy().copy(), Eall.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_solve_gen_gloo_world2():
+    """Algorithm 1 with the sharded back-transform (2 ranks): the gathered
+    eigenvectors satisfy the residual / B-orthogonality gates and equal the
+    single-process composition bitwise."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_gen, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    w, E = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    A, B = synth.pencil_rand(N, seed=9, kappa=10.0)
+    R = A @ E - (B @ E) * w[None, :]
+    assert np.linalg.norm(R, 1) / (N * np.linalg.norm(A, 1) * np.linalg.norm(E, 1)) < 1e-14
+    assert np.linalg.norm(E.conj().T @ B @ E - np.eye(N), 1) / N < 1e-14
+    # single process, same stand-in solver
+    s = OracleSolver(NB)
+    tA, tB = _cm(A), _cm(B)
+    assert s.potrf(tB) == 0
+    s.hegst(tA, tB)
+    tau1, T1 = s.he2hb(tA)
+    d, e, V2, tau2 = s.hb2st(tA)
+    w1, Zr = s.stedc(d, e)
+    E1 = torch.zeros((N, N), dtype=torch.complex128).t()
+    s.apply_q2(V2, tau2, E1, Z=Zr)
+    s.apply_q1(tA, T1, E1)
+    s.trsm_lh(tB, E1)
+    assert np.array_equal(E, E1.numpy()) and np.array_equal(w, w1.numpy())
 
 
 def test_column_slices_partition():
