@@ -126,6 +126,25 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
     cp_async_commit();
   }
 
+  // C += alpha A B with alpha = +-1: start the accumulators from C (its loads
+  // overlap the pipeline prologue instead of trailing the main loop) and fold
+  // the sign of alpha into the A fragments.
+  const bool fuse_c = (p.part == nullptr) && p.beta == 1.0 && (p.alpha == 1.0 || p.alpha == -1.0);
+  const unsigned aflip = (fuse_c && p.alpha == -1.0) ? 0x80000000u : 0u;
+  if (fuse_c) {
+    const int rpc = (lane >> 2) & 1;
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int64_t gm = m0 + wm * 16 + i * 4 + (lane >> 3);
+        const int64_t gn = n0 + wn * 32 + j * 8 + (lane & 3) * 2;
+        const double *cb = reinterpret_cast<const double *>(p.C);
+        acc[i][j][0] = (gm < p.M && gn < p.N) ? cb[(gm + gn * p.ldc) * 2 + rpc] : 0.0;
+        acc[i][j][1] = (gm < p.M && gn + 1 < p.N) ? cb[(gm + (gn + 1) * p.ldc) * 2 + rpc] : 0.0;
+      }
+  }
+
   for (int kt = 0; kt < nk; kt++) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -158,7 +177,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
     }
     const double *a = reinterpret_cast<const double *>(smem + st * STAGE_ELEMS);
     const double *b = reinterpret_cast<const double *>(smem + st * STAGE_ELEMS + SA_ELEMS);
-    const unsigned anm = conjA ? le.a_neg_conj : le.a_neg;
+    const unsigned anm = (conjA ? le.a_neg_conj : le.a_neg) ^ aflip;
     const unsigned bnm = (OPB == OP_C) ? le.b_neg_conj : 0u;
 #pragma unroll
     for (int ks = 0; ks < BK / 2; ks++) {
@@ -198,9 +217,9 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
           p.part[(int64_t)blockIdx.y * p.M * p.N + gm + gn * p.M] = v;
         } else {
           if (LOWER && p.row0 + gm < gn) continue;
-          double2 out = make_double2(p.alpha * v.x, p.alpha * v.y);
           double2 *cp = p.C + gm + gn * p.ldc;
-          if (p.beta != 0.0) {
+          double2 out = fuse_c ? v : make_double2(p.alpha * v.x, p.alpha * v.y);
+          if (!fuse_c && p.beta != 0.0) {
             const double2 c = *cp;
             out.x += p.beta * c.x;
             out.y += p.beta * c.y;
