@@ -26,7 +26,7 @@
 namespace eig {
 namespace {
 
-constexpr int HT = 256;
+constexpr int HT = 512;
 
 struct HbArgs {
   int64_t n;
@@ -47,11 +47,25 @@ __device__ __forceinline__ void st_release_i32(int *p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Task layout (one CTA, 8 warps):
+//   1. every thread issues its cp.async loads at once: the target column x,
+//      the rest of the previous bulge Ablk = M[R, c+1:r0], the diagonal block
+//      D = M[R, R] (lower) and the rows below Cblk = M[r1+1:kend, R];
+//   2. warp 0 builds (beta, tau, v) and writes the reflector outputs;
+//   3. the three updates run concurrently: warps 0-1 (a) on Ablk, warps 2-5
+//      (b) on D, warps 6-7 (c) on Cblk, each storing straight to global.
+constexpr int LDD = 65;
 __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
+  extern __shared__ __align__(16) double2 hsm[];
+  double2 *sD = hsm;                  // [64][LDD] diagonal block (full Hermitian)
+  double2 *sA = sD + 64 * LDD;        // [63 cols][64 rows] previous bulge (column-major)
+  double2 *sC = sA + 64 * 64;         // [64 cols][64 rows] rows below R (column-major, row index fast)
+  double2 *sx = sC + 64 * 64;         // [64]
   __shared__ double2 sv[64];          // reflector
-  extern __shared__ __align__(16) double2 sD[];   // [64 * 65] diagonal block (full Hermitian), ld 65
   __shared__ double2 sp[64];          // p, then w
-  __shared__ double2 s_tau, s_beta_scale;
+  __shared__ double2 sg[64];          // g = tau (C v)
+  __shared__ double2 spart[6][64];    // half dot products
+  __shared__ double2 s_tau, s_beta;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n;
   const int nb = a.nb, ldab = a.ldab;
@@ -74,27 +88,44 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       if (r0 > n - 1) break;
       const int64_t r1 = imin64(i + (j + 1) * nb, n - 1);
       const int len = (int)(r1 - r0 + 1);
+      const int na = (int)(r0 - c - 1);                       // previous-bulge columns
+      const int64_t kend = imin64(r1 + nb, n - 1);
+      const int nc = (int)(kend - r1);                        // rows below R
       mark(-1);
-      // wait for sweep i-1 to finish step j+2 (or to finish)
-      if (i > 0 && tid == 0) {
+      if (i > 0 && tid == 0) {   // sweep i-1 must have finished step j+2
         const int64_t prev = i - 1;
-        const int64_t jprev_max = (n - 2 - prev) / nb;   // last step index of sweep i-1
+        const int64_t jprev_max = (n - 2 - prev) / nb;
         const int need = (int)imin64(j + 3, jprev_max + 1);
         while (ld_acquire_i32(a.progress + prev) < need) {
         }
       }
       __syncthreads();
       mark(0);
-      // ---- reflector from M[R, c]
+      // ---- 1. all loads at once
+      for (int t = tid; t < len; t += HT) cp_async16(&sx[t], M(r0 + t, c), true);
+      for (int e = tid; e < na * 64; e += HT) {
+        const int t = e & 63, k = e >> 6;
+        if (t < len) cp_async16(&sA[t + k * 64], M(r0 + t, c + 1 + k), true);
+      }
+      for (int e = tid; e < 64 * 64; e += HT) {
+        const int rr = e & 63, cc = e >> 6;
+        if (rr < len && cc <= rr) cp_async16(&sD[rr + cc * LDD], M(r0 + rr, r0 + cc), true);
+      }
+      for (int e = tid; e < nc * 64; e += HT) {
+        const int rr = e % nc, t = e / nc;
+        if (t < len) cp_async16(&sC[rr + t * 64], M(r1 + 1 + rr, r0 + t), true);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      mark(1);
+      // ---- 2. reflector
       if (warp == 0) {
-        double2 x0 = czero(), x1 = czero();
-        if (lane < len) x0 = __ldcg(M(r0 + lane, c));
-        if (lane + 32 < len) x1 = __ldcg(M(r0 + lane + 32, c));
-        double nrm = 0.0;
-        if (lane >= 1) nrm += x0.x * x0.x + x0.y * x0.y;
-        nrm += x1.x * x1.x + x1.y * x1.y;
+        const double2 x0 = lane < len ? sx[lane] : czero();
+        const double2 x1 = lane + 32 < len ? sx[lane + 32] : czero();
+        double nrm = (lane >= 1 ? x0.x * x0.x + x0.y * x0.y : 0.0) + x1.x * x1.x + x1.y * x1.y;
         nrm = warp_sum(nrm);
-        double2 al = make_double2(__shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0));
+        const double2 al = sx[0];
         double2 tau, scale;
         double beta;
         if (nrm == 0.0 && al.y == 0.0) {
@@ -108,125 +139,87 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
           const double dd = d.x * d.x + d.y * d.y;
           scale = make_double2(d.x / dd, -d.y / dd);
         }
-        // v
         sv[lane] = (lane == 0) ? make_double2(1.0, 0.0) : (lane < len ? cmul(x0, scale) : czero());
         sv[lane + 32] = (lane + 32 < len) ? cmul(x1, scale) : czero();
         if (lane == 0) {
           s_tau = tau;
-          s_beta_scale = make_double2(beta, 0.0);
+          s_beta = make_double2(beta, 0.0);
         }
       }
       __syncthreads();
       const double2 tau = s_tau, ctau = cconj(tau);
-      // outputs: V2 slot, tau2, the eliminated column
       {
         const int64_t slot = a.off[j] + i;
         for (int t = tid; t < nb; t += HT) a.V2[slot * nb + t] = (t < len) ? sv[t] : czero();
         if (tid == 0) a.tau2[slot] = tau;
-        for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta_scale : czero();
+        for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta : czero();
       }
-      mark(1);
+      mark(2);
       if (tau.x != 0.0 || tau.y != 0.0) {
-        // ---- (a) left application to columns c < k < r0 (rest of the previous bulge),
-        //      4 columns per warp in flight (loads first, then the reductions)
-        for (int64_t k0 = c + 1 + 4 * warp; k0 < r0; k0 += 4 * (HT / 32)) {
-          double2 y0[4], y1[4];
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const int64_t k = k0 + u;
-            y0[u] = (k < r0 && lane < len) ? __ldcg(M(r0 + lane, k)) : czero();
-            y1[u] = (k < r0 && lane + 32 < len) ? __ldcg(M(r0 + lane + 32, k)) : czero();
-          }
-          const double2 va = sv[lane], vb = sv[lane + 32];
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const int64_t k = k0 + u;
-            double2 sdot = cadd(cmulc(va, y0[u]), cmulc(vb, y1[u]));   // v^H y
-            sdot = warp_sum2(sdot);
-            const double2 f = cmul(ctau, sdot);
-            if (k < r0) {
-              if (lane < len) *M(r0 + lane, k) = csub(y0[u], cmul(va, f));
-              if (lane + 32 < len) *M(r0 + lane + 32, k) = csub(y1[u], cmul(vb, f));
-            }
-          }
-        }
-        mark(2);
-        // ---- (b) two-sided on the diagonal block
-        {
-          // thread (rr, cq): rows rr, columns cq, cq+4, ... ; all 16 loads in flight at once
-          const int rr = tid & 63, cq = tid >> 6;
-          double2 dv[16];
-#pragma unroll
-          for (int u = 0; u < 16; u++) {
-            const int cc = cq + 4 * u;
-            dv[u] = (rr < len && cc <= rr) ? __ldcg(M(r0 + rr, r0 + cc)) : czero();
-          }
-#pragma unroll
-          for (int u = 0; u < 16; u++) {
-            const int cc = cq + 4 * u;
-            if (rr < len && cc <= rr) {
-              double2 d = dv[u];
-              if (rr == cc) d.y = 0.0;
-              sD[rr + cc * 65] = d;
-              sD[cc + rr * 65] = cconj(d);
-            }
-          }
-        }
-        __syncthreads();
-        if (tid < len) {   // p = tau D v
+        // U1: all dot products in parallel, each split in two halves over t
+        //   f_k = conj(tau) v^H Ablk[:, k];  p_r = tau (D v)_r;  g_rr = tau (Cblk v)_rr
+        if (tid < 384) {
+          const int g = tid >> 6, q = tid & 63, h = g & 1;
+          const int t0 = h * 32, t1 = imin64(t0 + 32, len);
           double2 acc = czero();
-          for (int cc = 0; cc < len; cc++) acc = cadd(acc, cmul(sD[tid + cc * 65], sv[cc]));
-          sp[tid] = cmul(tau, acc);
+          if (g < 2) {
+            if (q < na)
+              for (int t = t0; t < t1; t++) acc = cadd(acc, cmulc(sv[t], sA[t + q * 64]));
+          } else if (g < 4) {
+            if (q < len)
+              for (int cc = t0; cc < t1; cc++) {
+                double2 d;
+                if (cc < q) d = sD[q + cc * LDD];
+                else if (cc > q) d = cconj(sD[cc + q * LDD]);
+                else d = make_double2(sD[q + q * LDD].x, 0.0);
+                acc = cadd(acc, cmul(d, sv[cc]));
+              }
+          } else {
+            if (q < nc)
+              for (int t = t0; t < t1; t++) acc = cadd(acc, cmul(sC[q + t * 64], sv[t]));
+          }
+          spart[g][q] = acc;
         }
         __syncthreads();
+        if (tid < 64) {
+          if (tid < na) sx[tid] = cmul(ctau, cadd(spart[0][tid], spart[1][tid]));
+        } else if (tid < 128) {
+          const int r = tid - 64;
+          if (r < len) sp[r] = cmul(tau, cadd(spart[2][r], spart[3][r]));
+        } else if (tid < 192) {
+          const int rr = tid - 128;
+          if (rr < nc) sg[rr] = cmul(cadd(spart[4][rr], spart[5][rr]), tau);
+        }
+        __syncthreads();
+        mark(4);
         if (warp == 0) {   // w = p - 1/2 tau (p^H v) v
-          double2 s = czero();
-          for (int t = lane; t < len; t += 32) s = cadd(s, cmulc(sp[t], sv[t]));
-          s = warp_sum2(s);
-          const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), s);
+          double2 sdot = czero();
+          for (int t = lane; t < len; t += 32) sdot = cadd(sdot, cmulc(sp[t], sv[t]));
+          sdot = warp_sum2(sdot);
+          const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), sdot);
           for (int t = lane; t < len; t += 32) sp[t] = cadd(sp[t], cmul(al, sv[t]));
         }
         __syncthreads();
-        {
-          const int rr = tid & 63, cq = tid >> 6;
-          const double2 vr = sv[rr], pr = sp[rr];
-#pragma unroll
-          for (int u = 0; u < 16; u++) {
-            const int cc = cq + 4 * u;
-            if (rr < len && cc <= rr) {
-              double2 d = sD[rr + cc * 65];
-              d = csub(d, cadd(cmul(vr, cconj(sp[cc])), cmul(pr, cconj(sv[cc]))));
-              if (rr == cc) d.y = 0.0;
-              *M(r0 + rr, r0 + cc) = d;
-            }
+        // U3: element-wise updates, stored straight to global
+        for (int e = tid; e < na * 64; e += HT) {          // (a) y_k - v f_k
+          const int t = e & 63, k = e >> 6;
+          if (t < len) *M(r0 + t, c + 1 + k) = csub(sA[t + k * 64], cmul(sv[t], sx[k]));
+        }
+        for (int e = tid; e < 64 * 64; e += HT) {          // (b) D - v w^H - w v^H  (lower)
+          const int rr = e & 63, cc = e >> 6;
+          if (rr < len && cc <= rr) {
+            double2 d = sD[rr + cc * LDD];
+            d = csub(d, cadd(cmul(sv[rr], cconj(sp[cc])), cmul(sp[rr], cconj(sv[cc]))));
+            if (rr == cc) d.y = 0.0;
+            *M(r0 + rr, r0 + cc) = d;
           }
         }
-        mark(3);
-        // ---- (c) right application to rows r1 < k <= min(r1 + nb, n-1)
-        const int64_t kend = imin64(r1 + nb, n - 1);
-        for (int64_t k0 = r1 + 1 + 4 * warp; k0 <= kend; k0 += 4 * (HT / 32)) {
-          double2 y0[4], y1[4];
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const int64_t k = k0 + u;
-            y0[u] = (k <= kend && lane < len) ? __ldcg(M(k, r0 + lane)) : czero();
-            y1[u] = (k <= kend && lane + 32 < len) ? __ldcg(M(k, r0 + lane + 32)) : czero();
-          }
-          const double2 va = sv[lane], vb = sv[lane + 32];
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const int64_t k = k0 + u;
-            double2 t = cadd(cmul(y0[u], va), cmul(y1[u], vb));   // y v
-            t = warp_sum2(t);
-            const double2 f = cmul(t, tau);
-            if (k <= kend) {
-              if (lane < len) *M(k, r0 + lane) = csub(y0[u], cmul(f, cconj(va)));
-              if (lane + 32 < len) *M(k, r0 + lane + 32) = csub(y1[u], cmul(f, cconj(vb)));
-            }
-          }
+        for (int e = tid; e < nc * 64; e += HT) {          // (c) y - g v^H
+          const int rr = e % nc, t = e / nc;
+          if (t < len) *M(r1 + 1 + rr, r0 + t) = csub(sC[rr + t * 64], cmul(sg[rr], cconj(sv[t])));
         }
       }
-      mark(4);
+      mark(3);
       __threadfence();
       __syncthreads();
       if (tid == 0) st_release_i32(a.progress + i, (int)(j + 1));
@@ -287,7 +280,7 @@ int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d,
     const int64_t J = (n - 2) / nb + 1;   // steps of sweep 0
     const int P = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, std::min<int64_t>(n - 1, J / 3 + 2)));
     void *args[] = {&a};
-    const size_t smem = (size_t)64 * 65 * sizeof(double2);
+    const size_t smem = ((size_t)64 * LDD + 64 * 64 + 64 * 64 + 64) * sizeof(double2);
     static bool attr = false;
     if (!attr) {
       EIG_TRY(ctx.check(cudaFuncSetAttribute(hb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
