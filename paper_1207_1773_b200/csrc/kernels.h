@@ -93,5 +93,7 @@ struct Q2Plan {
 };
 int q2_tfactors(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *tau2, double2 *T2);
 int q2_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, double2 *E, int64_t lde, int64_t m);
+// column-owning-warp variant (nb = 64, g = 32); returns 1 if the shape is not handled
+int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, double2 *E, int64_t lde, int64_t m);
 
 }  // namespace eig

@@ -22,6 +22,7 @@
 //                           k-steps outside the parallelogram;
 //    all fragment loads are plain LDS.64 (no per-element bounds logic).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -30,7 +31,13 @@
 namespace eig {
 namespace {
 
-constexpr int QT = 512;   // 16 warps: 8 reflector/row groups x 2 column halves
+constexpr int NH = 2;                // column parts
+constexpr int QT = 256 * NH;         // 8 reflector/row groups x NH column parts
+
+// fragments of part h when NF fragments are split over NH parts
+__host__ __device__ constexpr int nf_part(int NF, int h) { return (NF + NH - 1 - h) / NH; }
+__host__ __device__ constexpr int nf_lo(int NF, int h) { return h == 0 ? 0 : nf_lo(NF, h - 1) + nf_part(NF, h - 1); }
+__host__ __device__ constexpr int nf_c(int NF, int h) { return nf_part(NF, h) > 0 ? nf_part(NF, h) : 1; }
 constexpr int NFMAX = 9;           // 8-column fragments per slab
 constexpr int QBN = NFMAX * 8;     // 72 columns
 constexpr int LDV = 36;            // Vd row stride (complex), == 4 mod 8
@@ -154,7 +161,7 @@ struct NextBlk {
 // before the end-of-block barrier, so the loads overlap the rest of phase C.
 template <int NFH>
 __device__ __forceinline__ void phase_c(const Q2Args &a, double2 *sVd, const double *sy, double2 *sE, int mw,
-                                        int nlo, int h, int base, int R, int nout, int64_t rs, int64_t c0, int ncols,
+                                        int nlo, int nfh, int h, int base, int R, int nout, int64_t rs, int64_t c0, int ncols,
                                         int ncolsl, const NextBlk &nx, int lane, const LaneEmb &le, int rp) {
   const int nb = a.nb, g = a.g, W = a.W, nmfC = a.Wp / 4;
   const int kq = (lane & 3) >> 1;
@@ -165,6 +172,7 @@ __device__ __forceinline__ void phase_c(const Q2Args &a, double2 *sVd, const dou
     const int mf = mw + 8 * i;
     if (mf >= nmfC) break;
     const int q0 = mf * 4;
+    if (nfh > 0) {
     const int klo = max(0, q0 - nb + 1) >> 1, khi = min(g - 1, q0 + 3) >> 1;
     double acc[NFH][2];
 #pragma unroll
@@ -208,22 +216,25 @@ __device__ __forceinline__ void phase_c(const Q2Args &a, double2 *sVd, const dou
         }
       }
     }
+    }
     if (nx.more) {
       // both column halves of this row group must be done before its slots are refilled
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + mw) : "memory");
-      // next block's V entries of rows q0..q0+3: Vd[qq][t] = v_t[qq - t]   (half 0)
-      if (h == 0)
-      for (int e = lane; e < 4 * g; e += 32) {
-        const int qq = q0 + e / g, t = e % g;
-        const int sidx = qq - t;
-        if (qq < W && sidx >= 0 && sidx < nb) {
-          const bool ok = t < nx.nvalid;
-          cp_async16(&sVd[qq * LDV + t], ok ? nx.v2 + t * nb + sidx : a.V2, ok);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + mw), "r"(32 * NH) : "memory");
+      // next block's V entries of rows q0..q0+3: Vd[qq][t] = v_t[qq - t]   (part 0; t = lane, g <= 32)
+      if (h == 0 && lane < g) {
+        const int t = lane;
+#pragma unroll
+        for (int rr = 0; rr < 4; rr++) {
+          const int qq = q0 + rr, sidx = qq - t;
+          if (qq < W && sidx >= 0 && sidx < nb) {
+            const bool ok = t < nx.nvalid;
+            cp_async16(&sVd[qq * LDV + t], ok ? nx.v2 + t * nb + sidx : a.V2, ok);
+          }
         }
       }
-      // next block's new E rows land in the ring slots of rows q0..q0+3 (< nb)   (half 1)
-      if (h == 1 && q0 < nb) {
-        for (int e = lane; e < 4 * ncolsl; e += 32) {
+      // next block's new E rows land in the ring slots of rows q0..q0+3 (< nb)   (parts 1..)
+      if (h >= 1 && q0 < nb) {
+        for (int e = lane + 32 * (h - 1); e < 4 * ncolsl; e += 32 * (NH - 1)) {
           const int qq = q0 + (e & 3), c = e >> 2;
           if (qq < nb) {
             const int64_t row1 = nx.rs1 + qq + g - 1;
@@ -240,9 +251,12 @@ template <int NF>
 __device__ __forceinline__ void q2_slab(const Q2Args &a, const Smem &s, int64_t c0, int ncols) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int wu = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform warp id
-  const int mw = wu & 7, h = wu >> 3;
-  constexpr int NF0 = (NF + 1) / 2, NF1 = NF / 2, NF1c = NF1 > 0 ? NF1 : 1;
-  const int nlo = h ? NF0 : 0, nfh = h ? NF1 : NF0;
+  // SMSP s (= wu % 4) gets reflector groups s and 7 - s of every part, which
+  // balances the triangular phase B across the four schedulers
+  const int mw = ((wu >> 2) & 1) ? 7 - (wu & 3) : (wu & 3), h = wu >> 3;
+  constexpr int NF0 = nf_c(NF, 0), NF1 = nf_c(NF, 1), NF2 = nf_c(NF, NH > 2 ? 2 : 1);
+  const int nlo = h == 0 ? 0 : h == 1 ? nf_lo(NF, 1) : nf_lo(NF, 2);
+  const int nfh = h == 0 ? nf_part(NF, 0) : h == 1 ? nf_part(NF, 1) : nf_part(NF, 2);
   const LaneEmb le(lane);
   const int rp = (lane >> 2) & 1;
   const int nb = a.nb, g = a.g, W = a.W, R = a.W;
@@ -257,13 +271,17 @@ __device__ __forceinline__ void q2_slab(const Q2Args &a, const Smem &s, int64_t 
   // per-k increments, so the prefetch loops need no integer division
   const int d_q = QT % nb, d_c = QT / nb;
   const int q_0 = tid % nb, c_0 = tid / nb;
+  // optional phase profile (CTA 0, thread 0), accumulated in shared memory so
+  // that it costs no registers when disabled
+  __shared__ long long t_acc[6];   // [5] = last mark
   const bool prof = a.prof != nullptr && blockIdx.x == 0 && tid == 0;
-  long long t_mark = 0, t_acc[5] = {0, 0, 0, 0, 0};
+  if (prof)
+    for (int k = 0; k < 6; k++) t_acc[k] = 0;
   auto mark = [&](int k) {
     if (prof) {
       const long long now = clock64();
-      if (k >= 0) t_acc[k] += now - t_mark;
-      t_mark = now;
+      if (k >= 0) t_acc[k] += now - t_acc[5];
+      t_acc[5] = now;
     }
   };
 
@@ -306,7 +324,8 @@ __device__ __forceinline__ void q2_slab(const Q2Args &a, const Smem &s, int64_t 
       // ---------------- phase A: Y = V^H E_win
       if (actAB) {
         if (h == 0) phase_a<NF0>(vd, se, s.Y, mw, nlo, nb, base, R, lane, le, rp);
-        else phase_a<NF1c>(vd, se, s.Y, mw, nlo, nb, base, R, lane, le, rp);
+        else if (h == 1) phase_a<NF1>(vd, se, s.Y, mw, nlo, nb, base, R, lane, le, rp);
+        else phase_a<NF2>(vd, se, s.Y, mw, nlo, nb, base, R, lane, le, rp);
       }
       __syncthreads();
       mark(1);
@@ -340,9 +359,11 @@ __device__ __forceinline__ void q2_slab(const Q2Args &a, const Smem &s, int64_t 
           for (int x = lane; x < g; x += 32) cp_async16(&s.T[y * LDT + x], tsrc + y * g + x, true);
       }
       if (h == 0)
-        phase_c<NF0>(a, s.Vd, sy, s.E, mw, nlo, h, base, R, more ? nb : W, rs, c0, ncols, ncolsl, nx, lane, le, rp);
+        phase_c<NF0>(a, s.Vd, sy, s.E, mw, nlo, nfh, h, base, R, more ? nb : W, rs, c0, ncols, ncolsl, nx, lane, le, rp);
+      else if (h == 1)
+        phase_c<NF1>(a, s.Vd, sy, s.E, mw, nlo, nfh, h, base, R, more ? nb : W, rs, c0, ncols, ncolsl, nx, lane, le, rp);
       else
-        phase_c<NF1c>(a, s.Vd, sy, s.E, mw, nlo, h, base, R, more ? nb : W, rs, c0, ncols, ncolsl, nx, lane, le, rp);
+        phase_c<NF2>(a, s.Vd, sy, s.E, mw, nlo, nfh, h, base, R, more ? nb : W, rs, c0, ncols, ncolsl, nx, lane, le, rp);
       cp_async_commit();
       mark(3);
       if (more) {
@@ -389,6 +410,15 @@ __global__ void __launch_bounds__(QT, 1) apply_q2_kernel(Q2Args a, int nslab) {
 
 int q2_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, double2 *E, int64_t lde, int64_t m) {
   if (p.nblocks <= 0 || m <= 0) return 0;
+  // column-owning-warp kernel (q2w.cu) for its shape unless EIG_Q2_KERNEL=row
+  static const int use_w = [] {
+    const char *e = getenv("EIG_Q2_KERNEL");
+    return (e && e[0] == 'r') ? 0 : 1;
+  }();
+  if (use_w) {
+    const int rc = q2w_apply(ctx, p, V2, T2, E, lde, m);
+    if (rc <= 0) return rc;
+  }
   if (p.g > 32 || p.nb > 64 || p.g % 4 != 0 || p.g < 4 || p.nb < p.g - 1 || (p.nb % 2)) return EIG_ERR_NOTIMPL;
   Q2Args a;
   a.n = p.n;

@@ -171,6 +171,24 @@ def test_apply_q2_parity_synthetic(n, nb, g, m):
 
 
 @gpu
+@pytest.mark.parametrize("n,m", [(517, 2000), (300, 10700), (129, 1333), (66, 9)])
+def test_apply_q2_parity_wide_sampled(n, m):
+    """nb = 64, g = 32 (the column-owning-warp kernel): wide E, several
+    fragments per CTA, and (m = 10700 > 148 x 72) two column slabs; the columns
+    are independent, so sampled columns are checked against the oracle."""
+    nb, g = 64, 32
+    s = _solver(nb=nb, g=g)
+    V2, tau2 = synth.synthetic_v2(n, nb, 6)
+    Z = synth.real_orthonormalish(n, m, 6)
+    from paper_1207_1773_b200 import empty_colmajor
+    dE = empty_colmajor(n, m)
+    s.apply_q2(torch.from_numpy(V2).cuda(), torch.from_numpy(tau2).cuda(), dE, Z=_dev(Z))
+    cols = sorted({0, 1, 7, 8, 9, m // 3, m // 2 + 5, m - 9, m - 2, m - 1} & set(range(m)))
+    ref = oracle.apply_q2(V2, tau2, nb, Z[:, cols].astype(complex))
+    assert _rel(dE.cpu().numpy()[:, cols], ref) < TOL
+
+
+@gpu
 def test_apply_q2_parity_real_bulge_chase_reflectors():
     n, nb, g = 150, 16, 8
     A = synth.rand_hermitian(n, 9)

@@ -38,7 +38,7 @@ double run(int sms, int warps, int iters) {
 
 int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  int ws[] = {4, 8, 16};
+  int ws[] = {1, 2, 3, 4, 5, 8, 16};
   printf("warps/CTA(1 CTA/SM) x chains/warp -> TFLOP/s\n");
   for (int w : ws) {
     printf("W=%2d: C1 %.1f  C2 %.1f  C4 %.1f  C8 %.1f  C16 %.1f\n", w, run<1>(sms, w, 20000), run<2>(sms, w, 10000),
