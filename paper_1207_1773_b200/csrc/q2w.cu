@@ -4,21 +4,26 @@
 // I - V T V^H, V the W x g parallelogram, W = nb + g - 1 = 95; groups applied
 // last to first, steps ascending), different work split:
 //
-//  * each consumer warp owns one 8-column fragment of E and its 96-row window
-//    (a ring of three 32-row chunks in shared memory), and runs all three
-//    contractions for it alone — Y = V^H E (phase A), Y = T Y (phase B),
-//    E -= V Y (phase C) — with Y kept in registers and moved between the
-//    accumulator and operand layouts by warp shuffles, so no barrier is ever
-//    shared between consumer warps;
-//  * V (compact: Vc[t][4 + s] = v_t[s], zero pads on both sides) and T of the
-//    next block are streamed by a producer warp with bulk async copies into a
-//    double buffer (full/empty mbarriers), so loading them overlaps compute;
+//  * a CTA owns up to 9 eight-column fragments of E per slab; 8 "full" warps
+//    own one fragment each and its 96-row window (a ring of three 32-row
+//    chunks in shared memory) and run all three contractions for it alone —
+//    Y = V^H E (phase A), Y = T Y (phase B), E -= V Y (phase C) — with Y in
+//    registers, moved between the accumulator and operand layouts by warp
+//    shuffles, so they never wait for each other;
+//  * the 9th fragment is shared by a quad of warps (one per SM sub-partition,
+//    each doing a quarter of every phase, Y exchanged through shared memory
+//    under a 128-thread named barrier), so all four DMMA pipes get the same
+//    work (2.25 fragments each instead of 3 on one of them);
+//  * V (compact: Vc[t][4 + s] = v_t[s], zero pads on both sides) and T are
+//    double-buffered and loaded with bulk async copies that complete on an
+//    mbarrier; the last warp to release a buffer issues the copies of the
+//    block two ahead into it (no producer warp, no block-wide barrier);
 //  * every loop over k-steps and row groups is fully unrolled against the
 //    compile-time parallelogram shape: all shared-memory addresses are a lane
 //    base plus an immediate, and only the nonzero DMMA tiles are issued;
-//  * a warp stores its rows that leave the window straight from the
-//    accumulators, then refills their ring slots with the next block's rows
-//    (cp.async) while it finishes the remaining row groups.
+//  * rows that leave the window are stored straight from the accumulators and
+//    their ring slots are refilled with the next block's rows (cp.async)
+//    while the remaining row groups are computed.
 #include <algorithm>
 
 #include "common.cuh"
@@ -30,11 +35,24 @@ namespace {
 
 constexpr int NB = 64, G = 32, W = NB + G - 1;   // 95 window rows
 constexpr int RING = 96;                         // 3 chunks of 32 rows
-constexpr int LDE = 98;                          // per-warp E column stride (complex), 2 mod 16
-constexpr int LDVC = 72, PADL = 4;               // compact V row stride / left zero pad
-constexpr int LDT = 36;                          // T column stride
-constexpr int NCW = 9;                           // consumer warps (fragments per slab)
-constexpr int WT = (NCW + 1) * 32;               // + producer warp
+constexpr int LDE = 97;                          // E window column stride (complex, odd)
+// Shared-memory banks: a 16-byte complex element e sits in bank group e mod 8
+// (plus the component).  The compact V rows are placed at
+//   rb(t) = 72 t + DV[t mod 4],  DV = {0, 5, 4, 1}
+// so that rb(t) - t mod 8 runs through {0,4,2,6} (+4 on odd quads): phase A
+// (4 consecutive reflectors x 2 rows) and phase C (2 reflectors x 4 rows)
+// both hit 8 distinct bank groups per fragment load.  Neighbouring rows
+// overlap only in their zero pads (4 on each side).
+constexpr int LDVC = 72, PADL = 4, VC_STAGE = 72 * G + 8;
+__host__ __device__ constexpr int dv(int i) { return i == 0 ? 0 : i == 1 ? 5 : i == 2 ? 4 : 1; }
+__host__ __device__ constexpr int vrow(int t) { return LDVC * t + dv(t & 3); }
+// T columns: cb(k) = 68 (k >> 1) + 36 (k & 1): consecutive columns 4 apart mod 8
+constexpr int T_STAGE = 68 * (G / 2);
+__host__ __device__ constexpr int tcol(int k) { return 68 * (k >> 1) + 36 * (k & 1); }
+constexpr int LDY = 34;                          // quad Y exchange: Y[col][refl]
+constexpr int NFW = 8, NQW = 4, NW = NFW + NQW;  // full warps, quad warps
+constexpr int NFS = NFW + 1;                     // fragments per slab
+constexpr int WT = NW * 32;
 
 struct Q2wArgs {
   int64_t n, m, lde;
@@ -44,15 +62,13 @@ struct Q2wArgs {
   const double2 *V2;
   const double2 *T2;
   double2 *E;
-  int nfr_total;
+  int nfr_total, nslab;
+  unsigned long long *prof;   // optional: CTA 0 warps 0 / 8 cycles [24..29] (wait, work, release)
 };
 
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *b, unsigned cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(cnt));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, unsigned tx) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
@@ -77,6 +93,11 @@ __device__ __forceinline__ void dmma_nv(double (&c)[2], double a, double b) {
       : "+d"(c[0]), "+d"(c[1])
       : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void cp_async16m(void *smem, const void *gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(su32(smem)), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void quad_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __host__ __device__ constexpr int imin_c(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int imax_c(int a, int b) { return a > b ? a : b; }
@@ -97,201 +118,401 @@ __device__ __forceinline__ void acc_to_b(const double (&acc)[NM][2], double (&bl
   }
 }
 
-// shared memory: Vc[2] | T[2] | E windows (NCW) | full[2], empty[2] mbarriers
+// shared memory: Vc[2] | T[2] | E windows (NFS) | Y, Y2 (quad) | full[2] mbarriers, done[2] counters
 extern __shared__ __align__(128) double2 q2w_sm[];
-constexpr int OFF_T = 2 * G * LDVC, OFF_E = OFF_T + 2 * G * LDT, OFF_BAR = OFF_E + NCW * 8 * LDE;
-__device__ __forceinline__ double2 *vc_buf(int bi) { return q2w_sm + bi * (G * LDVC); }
-__device__ __forceinline__ double2 *t_buf(int bi) { return q2w_sm + OFF_T + bi * (G * LDT); }
+constexpr int OFF_T = 2 * VC_STAGE, OFF_E = OFF_T + 2 * T_STAGE, OFF_Y = OFF_E + NFS * 8 * LDE,
+              OFF_Y2 = OFF_Y + 8 * LDY, OFF_BAR = OFF_Y2 + 8 * LDY;
+__device__ __forceinline__ double2 *vc_buf(int bi) { return q2w_sm + bi * VC_STAGE; }
+__device__ __forceinline__ double2 *t_buf(int bi) { return q2w_sm + OFF_T + bi * T_STAGE; }
 __device__ __forceinline__ uint64_t *full_bar(int bi) { return reinterpret_cast<uint64_t *>(q2w_sm + OFF_BAR) + bi; }
-__device__ __forceinline__ uint64_t *empty_bar(int bi) { return reinterpret_cast<uint64_t *>(q2w_sm + OFF_BAR) + 2 + bi; }
+__device__ __forceinline__ int *done_cnt(int bi) { return reinterpret_cast<int *>(q2w_sm + OFF_BAR + 1) + bi; }
 
-// ---------------------------------------------------------------- producer
-__device__ __forceinline__ void q2w_producer(const Q2wArgs &a, int nslab) {
-  const int lane = threadIdx.x & 31;
-  int64_t cnt = 0;
-  for (int sl = 0; sl < nslab; sl++)
-    for (int64_t gi = a.ngroups - 1; gi >= 0; gi--) {
-      const int64_t i0 = gi * G;
-      const int64_t J = (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
-      const int64_t blk0 = a.first[gi];
-      for (int64_t j = 0; j < J; j++, cnt++) {
-        const int bi = (int)(cnt & 1);
-        if (cnt >= 2) mbar_wait(empty_bar(bi), (unsigned)(((cnt >> 1) + 1) & 1));
-        const int nvalid = (int)imax64(0, imin64(G, a.n - 2 - j * NB - i0 + 1));
-        if (lane == 0) mbar_arrive_tx(full_bar(bi), (unsigned)(nvalid * NB * 16 + G * G * 16));
-        __syncwarp();
-        const double2 *v2 = a.V2 + (a.off[j] + i0) * NB;
-        if (lane < nvalid) bulk_g2s(vc_buf(bi) + lane * LDVC + PADL, v2 + lane * NB, NB * 16, full_bar(bi));
-        bulk_g2s(t_buf(bi) + lane * LDT, a.T2 + (blk0 + j) * G * G + lane * G, G * 16, full_bar(bi));
+// ---------------------------------------------------------------- block sequence
+// (slab, group gi from last to first, step j ascending), identical in every warp.
+struct BlkIt {
+  int sl;
+  int64_t gi, j, J;
+  bool valid;
+};
+__device__ __forceinline__ int64_t steps_of(const Q2wArgs &a, int64_t gi) {
+  const int64_t i0 = gi * G;
+  return (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
+}
+__device__ __forceinline__ void it_settle(const Q2wArgs &a, BlkIt &it) {
+  while (it.valid && it.j >= it.J) {
+    if (--it.gi < 0) {
+      if (++it.sl >= a.nslab) {
+        it.valid = false;
+        return;
       }
+      it.gi = a.ngroups - 1;
     }
+    it.J = steps_of(a, it.gi);
+    it.j = 0;
+  }
+}
+__device__ __forceinline__ void it_begin(const Q2wArgs &a, BlkIt &it) {
+  it.sl = 0;
+  it.gi = a.ngroups - 1;
+  it.j = 0;
+  it.valid = a.ngroups > 0 && a.nslab > 0;
+  it.J = it.valid ? steps_of(a, it.gi) : 0;
+  it_settle(a, it);
+}
+__device__ __forceinline__ void it_next(const Q2wArgs &a, BlkIt &it) {
+  if (!it.valid) return;
+  it.j++;
+  it_settle(a, it);
 }
 
-// ---------------------------------------------------------------- consumer
-__device__ __forceinline__ void q2w_consumer(const Q2wArgs &a, int frag0, int frag1, int nslab) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double2 *Ew = q2w_sm + OFF_E + w * 8 * LDE;
-  const LaneEmb le(lane);
-  const int kq = (lane & 3) >> 1;
-  const unsigned negA = le.a_neg ^ 0x80000000u;   // -V in phase C
-  // per-lane shared-memory offsets (in doubles)
-  const int offA = 2 * (71 * (lane >> 3) + kq + PADL) + le.a_comp;    // phase A:  V^H  (t = 4mf + lane>>3, q = 2ks + kq)
-  const int offC = 2 * (71 * kq + (lane >> 3) + PADL) + le.a_comp;    // phase C:  V    (q = 4f + lane>>3, t = 2ks + kq)
-  const int offT = 2 * (kq * LDT + (lane >> 3)) + le.a_comp;          // phase B:  T[ra][kb]
-  const int offEB = 2 * (LDE * (lane >> 2) + kq) + (lane & 1);        // E operand layout
-  const int rr = lane >> 2;
-  const int offEC = 2 * (LDE * 2 * (lane & 3) + (rr >> 1)) + (rr & 1);  // E accumulator layout (col 2(lane&3))
-  double *ew = reinterpret_cast<double *>(Ew);
-  int64_t cnt = 0;
-  for (int sl = 0; sl < nslab; sl++) {
-    const int fr = frag0 + sl * NCW + w;
-    const bool active = fr < frag1;
-    const int64_t c0 = (int64_t)fr * 8;
-    const int ncols = active ? (int)imin64(8, a.m - c0) : 0;
-    // global column pointers of this lane (accumulator layout: columns 2(lane&3), +1)
-    const int cA = 2 * (lane & 3);
-    const bool okA0 = cA < ncols, okA1 = cA + 1 < ncols;
-    for (int64_t gi = a.ngroups - 1; gi >= 0; gi--) {
-      const int64_t i0 = gi * G;
-      const int64_t J = (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
-      int base = 0;   // ring offset: window row q lives in slot (q + base) mod 96
-      if (active && J > 0) {
-        // group start: whole window rows rs .. rs + 95 (row 95 is padding)
-        const int64_t rs = i0 + 1;
-        for (int e = lane; e < RING * 8; e += 32) {
-          const int q = e % RING, c = e / RING;
-          const int64_t row = rs + q;
-          const bool ok = q < W && row < a.n && c < ncols;
-          cp_async16(&Ew[c * LDE + q], ok ? a.E + row + (c0 + c) * a.lde : a.E, ok);
-        }
-        cp_async_commit();
+// Warp-wide: bulk copies of block `it`'s V (live slots) and T into buffer bi.
+__device__ __forceinline__ void issue_block(const Q2wArgs &a, const BlkIt &it, int bi, int lane) {
+  const int64_t i0 = it.gi * G, j = it.j;
+  const int nvalid = (int)imax64(0, imin64(G, a.n - 2 - j * NB - i0 + 1));
+  if (lane == 0) mbar_arrive_tx(full_bar(bi), (unsigned)(nvalid * NB * 16 + G * G * 16));
+  __syncwarp();
+  const double2 *v2 = a.V2 + (a.off[j] + i0) * NB;
+  if (lane < nvalid) bulk_g2s(vc_buf(bi) + vrow(lane) + PADL, v2 + lane * NB, NB * 16, full_bar(bi));
+  bulk_g2s(t_buf(bi) + tcol(lane), a.T2 + (a.first[it.gi] + j) * G * G + lane * G, G * 16, full_bar(bi));
+}
+
+// ---------------------------------------------------------------- per-lane constants
+struct Lane {
+  int lane, kq, rr;
+  int offA, offC0, offC1, offT, offEB, offEC;   // shared-memory offsets (doubles)
+  unsigned negConj, negT, negA;
+  __device__ __forceinline__ explicit Lane(int l) {
+    const LaneEmb le(l);
+    lane = l;
+    kq = (l & 3) >> 1;
+    rr = l >> 2;
+    // V element (q, t) at vrow(t) + PADL + q - t = 71 t + dv(t mod 4) + PADL + q
+    offA = 2 * (71 * (l >> 3) + dv(l >> 3) + kq + PADL) + le.a_comp;   // V^H: t = 4mf + lane>>3, q = 2ks + kq
+    offC0 = 2 * (71 * kq + dv(kq) + (l >> 3) + PADL) + le.a_comp;      // V: q = 4f + lane>>3, t = 2ks + kq, ks even
+    offC1 = 2 * (71 * kq + dv(2 + kq) + (l >> 3) + PADL) + le.a_comp;  //                                 ks odd
+    offT = 2 * (36 * kq + (l >> 3)) + le.a_comp;                       // T[ra][kb] at tcol(kb) + ra
+    offEB = 2 * (LDE * (l >> 2) + kq) + (l & 1);           // E, operand layout
+    offEC = 2 * (LDE * 2 * (l & 3) + (rr >> 1)) + (rr & 1);  // E, accumulator layout (col 2(lane&3))
+    negConj = le.a_neg_conj;
+    negT = le.a_neg;
+    negA = le.a_neg ^ 0x80000000u;                          // -V in phase C
+  }
+};
+
+// One fragment's view of a block.
+struct Frag {
+  double *ew;                 // window (doubles)
+  double2 *Ew;
+  int ch0, ch1, ch2;          // chunk -> slot base (doubles)
+  int base;
+  int64_t rs;                 // first window row
+  bool more;                  // a next block exists in this group
+  double *gE;                 // lane's global pointer (accumulator layout, row rs)
+  int64_t lde2;
+  bool ok0, ok1;              // lane's two columns exist
+  const double2 *E;
+  int64_t lde, c0, n;
+  int ncols;
+};
+
+__device__ __forceinline__ int ring_slot(int s) { return s < 0 ? s + RING : (s >= RING ? s - RING : s); }
+
+// Phase C for row groups FL::f(0..NU-1): acc = E rows + (-V) Y2, then store.
+// Rows < 64 (or all rows of a group's last block) leave the window: global.
+// REFILL: after storing a leaving row group, load the next block's rows into
+// its four slots (the quad does this per row group).
+template <int NU, class FL, bool REFILL>
+__device__ __forceinline__ void phase_c_rows(const Frag &F, const Lane &L, const double *vc, const double (&yb)[16]) {
+  double acc[NU][2];
+#pragma unroll
+  for (int u = 0; u < NU; u++) {
+    const int f = FL::f(u);
+    const int ch = f < 8 ? F.ch0 : (f < 16 ? F.ch1 : F.ch2);
+    const double *p = F.ew + ch + L.offEC + 8 * (f & 7);
+    acc[u][0] = p[0];
+    acc[u][1] = p[2 * LDE];
+  }
+#pragma unroll
+  for (int ks = 0; ks < 16; ks++) {
+#pragma unroll
+    for (int u = 0; u < NU; u++) {
+      const int f = FL::f(u);
+      const int klo = imax_c(0, 4 * f - 63) >> 1, khi = imin_c(31, 4 * f + 3) >> 1;
+      if (ks >= klo && ks <= khi) dmma_nv(acc[u], xsign(vc[((ks & 1) ? L.offC1 : L.offC0) + 284 * ks + 8 * f], L.negA), yb[ks]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NU; u++) {
+    const int f = FL::f(u);
+    const int q = 4 * f + (L.rr >> 1);
+    if (f < 16 || !F.more) {
+      if (q < W && F.rs + q < F.n) {
+        double *g = F.gE + 8 * f;
+        if (F.ok0) g[0] = acc[u][0];
+        if (F.ok1) g[F.lde2] = acc[u][1];
       }
-      for (int64_t j = 0; j < J; j++, cnt++) {
-        const int bi = (int)(cnt & 1);
-        const int64_t rs = i0 + 1 + j * NB;
-        const bool more = j + 1 < J;
-        mbar_wait(full_bar(bi), (unsigned)((cnt >> 1) & 1));
-        if (active) {
-          cp_async_wait<0>();
-          __syncwarp();
-          const double *vc = reinterpret_cast<const double *>(vc_buf(bi));
-          const double *tt = reinterpret_cast<const double *>(t_buf(bi));
-          // chunk c (window rows 32c..32c+31) -> slot base (doubles)
-          const int ch0 = 2 * 32 * ((0 + base / 32) % 3), ch1 = 2 * 32 * ((1 + base / 32) % 3),
-                    ch2 = 2 * 32 * ((2 + base / 32) % 3);
-          // ---------------- phase A: Y = V^H E   (M-fragment mf nonzero on k-steps 2mf .. 2mf+33)
-          double y[8][2];
-#pragma unroll
-          for (int mf = 0; mf < 8; mf++) y[mf][0] = y[mf][1] = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < 48; ks++) {
-            const int ch = ks < 16 ? ch0 : (ks < 32 ? ch1 : ch2);
-            const double e = ew[ch + offEB + 4 * (ks & 15)];
-#pragma unroll
-            for (int mf = 0; mf < 8; mf++)
-              if (ks >= 2 * mf && ks <= 2 * mf + 33)
-                dmma_nv(y[mf], xsign(vc[offA + 568 * mf + 4 * ks - 0], le.a_neg_conj), e);
-          }
-          double yb[16];
-          acc_to_b<8>(y, yb, lane);
-          // ---------------- phase B: Y = T Y   (T upper triangular: k-steps 2mf .. 15)
-#pragma unroll
-          for (int mf = 0; mf < 8; mf++) {
-            y[mf][0] = y[mf][1] = 0.0;
-#pragma unroll
-            for (int ks = 2 * mf; ks < 16; ks++) dmma_nv(y[mf], xsign(tt[offT + 144 * ks + 8 * mf], le.a_neg), yb[ks]);
-          }
-          acc_to_b<8>(y, yb, lane);
-          // ---------------- phase C: E -= V Y, row groups f (rows 4f..4f+3), k-steps klo(f)..khi(f)
-          double *gE = reinterpret_cast<double *>(a.E + rs + (rr >> 1) + (c0 + cA) * a.lde) + (rr & 1);
-          const int64_t lde2 = 2 * a.lde;
-#pragma unroll
-          for (int fb = 0; fb < 24; fb += 4) {
-            if (fb == 16 && more) {
-              __syncwarp();
-              // rows 0..63 are final and stored: refill their slots (and the
-              // padding slot) with the next block's rows 95..158
-              for (int h = 0; h < 2; h++) {
-                const int i = lane + 32 * h;
-                int slot = base - 1 + i;
-                slot = slot < 0 ? slot + RING : (slot >= RING ? slot - RING : slot);
-                const int64_t row = rs + W + i;
-#pragma unroll
-                for (int c = 0; c < 8; c++) {
-                  const bool ok = row < a.n && c < ncols;
-                  cp_async16(&Ew[c * LDE + slot], ok ? a.E + row + (c0 + c) * a.lde : a.E, ok);
-                }
-              }
-              cp_async_commit();
-            }
-            double acc[4][2];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              const int f = fb + u;
-              const int ch = f < 8 ? ch0 : (f < 16 ? ch1 : ch2);
-              const double *p = ew + ch + offEC + 8 * (f & 7);
-              acc[u][0] = p[0];
-              acc[u][1] = p[2 * LDE];
-            }
-#pragma unroll
-            for (int ks = 0; ks < 16; ks++) {
-#pragma unroll
-              for (int u = 0; u < 4; u++) {
-                const int f = fb + u;
-                const int klo = imax_c(0, 4 * f - 63) >> 1, khi = imin_c(31, 4 * f + 3) >> 1;
-                if (ks >= klo && ks <= khi) dmma_nv(acc[u], xsign(vc[offC + 284 * ks + 8 * f], negA), yb[ks]);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              const int f = fb + u;
-              const int q = 4 * f + (rr >> 1);
-              if (f < 16 || !more) {
-                if (q < W && rs + q < a.n) {
-                  double *g = gE + 8 * f;
-                  if (okA0) g[0] = acc[u][0];
-                  if (okA1) g[lde2] = acc[u][1];
-                }
-              } else if (q < W) {
-                double *p = ew + ch2 + offEC + 8 * (f & 7);
-                p[0] = acc[u][0];
-                p[2 * LDE] = acc[u][1];
-              }
-            }
-          }
-          if (!more) __threadfence_block();   // the next group re-reads these rows
-          base = base + NB >= RING ? base + NB - RING : base + NB;
-        }
+      if (REFILL && f < 16 && F.more) {
+        // slot of current row 4f + r receives the next block's row 4f + r + 32
+        const int r = L.lane & 3, c = L.lane >> 2;
+        const int slot = ring_slot(4 * f + r + F.base);
+        const int64_t row = F.rs + RING + 4 * f + r;
+        const bool ok = row < F.n && c < F.ncols;
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty_bar(bi));
+        cp_async16m(&F.Ew[c * LDE + slot], ok ? F.E + row + (F.c0 + c) * F.lde : F.E, ok);
       }
+    } else if (q < W) {
+      double *p = F.ew + F.ch2 + L.offEC + 8 * (f & 7);
+      p[0] = acc[u][0];
+      p[2 * LDE] = acc[u][1];
     }
   }
 }
 
-__global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a, int nslab) {
+template <int FB>
+struct FullRows {
+  __device__ static constexpr int f(int u) { return FB + u; }
+};
+template <int I>
+struct QuadLow {   // row groups < 16 of quad warp I (balanced: 2I+2 + 16-2I + 16 + 16 k-steps)
+  __device__ static constexpr int f(int u) { return u == 0 ? I : u == 1 ? 7 - I : u == 2 ? 8 + I : 15 - I; }
+};
+template <int I>
+struct QuadHigh {
+  __device__ static constexpr int f(int u) { return u == 0 ? 16 + I : 23 - I; }
+};
+
+// Full warp: the whole block for its own fragment.
+__device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const double *vc, const double *tt) {
+  // ---------------- phase A: Y = V^H E   (M-fragment mf nonzero on k-steps 2mf .. 2mf+33)
+  double y[8][2];
+#pragma unroll
+  for (int mf = 0; mf < 8; mf++) y[mf][0] = y[mf][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 48; ks++) {
+    const int ch = ks < 16 ? F.ch0 : (ks < 32 ? F.ch1 : F.ch2);
+    const double e = F.ew[ch + L.offEB + 4 * (ks & 15)];
+#pragma unroll
+    for (int mf = 0; mf < 8; mf++)
+      if (ks >= 2 * mf && ks <= 2 * mf + 33) dmma_nv(y[mf], xsign(vc[L.offA + 568 * mf + 4 * ks], L.negConj), e);
+  }
+  double yb[16];
+  acc_to_b<8>(y, yb, L.lane);
+  // ---------------- phase B: Y = T Y   (T upper triangular: k-steps 2mf .. 15)
+#pragma unroll
+  for (int mf = 0; mf < 8; mf++) {
+    y[mf][0] = y[mf][1] = 0.0;
+#pragma unroll
+    for (int ks = 2 * mf; ks < 16; ks++) dmma_nv(y[mf], xsign(tt[L.offT + 136 * ks + 8 * mf], L.negT), yb[ks]);
+  }
+  acc_to_b<8>(y, yb, L.lane);
+  // ---------------- phase C
+  phase_c_rows<4, FullRows<0>, false>(F, L, vc, yb);
+  phase_c_rows<4, FullRows<4>, false>(F, L, vc, yb);
+  phase_c_rows<4, FullRows<8>, false>(F, L, vc, yb);
+  phase_c_rows<4, FullRows<12>, false>(F, L, vc, yb);
+  if (F.more) {
+    // rows 0..63 are stored: refill their slots (and the padding slot) with the next block's rows 95..158
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int i = L.lane + 32 * h;
+      const int slot = ring_slot(F.base - 1 + i);
+      const int64_t row = F.rs + W + i;
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const bool ok = row < F.n && c < F.ncols;
+        cp_async16m(&F.Ew[c * LDE + slot], ok ? F.E + row + (F.c0 + c) * F.lde : F.E, ok);
+      }
+    }
+    cp_async_commit();
+  }
+  phase_c_rows<4, FullRows<16>, false>(F, L, vc, yb);
+  phase_c_rows<4, FullRows<20>, false>(F, L, vc, yb);
+}
+
+// Quad warp I: a quarter of every phase of the shared fragment.
+template <int I>
+__device__ __forceinline__ void quad_block(const Frag &F, const Lane &L, const double *vc, const double *tt) {
+  double *yq = reinterpret_cast<double *>(q2w_sm + OFF_Y);
+  double *y2q = reinterpret_cast<double *>(q2w_sm + OFF_Y2);
+  const int lane = L.lane;
+  // ---------------- phase A: M-fragments 2I, 2I+1
+  double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int ks = 4 * I; ks < imin_c(48, 4 * I + 36); ks++) {
+    const int ch = ks < 16 ? F.ch0 : (ks < 32 ? F.ch1 : F.ch2);
+    const double e = F.ew[ch + L.offEB + 4 * (ks & 15)];
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int mf = 2 * I + u;
+      if (ks >= 2 * mf && ks <= 2 * mf + 33) dmma_nv(y[u], xsign(vc[L.offA + 568 * mf + 4 * ks], L.negConj), e);
+    }
+  }
+  // Y[col][refl] (accumulator layout: refl 4mf + rr>>1, comp rr&1, cols 2(lane&3), +1)
+#pragma unroll
+  for (int u = 0; u < 2; u++) {
+    const int refl = 4 * (2 * I + u) + (L.rr >> 1);
+#pragma unroll
+    for (int c = 0; c < 2; c++) yq[2 * ((2 * (lane & 3) + c) * LDY + refl) + (L.rr & 1)] = y[u][c];
+  }
+  quad_sync();
+  // ---------------- phase B: M-fragments I, 7-I (k-steps 2mf .. 15)
+  const int offYB = 2 * ((lane >> 2) * LDY + L.kq) + (lane & 1);
+#pragma unroll
+  for (int u = 0; u < 2; u++) {
+    const int mf = u == 0 ? I : 7 - I;
+    y[u][0] = y[u][1] = 0.0;
+#pragma unroll
+    for (int ks = 2 * mf; ks < 16; ks++) dmma_nv(y[u], xsign(tt[L.offT + 136 * ks + 8 * mf], L.negT), yq[offYB + 4 * ks]);
+  }
+#pragma unroll
+  for (int u = 0; u < 2; u++) {
+    const int refl = 4 * (u == 0 ? I : 7 - I) + (L.rr >> 1);
+#pragma unroll
+    for (int c = 0; c < 2; c++) y2q[2 * ((2 * (lane & 3) + c) * LDY + refl) + (L.rr & 1)] = y[u][c];
+  }
+  quad_sync();
+  // ---------------- phase C: row groups {I, 7-I, 8+I, 15-I} then {16+I, 23-I}
+  double yb[16];
+#pragma unroll
+  for (int ks = 0; ks < 16; ks++) yb[ks] = y2q[offYB + 4 * ks];
+  if (I == 0 && F.more) {
+    // the padding slot (current row 95) receives the next block's row 31
+    const int c = lane >> 2;
+    const int64_t row = F.rs + W;
+    const bool ok = (lane & 3) == 0 && row < F.n && c < F.ncols;
+    if ((lane & 3) == 0) cp_async16m(&F.Ew[c * LDE + ring_slot(F.base - 1)], ok ? F.E + row + (F.c0 + c) * F.lde : F.E, ok);
+  }
+  phase_c_rows<4, QuadLow<I>, true>(F, L, vc, yb);
+  cp_async_commit();
+  phase_c_rows<2, QuadHigh<I>, false>(F, L, vc, yb);
+}
+
+// ---------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // zero the compact V buffers once (their pads are never written again) and the E windows
   for (int e = threadIdx.x; e < OFF_T; e += WT) q2w_sm[e] = czero();
-  for (int e = threadIdx.x; e < NCW * 8 * LDE; e += WT) q2w_sm[OFF_E + e] = czero();
+  for (int e = threadIdx.x; e < NFS * 8 * LDE; e += WT) q2w_sm[OFF_E + e] = czero();
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; i++) {
       mbar_init(full_bar(i), 1);
-      mbar_init(empty_bar(i), NCW);
+      *done_cnt(i) = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  BlkIt cur, ahead;
+  it_begin(a, cur);
+  ahead = cur;
+  if (w == 0) {   // prologue: blocks 0 and 1
+    if (ahead.valid) issue_block(a, ahead, 0, lane);
+    it_next(a, ahead);
+    if (ahead.valid) issue_block(a, ahead, 1, lane);
+    it_next(a, ahead);
+  } else {
+    it_next(a, ahead);
+    it_next(a, ahead);
+  }
   const int F = a.nfr_total, Gd = gridDim.x;
   const int f0 = (int)((int64_t)F * blockIdx.x / Gd), f1 = (int)((int64_t)F * (blockIdx.x + 1) / Gd);
-  if ((threadIdx.x >> 5) == NCW) q2w_producer(a, nslab);
-  else q2w_consumer(a, f0, f1, nslab);
+  const bool quad = w >= NFW;
+  const int qi = w - NFW;
+  const Lane L(lane);
+  Frag Fr;
+  Fr.Ew = q2w_sm + OFF_E + (quad ? NFW : w) * 8 * LDE;
+  Fr.ew = reinterpret_cast<double *>(Fr.Ew);
+  Fr.E = a.E;
+  Fr.lde = a.lde;
+  Fr.lde2 = 2 * a.lde;
+  Fr.n = a.n;
+  bool active = false;
+  int cur_sl = -1;
+  int64_t cnt = 0;
+  while (cur.valid) {
+    if (cur.sl != cur_sl) {
+      cur_sl = cur.sl;
+      const int s0 = f0 + cur_sl * NFS;
+      const int k = imax_c(0, imin_c(NFS, f1 - s0));
+      const bool quad_on = (k & 3) == 1;
+      const int nfull = quad_on ? k - 1 : k;
+      active = quad ? quad_on : (w < nfull);
+      const int fr = quad ? s0 + nfull : s0 + w;
+      Fr.c0 = (int64_t)fr * 8;
+      Fr.ncols = active ? (int)imin64(8, a.m - Fr.c0) : 0;
+      const int cA = 2 * (lane & 3);
+      Fr.ok0 = cA < Fr.ncols;
+      Fr.ok1 = cA + 1 < Fr.ncols;
+    }
+    const int64_t i0 = cur.gi * G;
+    if (cur.j == 0) {
+      Fr.base = 0;
+      if (active) {
+        // group start: the whole window, rows rs .. rs + 95 (row 95 is padding)
+        const int64_t rs = i0 + 1;
+        const int e0 = quad ? lane + 32 * qi : lane, es = quad ? 32 * NQW : 32;
+        for (int e = e0; e < RING * 8; e += es) {
+          const int q = e % RING, c = e / RING;
+          const int64_t row = rs + q;
+          const bool ok = q < W && row < a.n && c < Fr.ncols;
+          cp_async16m(&Fr.Ew[c * LDE + q], ok ? a.E + row + (Fr.c0 + c) * a.lde : a.E, ok);
+        }
+        cp_async_commit();
+      }
+    }
+    const int bi = (int)(cnt & 1);
+    Fr.rs = i0 + 1 + cur.j * NB;
+    Fr.more = cur.j + 1 < cur.J;
+    const bool prof = a.prof != nullptr && blockIdx.x == 0 && lane == 0 && (w == 0 || w == NFW);
+    long long t0 = prof ? clock64() : 0;
+    mbar_wait(full_bar(bi), (unsigned)((cnt >> 1) & 1));
+    long long t1 = prof ? clock64() : 0;
+    if (active) {
+      cp_async_wait<0>();
+      __syncwarp();
+      if (quad) quad_sync();   // the quad's refills and row-group stores of the previous block
+      Fr.ch0 = 2 * 32 * ((0 + Fr.base / 32) % 3);
+      Fr.ch1 = 2 * 32 * ((1 + Fr.base / 32) % 3);
+      Fr.ch2 = 2 * 32 * ((2 + Fr.base / 32) % 3);
+      Fr.gE = reinterpret_cast<double *>(a.E + Fr.rs + (L.rr >> 1) + (Fr.c0 + 2 * (lane & 3)) * a.lde) + (L.rr & 1);
+      const double *vc = reinterpret_cast<const double *>(vc_buf(bi));
+      const double *tt = reinterpret_cast<const double *>(t_buf(bi));
+      if (!quad) full_block(Fr, L, vc, tt);
+      else if (qi == 0) quad_block<0>(Fr, L, vc, tt);
+      else if (qi == 1) quad_block<1>(Fr, L, vc, tt);
+      else if (qi == 2) quad_block<2>(Fr, L, vc, tt);
+      else quad_block<3>(Fr, L, vc, tt);
+      if (!Fr.more) __threadfence_block();   // the next group re-reads these rows
+      Fr.base = Fr.base + NB >= RING ? Fr.base + NB - RING : Fr.base + NB;
+    }
+    // release buffer bi; the last warp refills it with the block two ahead
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd(done_cnt(bi), 1) == NW - 1;
+      if (last) *done_cnt(bi) = 0;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last && ahead.valid) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_block(a, ahead, bi, lane);
+    }
+    if (prof) {
+      const long long t2 = clock64();
+      unsigned long long *pp = a.prof + 24 + (w == 0 ? 0 : 3);
+      pp[0] += t1 - t0;
+      pp[2] += t2 - t1;
+    }
+    it_next(a, cur);
+    it_next(a, ahead);
+    cnt++;
+  }
 }
 
 }  // namespace
 
-size_t q2w_smem_bytes() {
-  return (size_t)OFF_BAR * sizeof(double2) + 4 * sizeof(uint64_t);
-}
+size_t q2w_smem_bytes() { return (size_t)OFF_BAR * sizeof(double2) + 32; }
 
 // Returns 1 if the shape is not handled here (caller falls back to q2.cu).
 int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, double2 *E, int64_t lde, int64_t m) {
@@ -307,9 +528,10 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
   a.T2 = T2;
   a.E = E;
   a.nfr_total = (int)((m + 7) / 8);
+  a.prof = ctx.q2_prof;
   const int grid = std::min(ctx.num_sms, a.nfr_total);
   const int per = (a.nfr_total + grid - 1) / grid;
-  const int nslab = (per + NCW - 1) / NCW;
+  a.nslab = (per + NFS - 1) / NFS;
   const size_t smem = q2w_smem_bytes();
   static bool attr = false;
   if (!attr) {
@@ -317,7 +539,7 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
                       "q2w attr"));
     attr = true;
   }
-  apply_q2w_kernel<<<grid, WT, smem, ctx.stream>>>(a, nslab);
+  apply_q2w_kernel<<<grid, WT, smem, ctx.stream>>>(a);
   EIG_TRY(ctx.launched("apply_q2w_kernel"));
   return 0;
 }

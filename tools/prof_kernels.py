@@ -77,8 +77,10 @@ def main():
         print(f"apply_q2 n={n} m={m} nb={a.nb} g={s.q2_group}: {ms:.3f} ms  {8.0 * n * n * m / ms / 1e9:.2f} TFLOP/s")
         if os.environ.get("EIG_Q2_PROFILE"):
             pr = s.q2_profile()[:5]
-            tot = sum(pr)
+            tot = max(sum(pr), 1)
             print("  CTA0 phase cycles (load, A, B, C, commit):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
+            pw = s.q2_profile()[24:30]
+            print("  q2w CTA0 warp0 (wait, -, wait+work+release), quad warp (same):", pw)
     elif a.mode == "hb2st":
         A0 = colmajor(synth.rand_hermitian(n, 0), dev)
         s.he2hb(A0)
@@ -87,7 +89,7 @@ def main():
         if os.environ.get("EIG_Q2_PROFILE"):
             pr = s.q2_profile()[16:22]
             tot = sum(pr)
-            print("  hb2st CTA0 (wait, refl, a, b, c, flag):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
+            print("  hb2st CTA0 (wait, load, refl, update, -, flag):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
     elif a.mode == "he2hb":
         A0 = colmajor(synth.rand_hermitian(n, 0), dev)
         A = A0.clone()
