@@ -166,14 +166,27 @@ __device__ __forceinline__ void it_next(const Q2wArgs &a, BlkIt &it) {
 }
 
 // Warp-wide: bulk copies of block `it`'s V (live slots) and T into buffer bi.
-__device__ __forceinline__ void issue_block(const Q2wArgs &a, const BlkIt &it, int bi, int lane) {
-  const int64_t i0 = it.gi * G, j = it.j;
-  const int nvalid = (int)imax64(0, imin64(G, a.n - 2 - j * NB - i0 + 1));
+// The global offsets of a block (off[j], first[gi]) are read when the
+// iterator reaches it, two blocks before its copies are issued.
+struct BlkSrc {
+  int64_t offj, firstg;   // raw off[j], first[gi] (used only when the copies are issued)
+  int64_t gi, j;
+};
+__device__ __forceinline__ BlkSrc blk_src(const Q2wArgs &a, const BlkIt &it) {
+  BlkSrc b;
+  b.gi = it.gi;
+  b.j = it.j;
+  b.offj = it.valid ? a.off[it.j] : 0;
+  b.firstg = it.valid ? a.first[it.gi] : 0;
+  return b;
+}
+__device__ __forceinline__ void issue_block(const Q2wArgs &a, const BlkSrc &b, int bi, int lane) {
+  const int64_t i0 = b.gi * G;
+  const int nvalid = (int)imax64(0, imin64(G, a.n - 2 - b.j * NB - i0 + 1));
   if (lane == 0) mbar_arrive_tx(full_bar(bi), (unsigned)(nvalid * NB * 16 + G * G * 16));
   __syncwarp();
-  const double2 *v2 = a.V2 + (a.off[j] + i0) * NB;
-  if (lane < nvalid) bulk_g2s(vc_buf(bi) + vrow(lane) + PADL, v2 + lane * NB, NB * 16, full_bar(bi));
-  bulk_g2s(t_buf(bi) + tcol(lane), a.T2 + (a.first[it.gi] + j) * G * G + lane * G, G * 16, full_bar(bi));
+  if (lane < nvalid) bulk_g2s(vc_buf(bi) + vrow(lane) + PADL, a.V2 + (b.offj + i0 + lane) * NB, NB * 16, full_bar(bi));
+  bulk_g2s(t_buf(bi) + tcol(lane), a.T2 + (b.firstg + b.j) * G * G + lane * G, G * 16, full_bar(bi));
 }
 
 // ---------------------------------------------------------------- per-lane constants
@@ -272,6 +285,12 @@ template <int FB>
 struct FullRows {
   __device__ static constexpr int f(int u) { return FB + u; }
 };
+struct PairsA {   // (f, f + 17): k-step ranges [0, 2f+1] and [2f+2, 15]
+  __device__ static constexpr int f(int u) { return (u & 1) ? 17 + (u >> 1) : (u >> 1); }
+};
+struct PairsB {
+  __device__ static constexpr int f(int u) { return u == 6 ? 7 : u == 7 ? 16 : ((u & 1) ? 21 + (u >> 1) : 4 + (u >> 1)); }
+};
 template <int I>
 struct QuadLow {   // row groups < 16 of quad warp I (balanced: 2I+2 + 16-2I + 16 + 16 k-steps)
   __device__ static constexpr int f(int u) { return u == 0 ? I : u == 1 ? 7 - I : u == 2 ? 8 + I : 15 - I; }
@@ -282,13 +301,25 @@ struct QuadHigh {
 };
 
 // Full warp: the whole block for its own fragment.
-__device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const double *vc, const double *tt) {
+__device__ __forceinline__ void pmark(unsigned long long *pp, long long &tl, int k) {
+  if (pp) {
+    const long long t = clock64();
+    pp[k] += t - tl;
+    tl = t;
+  }
+}
+__device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const double *vc, const double *tt,
+                                           unsigned long long *pp, long long &tl) {
   // ---------------- phase A: Y = V^H E   (M-fragment mf nonzero on k-steps 2mf .. 2mf+33)
   double y[8][2];
 #pragma unroll
   for (int mf = 0; mf < 8; mf++) y[mf][0] = y[mf][1] = 0.0;
 #pragma unroll
   for (int ks = 0; ks < 48; ks++) {
+    if (ks == 15) {   // rows 31..63 (cp.async group Y of the previous block)
+      cp_async_wait<0>();
+      __syncwarp();
+    }
     const int ch = ks < 16 ? F.ch0 : (ks < 32 ? F.ch1 : F.ch2);
     const double e = F.ew[ch + L.offEB + 4 * (ks & 15)];
 #pragma unroll
@@ -297,6 +328,7 @@ __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const d
   }
   double yb[16];
   acc_to_b<8>(y, yb, L.lane);
+  pmark(pp, tl, 1);
   // ---------------- phase B: Y = T Y   (T upper triangular: k-steps 2mf .. 15)
 #pragma unroll
   for (int mf = 0; mf < 8; mf++) {
@@ -305,29 +337,48 @@ __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const d
     for (int ks = 2 * mf; ks < 16; ks++) dmma_nv(y[mf], xsign(tt[L.offT + 136 * ks + 8 * mf], L.negT), yb[ks]);
   }
   acc_to_b<8>(y, yb, L.lane);
-  // ---------------- phase C
-  phase_c_rows<4, FullRows<0>, false>(F, L, vc, yb);
-  phase_c_rows<4, FullRows<4>, false>(F, L, vc, yb);
+  pmark(pp, tl, 2);
+  // ---------------- phase C, rows 32..63 first, then the rows 0..31 paired with
+  // rows 64..95 so that every batch keeps four independent accumulators busy
   phase_c_rows<4, FullRows<8>, false>(F, L, vc, yb);
   phase_c_rows<4, FullRows<12>, false>(F, L, vc, yb);
   if (F.more) {
-    // rows 0..63 are stored: refill their slots (and the padding slot) with the next block's rows 95..158
+    // slots of current rows 32..62 <- next block's rows 64..94 (global rs + 96 + r)
     __syncwarp();
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int i = L.lane + 32 * h;
-      const int slot = ring_slot(F.base - 1 + i);
-      const int64_t row = F.rs + W + i;
+    const int r = 32 + L.lane;
+    if (r < 63) {
+      const int slot = ring_slot(F.base + r);
+      const int64_t row = F.rs + RING + r;
 #pragma unroll
       for (int c = 0; c < 8; c++) {
         const bool ok = row < F.n && c < F.ncols;
         cp_async16m(&F.Ew[c * LDE + slot], ok ? F.E + row + (F.c0 + c) * F.lde : F.E, ok);
       }
     }
-    cp_async_commit();
   }
-  phase_c_rows<4, FullRows<16>, false>(F, L, vc, yb);
-  phase_c_rows<4, FullRows<20>, false>(F, L, vc, yb);
+  cp_async_commit();   // group X (possibly empty)
+  phase_c_rows<8, PairsA, false>(F, L, vc, yb);
+  phase_c_rows<8, PairsB, false>(F, L, vc, yb);
+  if (F.more) {
+    // slots of current rows 0..31 <- next rows 32..63; the padding slot (row 95) <- next row 31
+    __syncwarp();
+    const int r = L.lane;
+    const int slot = ring_slot(F.base + r);
+    const int64_t row = F.rs + RING + r;
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      const bool ok = row < F.n && c < F.ncols;
+      cp_async16m(&F.Ew[c * LDE + slot], ok ? F.E + row + (F.c0 + c) * F.lde : F.E, ok);
+    }
+    if (L.lane < 8) {
+      const int64_t prow = F.rs + W;
+      const int c = L.lane;
+      const bool ok = prow < F.n && c < F.ncols;
+      cp_async16m(&F.Ew[c * LDE + ring_slot(F.base - 1)], ok ? F.E + prow + (F.c0 + c) * F.lde : F.E, ok);
+    }
+  }
+  cp_async_commit();   // group Y (possibly empty): needed from phase A k-step 15 of the next block
+  pmark(pp, tl, 3);
 }
 
 // Quad warp I: a quarter of every phase of the shared fragment.
@@ -406,9 +457,9 @@ __global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
   it_begin(a, cur);
   ahead = cur;
   if (w == 0) {   // prologue: blocks 0 and 1
-    if (ahead.valid) issue_block(a, ahead, 0, lane);
+    if (ahead.valid) issue_block(a, blk_src(a, ahead), 0, lane);
     it_next(a, ahead);
-    if (ahead.valid) issue_block(a, ahead, 1, lane);
+    if (ahead.valid) issue_block(a, blk_src(a, ahead), 1, lane);
     it_next(a, ahead);
   } else {
     it_next(a, ahead);
@@ -426,17 +477,23 @@ __global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
   Fr.lde = a.lde;
   Fr.lde2 = 2 * a.lde;
   Fr.n = a.n;
+  // fragments of slab sl in this CTA, and how many warps work on them
+  auto slab_k = [&](int sl) { return imax_c(0, imin_c(NFS, f1 - (f0 + sl * NFS))); };
+  auto n_active = [](int k) { return ((k & 3) == 1) ? k - 1 + NQW : k; };
+  BlkSrc asrc;
   bool active = false;
-  int cur_sl = -1;
+  int cur_sl = -1, nact = 0;
   int64_t cnt = 0;
   while (cur.valid) {
     if (cur.sl != cur_sl) {
       cur_sl = cur.sl;
       const int s0 = f0 + cur_sl * NFS;
-      const int k = imax_c(0, imin_c(NFS, f1 - s0));
+      const int k = slab_k(cur_sl);
       const bool quad_on = (k & 3) == 1;
       const int nfull = quad_on ? k - 1 : k;
+      nact = n_active(k);
       active = quad ? quad_on : (w < nfull);
+      if (active) asrc = blk_src(a, ahead);
       const int fr = quad ? s0 + nfull : s0 + w;
       Fr.c0 = (int64_t)fr * 8;
       Fr.ncols = active ? (int)imin64(8, a.m - Fr.c0) : 0;
@@ -458,26 +515,39 @@ __global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
           cp_async16m(&Fr.Ew[c * LDE + q], ok ? a.E + row + (Fr.c0 + c) * a.lde : a.E, ok);
         }
         cp_async_commit();
+        cp_async_commit();   // empty group: the full warps' wait<1> then covers the window
       }
     }
     const int bi = (int)(cnt & 1);
+    if (!active) {   // idle in this slab: keep the block count, touch nothing
+      it_next(a, cur);
+      it_next(a, ahead);
+      cnt++;
+      continue;
+    }
     Fr.rs = i0 + 1 + cur.j * NB;
     Fr.more = cur.j + 1 < cur.J;
-    const bool prof = a.prof != nullptr && blockIdx.x == 0 && lane == 0 && (w == 0 || w == NFW);
-    long long t0 = prof ? clock64() : 0;
+    const bool prof = a.prof != nullptr && blockIdx.x == 0 && lane == 0 && w == 0;
+    unsigned long long *pp = prof ? a.prof + 24 : nullptr;
+    long long tl = prof ? clock64() : 0;
     mbar_wait(full_bar(bi), (unsigned)((cnt >> 1) & 1));
-    long long t1 = prof ? clock64() : 0;
-    if (active) {
-      cp_async_wait<0>();
-      __syncwarp();
-      if (quad) quad_sync();   // the quad's refills and row-group stores of the previous block
+    pmark(pp, tl, 0);
+    {
+      if (quad) {
+        cp_async_wait<0>();
+        __syncwarp();
+        quad_sync();   // the quad's refills and row-group stores of the previous block
+      } else {
+        cp_async_wait<1>();   // group X (rows 64..94 of this block's window); Y is awaited in phase A
+        __syncwarp();
+      }   // the quad's refills and row-group stores of the previous block
       Fr.ch0 = 2 * 32 * ((0 + Fr.base / 32) % 3);
       Fr.ch1 = 2 * 32 * ((1 + Fr.base / 32) % 3);
       Fr.ch2 = 2 * 32 * ((2 + Fr.base / 32) % 3);
       Fr.gE = reinterpret_cast<double *>(a.E + Fr.rs + (L.rr >> 1) + (Fr.c0 + 2 * (lane & 3)) * a.lde) + (L.rr & 1);
       const double *vc = reinterpret_cast<const double *>(vc_buf(bi));
       const double *tt = reinterpret_cast<const double *>(t_buf(bi));
-      if (!quad) full_block(Fr, L, vc, tt);
+      if (!quad) full_block(Fr, L, vc, tt, pp, tl);
       else if (qi == 0) quad_block<0>(Fr, L, vc, tt);
       else if (qi == 1) quad_block<1>(Fr, L, vc, tt);
       else if (qi == 2) quad_block<2>(Fr, L, vc, tt);
@@ -486,26 +556,22 @@ __global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
       Fr.base = Fr.base + NB >= RING ? Fr.base + NB - RING : Fr.base + NB;
     }
     // release buffer bi; the last warp refills it with the block two ahead
+    // (every value this warp loaded from it has been consumed by now)
     __syncwarp();
     int last = 0;
     if (lane == 0) {
-      __threadfence_block();
-      last = atomicAdd(done_cnt(bi), 1) == NW - 1;
+      last = atomicAdd(done_cnt(bi), 1) == nact - 1;
       if (last) *done_cnt(bi) = 0;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && ahead.valid) {
+    if (last && ahead.valid && slab_k(ahead.sl) > 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_block(a, ahead, bi, lane);
+      issue_block(a, asrc, bi, lane);
     }
-    if (prof) {
-      const long long t2 = clock64();
-      unsigned long long *pp = a.prof + 24 + (w == 0 ? 0 : 3);
-      pp[0] += t1 - t0;
-      pp[2] += t2 - t1;
-    }
+    pmark(pp, tl, 4);
     it_next(a, cur);
     it_next(a, ahead);
+    asrc = blk_src(a, ahead);
     cnt++;
   }
 }
