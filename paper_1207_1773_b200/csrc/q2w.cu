@@ -81,10 +81,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// L2 policies: the E stream (read and written once per group) is evict-first,
+// the V / T blocks (read by every CTA) evict-last.
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   su32(dst)),
-               "l"(src), "r"(bytes), "r"(su32(bar))
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol_evict_last())
+      : "memory");
+}
+__device__ __forceinline__ void st_stream(double *p, double v) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol_evict_first())
                : "memory");
 }
 // non-volatile DMMA: lets the scheduler interleave the unrolled tiles freely
@@ -94,7 +111,8 @@ __device__ __forceinline__ void dmma_nv(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 __device__ __forceinline__ void cp_async16m(void *smem, const void *gmem, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(su32(smem)), "l"(gmem), "r"(valid ? 16 : 0)
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(su32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0), "l"(pol_evict_first())
                : "memory");
 }
 __device__ __forceinline__ void quad_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
