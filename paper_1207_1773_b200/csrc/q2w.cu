@@ -53,6 +53,9 @@ constexpr int LDY = 34;                          // quad Y exchange: Y[col][refl
 constexpr int NFW = 8, NQW = 4, NW = NFW + NQW;  // full warps, quad warps
 constexpr int NFS = NFW + 1;                     // fragments per slab
 constexpr int WT = NW * 32;
+#ifndef Q2W_QUAD
+#define Q2W_QUAD 1   // 0: the 9th fragment goes to warp 8 as a full warp (measured 20% slower)
+#endif
 
 struct Q2wArgs {
   int64_t n, m, lde;
@@ -485,11 +488,11 @@ __global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
   }
   const int F = a.nfr_total, Gd = gridDim.x;
   const int f0 = (int)((int64_t)F * blockIdx.x / Gd), f1 = (int)((int64_t)F * (blockIdx.x + 1) / Gd);
-  const bool quad = w >= NFW;
+  const bool quad = Q2W_QUAD && w >= NFW;
   const int qi = w - NFW;
   const Lane L(lane);
   Frag Fr;
-  Fr.Ew = q2w_sm + OFF_E + (quad ? NFW : w) * 8 * LDE;
+  Fr.Ew = q2w_sm + OFF_E + (quad ? NFW : imin_c(w, NFW)) * 8 * LDE;
   Fr.ew = reinterpret_cast<double *>(Fr.Ew);
   Fr.E = a.E;
   Fr.lde = a.lde;
@@ -497,7 +500,7 @@ __global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
   Fr.n = a.n;
   // fragments of slab sl in this CTA, and how many warps work on them
   auto slab_k = [&](int sl) { return imax_c(0, imin_c(NFS, f1 - (f0 + sl * NFS))); };
-  auto n_active = [](int k) { return ((k & 3) == 1) ? k - 1 + NQW : k; };
+  auto n_active = [](int k) { return (Q2W_QUAD && (k & 3) == 1) ? k - 1 + NQW : k; };
   BlkSrc asrc;
   bool active = false;
   int cur_sl = -1, nact = 0;
@@ -507,7 +510,7 @@ __global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
       cur_sl = cur.sl;
       const int s0 = f0 + cur_sl * NFS;
       const int k = slab_k(cur_sl);
-      const bool quad_on = (k & 3) == 1;
+      const bool quad_on = Q2W_QUAD && (k & 3) == 1;
       const int nfull = quad_on ? k - 1 : k;
       nact = n_active(k);
       active = quad ? quad_on : (w < nfull);

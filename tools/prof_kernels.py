@@ -41,6 +41,7 @@ def main():
     p.add_argument("--nb", type=int, default=64)
     p.add_argument("--g", type=int, default=0)
     p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--kw", type=int, default=0, help="gemm mode: panel width of the V^H E / E -= V Y shapes (default nb)")
     a = p.parse_args()
     dev = torch.device("cuda:0")
     s = Solver(0, nb=a.nb, q2_group=a.g)
@@ -61,13 +62,15 @@ def main():
         VX = torch.randn(2 * a.nb, n, dtype=torch.complex128, device=dev).t()
         ms = timeit(lambda: s.zgemm("N", "C", VX, VX, H, alpha=-1.0, beta=1.0, lower_c=True), a.reps)
         print(f"her2k {n} k={2 * a.nb}: {ms:.3f} ms  {8.0 * n * n * a.nb / ms / 1e9:.2f} TFLOP/s (nominal 8 s^2 nb)")
-        Y = torch.zeros(m, a.nb, dtype=torch.complex128, device=dev).t()
+        kw = a.kw or a.nb
+        V = torch.randn(kw, n, dtype=torch.complex128, device=dev).t()
+        Y = torch.zeros(m, kw, dtype=torch.complex128, device=dev).t()
         E = torch.randn(m, n, dtype=torch.complex128, device=dev).t()
         ms = timeit(lambda: s.zgemm("C", "N", V, E, Y), a.reps)
-        print(f"V^H E {a.nb}x{m} K={n}: {ms:.3f} ms  {8.0 * n * m * a.nb / ms / 1e9:.2f} TFLOP/s")
-        Y2 = torch.randn(m, a.nb, dtype=torch.complex128, device=dev).t()
+        print(f"V^H E {kw}x{m} K={n}: {ms:.3f} ms  {8.0 * n * m * kw / ms / 1e9:.2f} TFLOP/s")
+        Y2 = torch.randn(m, kw, dtype=torch.complex128, device=dev).t()
         ms = timeit(lambda: s.zgemm("N", "N", V, Y2, E, alpha=-1.0, beta=1.0), a.reps)
-        print(f"E -= V Y {n}x{m} K={a.nb}: {ms:.3f} ms  {8.0 * n * m * a.nb / ms / 1e9:.2f} TFLOP/s")
+        print(f"E -= V Y {n}x{m} K={kw}: {ms:.3f} ms  {8.0 * n * m * kw / ms / 1e9:.2f} TFLOP/s")
     elif a.mode == "q2":
         V2, tau2 = synth.synthetic_v2(n, a.nb, 0)
         V2d, t2d = torch.from_numpy(V2).to(dev), torch.from_numpy(tau2).to(dev)
