@@ -393,7 +393,8 @@ def run_b200(a, rank, world, local_rank):
             solver.hotpath_host(Ap.numpy().T, V2p.numpy(), t2p.numpy(), Lp.numpy().T, Zp.numpy().T, Ep.numpy().T)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) / e_steps
-        h2d = n * n * 16 * 2 + slots * nb * 16 + slots * 16 + n * m * 8
+        lower = sum((n - j0) * min(256, n - j0) for j0 in range(0, n, 256)) * 16   # A, L: lower 256-col blocks
+        h2d = 2 * lower + slots * nb * 16 + slots * 16 + n * m * 8
         d2h = n * m * 16
         e2e = {"value": flops / dt / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": dt * 1e3, "steps": e_steps}

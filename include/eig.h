@@ -144,8 +144,10 @@ int eig_trsm_lh(eig_handle h, int64_t n, const void *L, int64_t ldl, void *E, in
  *   V2, tau2  Q2 reflectors (layout above).
  *   L    n x n lower (ldl).   Z n x m real (ldz).   E n x m complex128 (lde) out.
  * flags: EIG_HOST_BUFFERS -> A, V2, tau2, L, Z, E are HOST pointers (pinned
- * recommended); the call copies them to the device, runs, copies E back and
- * returns synchronously.  EIG_SKIP_HE2HB / EIG_SKIP_BT select a part. */
+ * recommended); the call copies the lower triangle of A to the device,
+ * copies V2, tau2, Z and the lower triangle of L on a transfer stream while
+ * he2hb runs, copies each final 256-row block of E back while the triangular
+ * solve works on the blocks above it, and returns synchronously.  EIG_SKIP_HE2HB / EIG_SKIP_BT select a part. */
 int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void *T1, const void *V2,
                 const void *tau2, const void *L, int64_t ldl, const double *Z, int64_t ldz, void *E, int64_t lde,
                 int64_t m, unsigned flags);

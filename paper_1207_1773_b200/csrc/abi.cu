@@ -215,7 +215,11 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
 // the bulk of the flops in one GEMM each (M = 256, K = n - I1), the 256 x 256
 // diagonal block is solved with 64-row steps using precomputed inverses of
 // the 64 x 64 diagonal blocks of L.
-static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2 *E, int64_t lde, int64_t m) {
+// hostE (optional, pinned host, leading dimension ldh): every 256-row block of E
+// is copied back on the transfer stream as soon as it is final (bottom block
+// first), overlapping the copy with the remaining blocks.
+static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2 *E, int64_t lde, int64_t m,
+                       double2 *hostE = nullptr, int64_t ldh = 0) {
   if (n <= 0 || m <= 0) return 0;
   const int bs = 64, BS = 256;
   const int64_t nblk = (n + bs - 1) / bs;
@@ -244,6 +248,13 @@ static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2
       g.opa = OP_C; g.M = bi; g.N = m; g.K = bi; g.A = Linv + (i0 / bs) * bs * bs; g.lda = bs; g.B = E + i0;
       g.ldb = lde; g.C = E + i0; g.ldc = lde; g.alpha = 1.0; g.beta = 0.0; g.splitk = 1;
       EIG_TRY(zgemm(c, g));
+    }
+    if (hostE) {   // rows I0..I1-1 are final
+      EIG_TRY(c.check(cudaEventRecord(c.ev_blk, c.stream), "blk event"));
+      EIG_TRY(c.check(cudaStreamWaitEvent(c.xfer, c.ev_blk, 0), "blk wait"));
+      EIG_TRY(c.check(cudaMemcpy2DAsync(hostE + I0, ldh * sizeof(double2), E + I0, lde * sizeof(double2),
+                                        (I1 - I0) * sizeof(double2), m, cudaMemcpyDeviceToHost, c.xfer),
+                      "D2H E block"));
     }
   }
   return 0;
@@ -395,6 +406,9 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
   rc = x->c.check(cudaStreamCreateWithPriority(&x->c.side, cudaStreamNonBlocking, hi_prio), "side stream");
   if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_fork, cudaEventDisableTiming), "event");
   if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_join, cudaEventDisableTiming), "event");
+  if (!rc) rc = x->c.check(cudaStreamCreateWithFlags(&x->c.xfer, cudaStreamNonBlocking), "xfer stream");
+  if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_xfer, cudaEventDisableTiming), "event");
+  if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_blk, cudaEventDisableTiming), "event");
   if (rc) { delete x; return rc; }
   void *bar = x->c.ws(WS_BARRIER, 64);
   if (!bar) { delete x; return EIG_ERR_NOMEM; }
@@ -421,6 +435,9 @@ int eig_finalize(eig_handle h) {
   if (h->c.side) { cudaStreamSynchronize(h->c.side); cudaStreamDestroy(h->c.side); }
   if (h->c.ev_fork) cudaEventDestroy(h->c.ev_fork);
   if (h->c.ev_join) cudaEventDestroy(h->c.ev_join);
+  if (h->c.xfer) { cudaStreamSynchronize(h->c.xfer); cudaStreamDestroy(h->c.xfer); }
+  if (h->c.ev_xfer) cudaEventDestroy(h->c.ev_xfer);
+  if (h->c.ev_blk) cudaEventDestroy(h->c.ev_blk);
   for (int i = 0; i < WS_COUNT; i++) {
     if (h->c.buf[i]) cudaFree(h->c.buf[i]);
   }
@@ -574,34 +591,48 @@ int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void 
     dtau1 = (double2 *)c.ws(WS_HOST_TAU1, (size_t)std::max<int64_t>(K, 1) * nb * sizeof(double2));
     dT1 = (double2 *)c.ws(WS_HOST_T1, (size_t)std::max<int64_t>(K, 1) * nb * nb * sizeof(double2));
     if (!dA || !v2 || !t2 || !l || !z || !dE || !dtau1 || !dT1) return EIG_ERR_NOMEM;
-    EIG_TRY(c.check(cudaMemcpy2DAsync(dA, n * sizeof(double2), A, lda * sizeof(double2), n * sizeof(double2), n,
-                                      cudaMemcpyHostToDevice, c.stream), "H2D A"));
+    // only the lower triangle of A is referenced: upload it in 256-column blocks
+    for (int64_t j0 = 0; j0 < n; j0 += 256) {
+      const int64_t w = std::min<int64_t>(256, n - j0);
+      EIG_TRY(c.check(cudaMemcpy2DAsync(dA + j0 + j0 * n, n * sizeof(double2), (const double2 *)A + j0 + j0 * lda,
+                                        lda * sizeof(double2), (n - j0) * sizeof(double2), w, cudaMemcpyHostToDevice,
+                                        c.stream), "H2D A"));
+    }
     if (!(flags & EIG_SKIP_BT)) {
-      EIG_TRY(c.check(cudaMemcpyAsync(v2, V2, (size_t)slots * nb * sizeof(double2), cudaMemcpyHostToDevice, c.stream),
+      // the back-transform inputs travel on the transfer stream while he2hb runs
+      EIG_TRY(c.check(cudaEventRecord(c.ev_xfer, c.stream), "xfer fork"));
+      EIG_TRY(c.check(cudaStreamWaitEvent(c.xfer, c.ev_xfer, 0), "xfer fork wait"));
+      EIG_TRY(c.check(cudaMemcpyAsync(v2, V2, (size_t)slots * nb * sizeof(double2), cudaMemcpyHostToDevice, c.xfer),
                       "H2D V2"));
-      EIG_TRY(c.check(cudaMemcpyAsync(t2, tau2, (size_t)slots * sizeof(double2), cudaMemcpyHostToDevice, c.stream),
+      EIG_TRY(c.check(cudaMemcpyAsync(t2, tau2, (size_t)slots * sizeof(double2), cudaMemcpyHostToDevice, c.xfer),
                       "H2D tau2"));
-      EIG_TRY(c.check(cudaMemcpy2DAsync(l, n * sizeof(double2), L, ldl * sizeof(double2), n * sizeof(double2), n,
-                                        cudaMemcpyHostToDevice, c.stream), "H2D L"));
       if (m > 0)
         EIG_TRY(c.check(cudaMemcpy2DAsync(z, n * sizeof(double), Z, ldz * sizeof(double), n * sizeof(double), m,
-                                          cudaMemcpyHostToDevice, c.stream), "H2D Z"));
+                                          cudaMemcpyHostToDevice, c.xfer), "H2D Z"));
+      for (int64_t j0 = 0; j0 < n; j0 += 256) {   // lower triangle of L only
+        const int64_t w = std::min<int64_t>(256, n - j0);
+        EIG_TRY(c.check(cudaMemcpy2DAsync(l + j0 + j0 * n, n * sizeof(double2), (const double2 *)L + j0 + j0 * ldl,
+                                          ldl * sizeof(double2), (n - j0) * sizeof(double2), w,
+                                          cudaMemcpyHostToDevice, c.xfer), "H2D L"));
+      }
+      EIG_TRY(c.check(cudaEventRecord(c.ev_xfer, c.xfer), "xfer join"));
     }
     dV2 = v2; dtau2 = t2; dL = l; dZ = z;
     dlda = n; dldl = n; dldz = n; dlde = n;
   }
   if (!(flags & EIG_SKIP_HE2HB)) EIG_TRY(he2hb_run(c, n, dA, dlda, dtau1, dT1));
+  if (host && !(flags & EIG_SKIP_BT)) EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_xfer, 0), "xfer join wait"));
   if (!(flags & EIG_SKIP_BT) && m > 0) {
     EIG_TRY(complexify(c, n, m, dZ, dldz, dE, dlde));                      // a6: complexify
     EIG_TRY(apply_q2_run(c, n, dV2, dtau2, dE, dlde, m));                   // a6: Q2
     EIG_TRY(apply_q1_run(c, n, dA, dlda, dT1, dE, dlde, m));                // a7: Q1
-    EIG_TRY(trsm_lh_run(c, n, dL, dldl, dE, dlde, m));                      // a8: L^-H
+    // a8: L^-H; with host buffers each final row block of E is copied back
+    // on the transfer stream while the blocks above it are solved
+    EIG_TRY(trsm_lh_run(c, n, dL, dldl, dE, dlde, m, (host && E) ? (double2 *)E : nullptr, lde));
   }
   if (host) {
-    if (!(flags & EIG_SKIP_BT) && m > 0 && E)
-      EIG_TRY(c.check(cudaMemcpy2DAsync(E, lde * sizeof(double2), dE, n * sizeof(double2), n * sizeof(double2), m,
-                                        cudaMemcpyDeviceToHost, c.stream), "D2H E"));
     EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync"));
+    EIG_TRY(c.check(cudaStreamSynchronize(c.xfer), "sync xfer"));
   }
   return 0;
 }

@@ -42,6 +42,8 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // high-priority stream for the he2hb panels (look-ahead)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t xfer = nullptr;        // host <-> device copies overlapped with compute (EIG_HOST_BUFFERS)
+  cudaEvent_t ev_xfer = nullptr, ev_blk = nullptr;
   int nb = 64;
   int q2g = 32;
   int num_sms = 148;
