@@ -17,6 +17,7 @@
 // Because v = (a_j - beta e_j)/(alpha - beta), v^H P[:,l] follows from the raw
 // dots a_j^H P[:,l] without a second reduction.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -31,7 +32,7 @@ struct PanelArgs {
   double2 *P;
   int64_t lda;
   int64_t pn;
-  int nb, nref, R, G;
+  int nb, nref, R, R0, G;   // CTA 0 owns R0 = R - nb rows, the others R (CTA 0 keeps T in the rest)
   double2 *tau, *T, *vout, *vout2;
   int64_t ldv;
   double2 *rec;                  // [2][G][recw]: s_l (l != j), sumsq at l = j, then row j
@@ -68,15 +69,17 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
   double2 *sY = sW + nb;            // [nb]   y_i (T column)
   double2 *sPart = sY + nb;         // [4][64]
   double2 *sP = sPart + 4 * 64;     // [nb][R], column l at sP + l*R
-  double2 *gT = a.T;                // T is built in place in global memory by CTA 0 (off the critical path)
+  // CTA 0: T (nb x nb, column stride R) in the unused tail rows R0..R-1 of sP
+  double2 *sT = sP + a.R0;
   __shared__ double2 s_tau, s_scale;
   __shared__ double s_beta;
 
   const int tid = threadIdx.x;
   const int g = blockIdx.x;
-  const int64_t row0 = (int64_t)g * R;
+  const int64_t row0 = g == 0 ? 0 : (int64_t)a.R0 + (int64_t)(g - 1) * R;
   const int64_t left = a.pn - row0;
-  const int rows = left <= 0 ? 0 : (left < R ? (int)left : R);
+  const int cap = g == 0 ? a.R0 : R;
+  const int rows = left <= 0 ? 0 : (left < cap ? (int)left : cap);
   const int cl = tid & 63, rq = tid >> 6;          // column / row-quarter of this thread
   const int R4 = (rows + 3) >> 2;
   const int rlo = min(rows, rq * R4), rhi = min(rows, (rq + 1) * R4);
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
   for (int l = 0; l < nb; l++)
     for (int r = tid; r < R; r += PT) sP[l * R + r] = (r < rows) ? a.P[(row0 + r) + (int64_t)l * a.lda] : czero();
   if (g == 0)
-    for (int e = tid; e < nb * nb; e += PT) gT[e] = czero();
+    for (int e = tid; e < nb * nb; e += PT) sT[(e % nb) + (e / nb) * R] = czero();
   __syncthreads();
 
   const bool prof = a.prof != nullptr && g == 0 && tid == 0;
@@ -147,11 +150,12 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
     mark(0);
     const double2 *recs = a.rec + (int64_t)(j & 1) * G * recw;
     {
+      // s_l for l >= j (every CTA: norm, w_l); s_i for i < j only feed T (CTA 0)
       double2 acc = czero();
-      if (cl < nb)
+      if (cl < nb && (cl >= j || g == 0))
         for (int q = rq; q < G; q += 4) acc = cadd(acc, __ldcg(&recs[(int64_t)q * recw + cl]));
       sPart[rq * 64 + cl] = acc;
-      const int owner = j / R;
+      const int owner = j < a.R0 ? 0 : 1 + (j - a.R0) / R;
       if (tid < nb) sRow[tid] = __ldcg(&recs[(int64_t)owner * recw + nb + tid]);
     }
     __syncthreads();
@@ -232,13 +236,18 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
       }
     }
     if (g == 0) {
-      // T column j: T[0:j, j] = -tau_j T[0:j, 0:j] y
-      if (tid < j) {
-        double2 acc = czero();
-        for (int l = tid; l < j; l++) acc = cadd(acc, cmul(gT[tid + l * nb], sY[l]));
-        gT[tid + j * nb] = make_double2(-(tau.x * acc.x - tau.y * acc.y), -(tau.x * acc.y + tau.y * acc.x));
-      }
-      if (tid == 0) gT[j + j * nb] = tau;
+      // T column j: T[0:j, j] = -tau_j T[0:j, 0:j] y   (4 threads per row, shared memory)
+      const int i = tid >> 2, part = tid & 3;
+      double2 acc = czero();
+      if (i < j)
+        for (int l = i + part; l < j; l += 4) acc = cadd(acc, cmul(sT[i + l * R], sY[l]));
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+      if (i < j && part == 0)
+        sT[i + j * R] = make_double2(-(tau.x * acc.x - tau.y * acc.y), -(tau.x * acc.y + tau.y * acc.x));
+      if (tid == 0) sT[j + j * R] = tau;
     }
     __syncthreads();
     mark(5);
@@ -254,8 +263,10 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
       a.vout[grow + (int64_t)l * a.ldv] = v;
       if (a.vout2) a.vout2[grow + (int64_t)l * a.ldv] = v;
     }
-  if (g == 0)
+  if (g == 0) {
     for (int l = tid; l < nb; l += PT) a.tau[l] = (l < a.nref) ? sTau[l] : czero();
+    for (int e = tid; e < nb * nb; e += PT) a.T[e] = sT[(e % nb) + (e / nb) * R];
+  }
   if (prof)
     for (int k = 0; k < 6; k++) atomicAdd(&a.prof[8 + k], (unsigned long long)tacc[k]);
 }
@@ -285,11 +296,23 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   if (pn <= 0) return 0;
   if (nb > 64) return EIG_ERR_NOTIMPL;
   const int nref = (int)std::min<int64_t>(pn, nb);
-  int G = (int)std::min<int64_t>(ctx.num_sms, (pn + nb - 1) / nb);
+  // CTAs: one per nb rows, capped at 32 (fewer records to exchange per
+  // column, and the SMs left free run the concurrent trailing update), but at
+  // least as many as hold the panel rows in shared memory; EIG_PANEL_CTAS
+  // replaces the cap (tuning; he2hb n = 10^4: cap 8 / 16 / 24 / 32 / 48 / 148
+  // -> 283 / 277 / 273 / 269 / 273 / 281 ms)
+  static const int gmax_env = [] {
+    const char *e = getenv("EIG_PANEL_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  const int gmax = gmax_env > 0 ? std::min(gmax_env, ctx.num_sms) : std::min(32, ctx.num_sms);
+  int G = (int)std::min<int64_t>(gmax, (pn + nb - 1) / nb);
   G = std::max(G, 1);
-  int R = (int)((pn + G - 1) / G);
+  const int rmax = (int)((220 * 1024 / sizeof(double2) - 5 * nb - 4 * 64) / nb);   // rows that fit on chip
+  G = std::max<int64_t>(G, (pn + nb + rmax - 1) / rmax);
+  int R = (int)((pn + nb + G - 1) / G);   // CTA 0 holds R - nb rows
   R = std::max(R, nb);
-  G = (int)((pn + R - 1) / R);
+  G = (int)((pn + nb + R - 1) / R);
   const int recw = 2 * nb;
   const size_t smem = ((size_t)5 * nb + 4 * 64 + (size_t)nb * R) * sizeof(double2);
   if (smem > 220 * 1024) return EIG_ERR_NOTIMPL;  // panel too tall for on-chip residency (n > ~20000 at nb=64)
@@ -300,6 +323,7 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   a.nb = nb;
   a.nref = nref;
   a.R = R;
+  a.R0 = R - nb;
   a.G = G;
   a.tau = tau;
   a.T = T;
