@@ -26,7 +26,8 @@
 namespace eig {
 namespace {
 
-constexpr int PT = 256;
+constexpr int PT = 512;
+constexpr int NQ = PT / 64;   // row parts (64 columns x NQ parts of the rows)
 
 struct PanelArgs {
   double2 *P;
@@ -58,7 +59,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // so the trailing-column update and the T column
 //   T[0:j, j] = -tau_j T[0:j, 0:j] y   (zlarft, forward/columnwise)
 // need no second reduction.
-__global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
+__global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double2 sm[];
   const int nb = a.nb, R = a.R, G = a.G;
   const int recw = 2 * nb;
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
   double2 *sW = sS + nb;            // [nb]   w_l / y_i
   double2 *sY = sW + nb;            // [nb]   y_i (T column)
   double2 *sPart = sY + nb;         // [4][64]
-  double2 *sP = sPart + 4 * 64;     // [nb][R], column l at sP + l*R
+  double2 *sP = sPart + NQ * 64;    // [nb][R], column l at sP + l*R
   // CTA 0: T (nb x nb, column stride R) in the unused tail rows R0..R-1 of sP
   double2 *sT = sP + a.R0;
   __shared__ double2 s_tau, s_scale;
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
   const int cap = g == 0 ? a.R0 : R;
   const int rows = left <= 0 ? 0 : (left < cap ? (int)left : cap);
   const int cl = tid & 63, rq = tid >> 6;          // column / row-quarter of this thread
-  const int R4 = (rows + 3) >> 2;
+  const int R4 = (rows + NQ - 1) / NQ;
   const int rlo = min(rows, rq * R4), rhi = min(rows, (rq + 1) * R4);
 
   for (int l = 0; l < nb; l++)
@@ -119,10 +120,14 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
     __syncthreads();
     double2 *out = a.rec + ((int64_t)(jn & 1) * G + g) * recw;
     if (tid < nb) {
-      double2 t = cadd(cadd(sPart[tid], sPart[64 + tid]), cadd(sPart[128 + tid], sPart[192 + tid]));
+      double2 t = sPart[tid];
+#pragma unroll
+      for (int q = 1; q < NQ; q++) t = cadd(t, sPart[q * 64 + tid]);
       if (corr && tid > jn) {
         const int jp = jn - 1;
-        const double2 c1 = cadd(cadd(sPart[jp], sPart[64 + jp]), cadd(sPart[128 + jp], sPart[192 + jp]));
+        double2 c1 = sPart[jp];
+#pragma unroll
+        for (int q = 1; q < NQ; q++) c1 = cadd(c1, sPart[q * 64 + jp]);
         t = csub(t, cmul(ctau, cmul(sW[tid], c1)));
       }
       __stcg(&out[tid], t);
@@ -153,13 +158,18 @@ __global__ void __launch_bounds__(PT, 2) panel_qr_kernel(PanelArgs a) {
       // s_l for l >= j (every CTA: norm, w_l); s_i for i < j only feed T (CTA 0)
       double2 acc = czero();
       if (cl < nb && (cl >= j || g == 0))
-        for (int q = rq; q < G; q += 4) acc = cadd(acc, __ldcg(&recs[(int64_t)q * recw + cl]));
+        for (int q = rq; q < G; q += NQ) acc = cadd(acc, __ldcg(&recs[(int64_t)q * recw + cl]));
       sPart[rq * 64 + cl] = acc;
       const int owner = j < a.R0 ? 0 : 1 + (j - a.R0) / R;
       if (tid < nb) sRow[tid] = __ldcg(&recs[(int64_t)owner * recw + nb + tid]);
     }
     __syncthreads();
-    if (tid < nb) sS[tid] = cadd(cadd(sPart[tid], sPart[64 + tid]), cadd(sPart[128 + tid], sPart[192 + tid]));
+    if (tid < nb) {
+      double2 t = sPart[tid];
+#pragma unroll
+      for (int q = 1; q < NQ; q++) t = cadd(t, sPart[q * 64 + tid]);
+      sS[tid] = t;
+    }
     __syncthreads();
     mark(1);
     if (tid == 0) {
@@ -308,13 +318,13 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   const int gmax = gmax_env > 0 ? std::min(gmax_env, ctx.num_sms) : std::min(32, ctx.num_sms);
   int G = (int)std::min<int64_t>(gmax, (pn + nb - 1) / nb);
   G = std::max(G, 1);
-  const int rmax = (int)((220 * 1024 / sizeof(double2) - 5 * nb - 4 * 64) / nb);   // rows that fit on chip
+  const int rmax = (int)((220 * 1024 / sizeof(double2) - 5 * nb - NQ * 64) / nb);   // rows that fit on chip
   G = std::max<int64_t>(G, (pn + nb + rmax - 1) / rmax);
   int R = (int)((pn + nb + G - 1) / G);   // CTA 0 holds R - nb rows
   R = std::max(R, nb);
   G = (int)((pn + nb + R - 1) / R);
   const int recw = 2 * nb;
-  const size_t smem = ((size_t)5 * nb + 4 * 64 + (size_t)nb * R) * sizeof(double2);
+  const size_t smem = ((size_t)5 * nb + NQ * 64 + (size_t)nb * R) * sizeof(double2);
   if (smem > 220 * 1024) return EIG_ERR_NOTIMPL;  // panel too tall for on-chip residency (n > ~20000 at nb=64)
   PanelArgs a;
   a.P = P;
