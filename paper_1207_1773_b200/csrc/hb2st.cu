@@ -57,14 +57,14 @@ __device__ __forceinline__ void st_release_i32(int *p, int v) {
 constexpr int LDD = 65;
 __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
   extern __shared__ __align__(16) double2 hsm[];
-  double2 *sD = hsm;                  // [64][LDD] diagonal block (full Hermitian)
-  double2 *sA = sD + 64 * LDD;        // [63 cols][64 rows] previous bulge (column-major)
-  double2 *sC = sA + 64 * 64;         // [64 cols][64 rows] rows below R (column-major, row index fast)
-  double2 *sx = sC + 64 * 64;         // [64]
+  double2 *sD = hsm;                  // [64][LDD] diagonal block (lower)
+  double2 *sP0 = sD + 64 * LDD;       // two [64 cols][64 rows] bulge buffers (column-major, row index fast)
+  double2 *sxg = sP0 + 2 * 64 * 64;   // [64] x of the first task of a sweep
   __shared__ double2 sv[64];          // reflector
   __shared__ double2 sp[64];          // p, then w
   __shared__ double2 sg[64];          // g = tau (C v)
-  __shared__ double2 spart[6][64];    // half dot products
+  __shared__ double2 sf[64];          // f = conj(tau) v^H Ablk
+  __shared__ double2 spart[8][64];    // partial dot products
   __shared__ double2 s_tau, s_beta;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n;
@@ -80,9 +80,29 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       tm = now;
     }
   };
+  // sweep i-1 must have finished step j+2 before task (i, j) touches D_j / Cblk_j
+  auto wait_prev = [&](int64_t i, int64_t j) {
+    if (i > 0 && tid == 0) {
+      const int64_t prev = i - 1;
+      const int64_t jprev_max = (n - 2 - prev) / nb;
+      const int need = (int)imin64(j + 3, jprev_max + 1);
+      while (ld_acquire_i32(a.progress + prev) < need) {
+      }
+    }
+    __syncthreads();
+  };
 
+  // Task (i, j+1) starts from task (i, j)'s updated Cblk: its target column x
+  // is Cblk's column 0 and its previous bulge Ablk is Cblk's columns 1.. (same
+  // rows).  So Cblk stays in shared memory (buffers alternate), is never
+  // stored by task j (task j+1 stores the final values of that region), and
+  // x / Ablk need no load; the reflector and the (a) update run before the
+  // wait on sweep i-1, which only D_j and Cblk_j depend on.
   for (int64_t i = blockIdx.x; i + 1 < n; i += gridDim.x) {
+    int cur = 0;
+    int64_t off_next = a.off[0];   // V2 slot offsets, read one task ahead
     for (int64_t j = 0;; j++) {
+      const int64_t off_j = off_next;
       const int64_t c = (j == 0) ? i : i + 1 + (j - 1) * nb;
       const int64_t r0 = i + 1 + j * nb;
       if (r0 > n - 1) break;
@@ -91,35 +111,21 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       const int na = (int)(r0 - c - 1);                       // previous-bulge columns
       const int64_t kend = imin64(r1 + nb, n - 1);
       const int nc = (int)(kend - r1);                        // rows below R
+      double2 *sC = sP0 + cur * 4096;                         // this task's Cblk
+      const double2 *sPrev = sP0 + (cur ^ 1) * 4096;          // previous task's Cblk = [x | Ablk]
+      const double2 *sx = (j == 0) ? sxg : sPrev;
+      const double2 *sA = sPrev + 64;                         // Ablk column k at sA + k*64
+      if (r1 < n - 1) off_next = a.off[j + 1];
       mark(-1);
-      if (i > 0 && tid == 0) {   // sweep i-1 must have finished step j+2
-        const int64_t prev = i - 1;
-        const int64_t jprev_max = (n - 2 - prev) / nb;
-        const int need = (int)imin64(j + 3, jprev_max + 1);
-        while (ld_acquire_i32(a.progress + prev) < need) {
-        }
+      if (j == 0) {
+        wait_prev(i, j);
+        for (int t = tid; t < len; t += HT) cp_async16(&sxg[t], M(r0 + t, c), true);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
       }
-      __syncthreads();
       mark(0);
-      // ---- 1. all loads at once
-      for (int t = tid; t < len; t += HT) cp_async16(&sx[t], M(r0 + t, c), true);
-      for (int e = tid; e < na * 64; e += HT) {
-        const int t = e & 63, k = e >> 6;
-        if (t < len) cp_async16(&sA[t + k * 64], M(r0 + t, c + 1 + k), true);
-      }
-      for (int e = tid; e < 64 * 64; e += HT) {
-        const int rr = e & 63, cc = e >> 6;
-        if (rr < len && cc <= rr) cp_async16(&sD[rr + cc * LDD], M(r0 + rr, r0 + cc), true);
-      }
-      for (int e = tid; e < nc * 64; e += HT) {
-        const int rr = e % nc, t = e / nc;
-        if (t < len) cp_async16(&sC[rr + t * 64], M(r1 + 1 + rr, r0 + t), true);
-      }
-      cp_async_commit();
-      cp_async_wait<0>();
-      __syncthreads();
-      mark(1);
-      // ---- 2. reflector
+      // ---- reflector (x in shared memory)
       if (warp == 0) {
         const double2 x0 = lane < len ? sx[lane] : czero();
         const double2 x1 = lane + 32 < len ? sx[lane + 32] : czero();
@@ -148,24 +154,55 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       }
       __syncthreads();
       const double2 tau = s_tau, ctau = cconj(tau);
+      const bool upd = tau.x != 0.0 || tau.y != 0.0;
       {
-        const int64_t slot = a.off[j] + i;
+        const int64_t slot = off_j + i;
         for (int t = tid; t < nb; t += HT) a.V2[slot * nb + t] = (t < len) ? sv[t] : czero();
         if (tid == 0) a.tau2[slot] = tau;
         for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta : czero();
       }
-      mark(2);
-      if (tau.x != 0.0 || tau.y != 0.0) {
-        // U1: all dot products in parallel, each split in two halves over t
-        //   f_k = conj(tau) v^H Ablk[:, k];  p_r = tau (D v)_r;  g_rr = tau (Cblk v)_rr
-        if (tid < 384) {
-          const int g = tid >> 6, q = tid & 63, h = g & 1;
-          const int t0 = h * 32, t1 = imin64(t0 + 32, len);
+      // ---- (a) on the previous bulge (shared memory only): f, then store
+      if (na > 0) {
+        if (upd && tid < 256) {   // four 16-row parts per column
+          const int q = tid & 63, h = tid >> 6;
+          const int t0 = h * 16, t1 = imin64(t0 + 16, len);
           double2 acc = czero();
-          if (g < 2) {
-            if (q < na)
-              for (int t = t0; t < t1; t++) acc = cadd(acc, cmulc(sv[t], sA[t + q * 64]));
-          } else if (g < 4) {
+          if (q < na)
+            for (int t = t0; t < t1; t++) acc = cadd(acc, cmulc(sv[t], sA[t + q * 64]));
+          spart[h][q] = acc;
+        }
+        __syncthreads();
+        if (upd && tid < na)
+          sf[tid] = cmul(ctau, cadd(cadd(spart[0][tid], spart[1][tid]), cadd(spart[2][tid], spart[3][tid])));
+        __syncthreads();
+        for (int e = tid; e < na * 64; e += HT) {          // y_k - v f_k  (stored even if tau = 0:
+          const int t = e & 63, k = e >> 6;               //  the previous task left this region in smem)
+          if (t < len) *M(r0 + t, c + 1 + k) = upd ? csub(sA[t + k * 64], cmul(sv[t], sf[k])) : sA[t + k * 64];
+        }
+      }
+      mark(2);
+      // ---- D_j and Cblk_j, after sweep i-1 is done with them
+      if (j > 0) wait_prev(i, j);
+      mark(1);
+      for (int e = tid; e < 64 * 64; e += HT) {
+        const int rr = e & 63, cc = e >> 6;
+        if (rr < len && cc <= rr) cp_async16(&sD[rr + cc * LDD], M(r0 + rr, r0 + cc), true);
+      }
+      for (int e = tid; e < 64 * 64; e += HT) {
+        const int rr = e & 63, t = e >> 6;
+        if (rr < nc && t < len) cp_async16(&sC[rr + t * 64], M(r1 + 1 + rr, r0 + t), true);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      mark(4);
+      if (upd) {
+        //   p_r = tau (D v)_r;  g_rr = tau (Cblk v)_rr   (each split in two halves)
+        {   // 8 groups of 64 threads: D (groups 0-3) and Cblk (4-7), 16 terms each
+          const int g = tid >> 6, q = tid & 63, h = g & 3;
+          const int t0 = h * 16, t1 = imin64(t0 + 16, len);
+          double2 acc = czero();
+          if (g < 4) {
             if (q < len)
               for (int cc = t0; cc < t1; cc++) {
                 double2 d;
@@ -182,16 +219,12 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
         }
         __syncthreads();
         if (tid < 64) {
-          if (tid < na) sx[tid] = cmul(ctau, cadd(spart[0][tid], spart[1][tid]));
+          if (tid < len) sp[tid] = cmul(tau, cadd(cadd(spart[0][tid], spart[1][tid]), cadd(spart[2][tid], spart[3][tid])));
         } else if (tid < 128) {
-          const int r = tid - 64;
-          if (r < len) sp[r] = cmul(tau, cadd(spart[2][r], spart[3][r]));
-        } else if (tid < 192) {
-          const int rr = tid - 128;
-          if (rr < nc) sg[rr] = cmul(cadd(spart[4][rr], spart[5][rr]), tau);
+          const int rr = tid - 64;
+          if (rr < nc) sg[rr] = cmul(cadd(cadd(spart[4][rr], spart[5][rr]), cadd(spart[6][rr], spart[7][rr])), tau);
         }
         __syncthreads();
-        mark(4);
         if (warp == 0) {   // w = p - 1/2 tau (p^H v) v
           double2 sdot = czero();
           for (int t = lane; t < len; t += 32) sdot = cadd(sdot, cmulc(sp[t], sv[t]));
@@ -200,12 +233,7 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
           for (int t = lane; t < len; t += 32) sp[t] = cadd(sp[t], cmul(al, sv[t]));
         }
         __syncthreads();
-        // U3: element-wise updates, stored straight to global
-        for (int e = tid; e < na * 64; e += HT) {          // (a) y_k - v f_k
-          const int t = e & 63, k = e >> 6;
-          if (t < len) *M(r0 + t, c + 1 + k) = csub(sA[t + k * 64], cmul(sv[t], sx[k]));
-        }
-        for (int e = tid; e < 64 * 64; e += HT) {          // (b) D - v w^H - w v^H  (lower)
+        for (int e = tid; e < 64 * 64; e += HT) {          // (b) D - v w^H - w v^H  (lower), to global
           const int rr = e & 63, cc = e >> 6;
           if (rr < len && cc <= rr) {
             double2 d = sD[rr + cc * LDD];
@@ -214,9 +242,9 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
             *M(r0 + rr, r0 + cc) = d;
           }
         }
-        for (int e = tid; e < nc * 64; e += HT) {          // (c) y - g v^H
-          const int rr = e % nc, t = e / nc;
-          if (t < len) *M(r1 + 1 + rr, r0 + t) = csub(sC[rr + t * 64], cmul(sg[rr], cconj(sv[t])));
+        for (int e = tid; e < 64 * 64; e += HT) {          // (c) y - g v^H, kept in shared memory
+          const int rr = e & 63, t = e >> 6;
+          if (rr < nc && t < len) sC[rr + t * 64] = csub(sC[rr + t * 64], cmul(sg[rr], cconj(sv[t])));
         }
       }
       mark(3);
@@ -224,6 +252,7 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       __syncthreads();
       if (tid == 0) st_release_i32(a.progress + i, (int)(j + 1));
       mark(5);
+      cur ^= 1;
     }
   }
   if (prof)
@@ -280,7 +309,7 @@ int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d,
     const int64_t J = (n - 2) / nb + 1;   // steps of sweep 0
     const int P = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, std::min<int64_t>(n - 1, J / 3 + 2)));
     void *args[] = {&a};
-    const size_t smem = ((size_t)64 * LDD + 64 * 64 + 64 * 64 + 64) * sizeof(double2);
+    const size_t smem = ((size_t)64 * LDD + 2 * 64 * 64 + 64) * sizeof(double2);
     static bool attr = false;
     if (!attr) {
       EIG_TRY(ctx.check(cudaFuncSetAttribute(hb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
