@@ -326,11 +326,26 @@ __global__ void __launch_bounds__(PT) dc_prep_kernel(DcBufs b) {
 // ------------------------------------------------------------------ secular equation
 // f(lambda) = 1 + rho sum_i z_i^2 / (D_i - lambda), increasing between poles;
 // root j is stored as (origin pole, offset tau) for accurate gaps.
+// One warp per root: every lane sums a strided share of the K terms and the
+// shares are combined with a fixed butterfly (deterministic), so the O(K^2)
+// bisection runs on all SMs instead of K threads.
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_allprod(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v *= __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __global__ void dc_secular_kernel(DcBufs b) {
   const Node nd = b.nodes[blockIdx.y];
   const int K = b.cnt[blockIdx.y * 4 + 0];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= K) return;
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= K) return;   // warp-uniform
   const int64_t lo = nd.lo;
   const double *D = b.Dn + lo, *z = b.zn + lo;
   const double rho = b.rho[blockIdx.y];
@@ -338,8 +353,9 @@ __global__ void dc_secular_kernel(DcBufs b) {
   double tl, th;
   if (j < K - 1) {
     const double half = 0.5 * (D[j + 1] - D[j]);
-    double f = 1.0;
-    for (int i = 0; i < K; i++) f += rho * z[i] * z[i] / ((D[i] - D[j]) - half);
+    double f = 0.0;
+    for (int i = lane; i < K; i += 32) f += rho * z[i] * z[i] / ((D[i] - D[j]) - half);
+    f = 1.0 + warp_allsum(f);
     if (f >= 0.0) {
       og = j;
       tl = 0.0;
@@ -350,40 +366,49 @@ __global__ void dc_secular_kernel(DcBufs b) {
       th = 0.0;
     }
   } else {
-    double s = 0.0;
-    for (int i = 0; i < K; i++) s += z[i] * z[i];
+    double sq = 0.0;
+    for (int i = lane; i < K; i += 32) sq += z[i] * z[i];
+    sq = warp_allsum(sq);
     og = K - 1;
     tl = 0.0;
-    th = rho * s;
+    th = rho * sq;
   }
   const double Do = D[og];
   for (int it = 0; it < 200; it++) {
     const double tm = 0.5 * (tl + th);
     if (tm <= tl || tm >= th) break;
-    double f = 1.0;
-    for (int i = 0; i < K; i++) f += rho * z[i] * z[i] / ((D[i] - Do) - tm);
+    double f = 0.0;
+    for (int i = lane; i < K; i += 32) f += rho * z[i] * z[i] / ((D[i] - Do) - tm);
+    f = 1.0 + warp_allsum(f);
     if (f > 0.0) th = tm; else tl = tm;
   }
-  b.org[lo + j] = og;
-  b.tau[lo + j] = 0.5 * (tl + th);
+  if (lane == 0) {
+    b.org[lo + j] = og;
+    b.tau[lo + j] = 0.5 * (tl + th);
+  }
 }
 
 // Gu-Eisenstat: zh_i^2 = ((lambda_i - D_i)/rho) prod_{j != i} (lambda_j - D_i)/(D_j - D_i)
+// (one warp per i, strided partial products combined with a fixed butterfly)
 __global__ void dc_zhat_kernel(DcBufs b) {
   const Node nd = b.nodes[blockIdx.y];
   const int K = b.cnt[blockIdx.y * 4 + 0];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= K) return;
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= K) return;   // warp-uniform
   const int64_t lo = nd.lo;
   const double *D = b.Dn + lo;
   const double rho = b.rho[blockIdx.y];
   const double Di = D[i];
   auto lam_minus_Di = [&](int j) { return (D[b.org[lo + j]] - Di) + b.tau[lo + j]; };
-  double p = lam_minus_Di(i) / rho;
-  for (int j = 0; j < K; j++)
+  double p = 1.0;
+  for (int j = lane; j < K; j += 32)
     if (j != i) p *= lam_minus_Di(j) / (D[j] - Di);
-  const double zi = b.zn[lo + i];
-  b.zh[lo + i] = copysign(sqrt(fabs(p)), zi);
+  p = warp_allprod(p) * (lam_minus_Di(i) / rho);
+  if (lane == 0) {
+    const double zi = b.zn[lo + i];
+    b.zh[lo + i] = copysign(sqrt(fabs(p)), zi);
+  }
 }
 
 // Final order of the node's k eigenpairs: roots (ascending) merged with the
@@ -651,9 +676,9 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
     int Kmax = 0;
     for (int i = 0; i < nn_; i++) Kmax = std::max(Kmax, cnt[4 * i]);
     if (Kmax > 0) {
-      dc_secular_kernel<<<dim3((Kmax + 127) / 128, nn_), 128, 0, c.stream>>>(b);
+      dc_secular_kernel<<<dim3((Kmax + 7) / 8, nn_), 256, 0, c.stream>>>(b);   // 8 roots (warps) per CTA
       EIG_TRY(c.launched("dc_secular_kernel"));
-      dc_zhat_kernel<<<dim3((Kmax + 127) / 128, nn_), 128, 0, c.stream>>>(b);
+      dc_zhat_kernel<<<dim3((Kmax + 7) / 8, nn_), 256, 0, c.stream>>>(b);
       EIG_TRY(c.launched("dc_zhat_kernel"));
     }
     dc_order_kernel<<<nn_, PT, 0, c.stream>>>(b, top ? 0 : -1);

@@ -4,6 +4,8 @@ standalone and under ncu.  Modes:
   gemm  : zgemm engine on square / he2hb-shaped products
   q2    : apply_q2 at (n, m) with synthetic reflectors
   he2hb : he2hb alone at n
+  hb2st : bulge chasing alone at n
+  stedc : tridiagonal divide and conquer at n (random d, e)
 """
 import argparse
 import os
@@ -94,6 +96,12 @@ def main():
             pr = s.q2_profile()[16:22]
             tot = sum(pr)
             print("  hb2st CTA0 (wait, load, refl, update, -, flag):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
+    elif a.mode == "stedc":
+        rng = np.random.default_rng(0)
+        d = torch.from_numpy(rng.standard_normal(n)).to(dev)
+        e = torch.from_numpy(rng.standard_normal(n - 1)).to(dev)
+        ms = timeit(lambda: s.stedc(d, e), a.reps)
+        print(f"stedc n={n}: {ms:.3f} ms")
     elif a.mode == "he2hb":
         A0 = colmajor(synth.rand_hermitian(n, 0), dev)
         A = A0.clone()
