@@ -20,7 +20,8 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
 constexpr int LDA_S = BM + 4;  // sA[k][m]: k-major, m contiguous (+4 complex pad -> conflict free)
 constexpr int LDB_S = BK + 2;  // sB[n][k]: n-major, k contiguous (+2 complex pad)
-constexpr int SA_ELEMS = BK * LDA_S;
+constexpr int LDAK = BK + 2;   // op(A) = A^H: sA[m][k], k contiguous like sB (conflict-free cp.async and fragments)
+constexpr int SA_ELEMS = (BK * LDA_S > BM * LDAK) ? BK * LDA_S : BM * LDAK;
 constexpr int SB_ELEMS = BN * LDB_S;
 constexpr int STAGE_ELEMS = SA_ELEMS + SB_ELEMS;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double2);
@@ -91,7 +92,10 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
         src = p.A + gk + gm * p.lda;
       else
         src = (gm >= gk) ? p.A + gm + gk * p.lda : p.A + gk + gm * p.lda;
-      cp_async16(&sA[k * LDA_S + m], valid ? src : p.A, valid);
+      if (!HERM && OPA == OP_C)
+        cp_async16(&sA[m * LDAK + k], valid ? src : p.A, valid);
+      else
+        cp_async16(&sA[k * LDA_S + m], valid ? src : p.A, valid);
     }
 #pragma unroll
     for (int r = 0; r < (BN * BK) / THREADS; r++) {
@@ -186,7 +190,8 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
 #pragma unroll
       for (int i = 0; i < 4; i++) {
         const int mm = wm * 16 + i * 4 + (lane >> 3);
-        af[i] = xsign(a[(kk * LDA_S + mm) * 2 + le.a_comp], anm);
+        af[i] = xsign((!HERM && OPA == OP_C) ? a[(mm * LDAK + kk) * 2 + le.a_comp] : a[(kk * LDA_S + mm) * 2 + le.a_comp],
+                      anm);
       }
 #pragma unroll
       for (int j = 0; j < 4; j++) {
