@@ -22,7 +22,8 @@ constexpr int LDA_S = BM + 4;  // sA[k][m]: k-major, m contiguous (+4 complex pa
 constexpr int LDB_S = BK + 2;  // sB[n][k]: n-major, k contiguous (+2 complex pad)
 constexpr int LDAK = BK + 2;   // op(A) = A^H: sA[m][k], k contiguous like sB (conflict-free cp.async and fragments)
 constexpr int SA_ELEMS = (BK * LDA_S > BM * LDAK) ? BK * LDA_S : BM * LDAK;
-constexpr int SB_ELEMS = BN * LDB_S;
+constexpr int LDBN = BN + 4;   // op(B) = B^H: sB[k][n], n contiguous
+constexpr int SB_ELEMS = (BN * LDB_S > BK * LDBN) ? BN * LDB_S : BK * LDBN;
 constexpr int STAGE_ELEMS = SA_ELEMS + SB_ELEMS;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double2);
 
@@ -112,7 +113,10 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
       const int64_t gn = n0 + n, gk = k0 + k;
       const bool valid = gn < p.N && gk < kend;
       src = (OPB == OP_N) ? p.B + gk + gn * p.ldb : p.B + gn + gk * p.ldb;
-      cp_async16(&sB[n * LDB_S + k], valid ? src : p.B, valid);
+      if (OPB == OP_C)
+        cp_async16(&sB[k * LDBN + n], valid ? src : p.B, valid);
+      else
+        cp_async16(&sB[n * LDB_S + k], valid ? src : p.B, valid);
     }
   };
 
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const int nn = wn * 32 + j * 8 + (lane >> 2);
-        bf[j] = xsign(b[(nn * LDB_S + kk) * 2 + le.b_comp], bnm);
+        bf[j] = xsign(OPB == OP_C ? b[(kk * LDBN + nn) * 2 + le.b_comp] : b[(nn * LDB_S + kk) * 2 + le.b_comp], bnm);
       }
 #pragma unroll
       for (int i = 0; i < 4; i++)
