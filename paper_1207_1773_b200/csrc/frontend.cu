@@ -115,6 +115,10 @@ __global__ void conj_transpose_kernel(int64_t n, const double2 *X, int64_t ldx, 
 
 }  // namespace
 
+// Look-ahead (like he2hb's): the trailing update of step k is split
+// into (i) the next block column and (ii) the rest; the next diagonal block
+// and its panel L21 are factored on the high-priority side stream right
+// after (i), concurrently with (ii).
 int potrf_lower(Ctx &c, int64_t n, double2 *B, int64_t ldb, int64_t *d_info) {
   double2 *Linv = (double2 *)c.ws(WS_FRONT, (size_t)FB * FB * sizeof(double2));
   if (!Linv) return EIG_ERR_NOMEM;
@@ -125,21 +129,54 @@ int potrf_lower(Ctx &c, int64_t n, double2 *B, int64_t ldb, int64_t *d_info) {
                     "potrf attr"));
     attr = true;
   }
-  for (int64_t k = 0; k < n; k += FB) {
+  // diagonal block at k (size b) and, below it, L21 = A21 L11^-H (s rows), on `st`
+  auto factor_block = [&](int64_t k, cudaStream_t st) -> int {
     const int b = (int)std::min<int64_t>(FB, n - k);
     double2 *A11 = B + k + k * ldb;
-    potrf_diag_kernel<<<1, 256, smem, c.stream>>>(A11, ldb, b, Linv, k, n, d_info);
+    potrf_diag_kernel<<<1, 256, smem, st>>>(A11, ldb, b, Linv, k, n, d_info);
     EIG_TRY(c.launched("potrf_diag_kernel"));
     const int64_t s = n - k - b;
-    if (s <= 0) break;
-    Zgemm g;   // L21 = A21 L11^-H   (in place: one 64-col N tile, no split-K)
+    if (s <= 0) return 0;
+    Zgemm g;   // in place: one 64-col N tile, no split-K
     g.opb = OP_C; g.M = s; g.N = b; g.K = b; g.A = A11 + b; g.lda = ldb; g.B = Linv; g.ldb = FB; g.C = A11 + b;
     g.ldc = ldb; g.splitk = 1;
-    EIG_TRY(zgemm(c, g));
-    g = Zgemm();   // A22 -= L21 L21^H (lower)
-    g.opb = OP_C; g.lower_c = 1; g.M = s; g.N = s; g.K = b; g.A = A11 + b; g.lda = ldb; g.B = A11 + b; g.ldb = ldb;
-    g.C = A11 + b + b * ldb; g.ldc = ldb; g.alpha = -1.0; g.beta = 1.0;
-    EIG_TRY(zgemm(c, g));
+    const cudaStream_t keep = c.stream;
+    c.stream = st;
+    const int rc = zgemm(c, g);
+    c.stream = keep;
+    return rc;
+  };
+  EIG_TRY(factor_block(0, c.stream));
+  for (int64_t k = 0; k < n; k += FB) {
+    const int b = (int)std::min<int64_t>(FB, n - k);
+    const int64_t s = n - k - b;
+    if (s <= 0) break;
+    if (k > 0) EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_join, 0), "potrf join"));
+    double2 *A11 = B + k + k * ldb, *L21 = A11 + b, *A22 = A11 + b + b * ldb;
+    const int b2 = (int)std::min<int64_t>(FB, s);
+    Zgemm g;
+    if (s > b2) {
+      // (i) the next block column: A22[:, 0:b2] -= L21 L21[0:b2]^H (rows >= cols)
+      g.opb = OP_C; g.lower_c = 2; g.M = s; g.N = b2; g.K = b; g.A = L21; g.lda = ldb; g.B = L21; g.ldb = ldb;
+      g.C = A22; g.ldc = ldb; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+      EIG_TRY(c.check(cudaEventRecord(c.ev_fork, c.stream), "potrf fork"));
+      EIG_TRY(c.check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "potrf fork wait"));
+      EIG_TRY(factor_block(k + b, c.side));
+      EIG_TRY(c.check(cudaEventRecord(c.ev_join, c.side), "potrf join rec"));
+      // (ii) the rest of the trailing lower triangle
+      g = Zgemm();
+      g.opb = OP_C; g.lower_c = 1; g.M = s - b2; g.N = s - b2; g.K = b; g.A = L21 + b2; g.lda = ldb; g.B = L21 + b2;
+      g.ldb = ldb; g.C = A22 + b2 + b2 * ldb; g.ldc = ldb; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+    } else {
+      // last block: the whole (b2 x b2) update, then its factorisation, in order
+      g.opb = OP_C; g.lower_c = 1; g.M = s; g.N = s; g.K = b; g.A = L21; g.lda = ldb; g.B = L21; g.ldb = ldb;
+      g.C = A22; g.ldc = ldb; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+      EIG_TRY(factor_block(k + b, c.stream));
+      break;
+    }
   }
   return 0;
 }
