@@ -293,17 +293,52 @@ static int trsm_ln_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2
   return 0;
 }
 
-// A' = L^-1 A L^-H = L^-1 (L^-1 A)^H  (A' Hermitian), Algorithm 1 step 2.
+// Z = X L^-H on the lower trapezoid only (rows >= the column block): column
+// block J of Z needs, besides X's own lower part, only Z's columns left of J
+// on the same rows, i.e. lower entries again.  Left-looking over 256-column
+// blocks, 64-column steps with the precomputed inverses of L's 64 x 64
+// diagonal blocks; in place (X's strictly upper blocks are never touched).
+static int trsm_rlh_lower(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2 *X, int64_t ldx) {
+  if (n <= 0) return 0;
+  const int bs = 64, BS = 256;
+  const int64_t nblk = (n + bs - 1) / bs;
+  double2 *Linv = (double2 *)c.ws(WS_LINV, (size_t)nblk * bs * bs * sizeof(double2));
+  if (!Linv) return EIG_ERR_NOMEM;
+  EIG_TRY(trinv_blocks(c, n, bs, L, ldl, Linv));
+  for (int64_t J0 = 0; J0 < n; J0 += BS) {
+    const int64_t J1 = std::min<int64_t>(n, J0 + BS);
+    Zgemm g;
+    if (J0 > 0) {   // X[J0:, J0:J1] -= Z[J0:, 0:J0] L[J0:J1, 0:J0]^H
+      g.opb = OP_C; g.M = n - J0; g.N = J1 - J0; g.K = J0; g.A = X + J0; g.lda = ldx; g.B = L + J0; g.ldb = ldl;
+      g.C = X + J0 + J0 * ldx; g.ldc = ldx; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));
+    }
+    for (int64_t j0 = J0; j0 < J1; j0 += bs) {
+      const int64_t j1 = std::min<int64_t>(J1, j0 + bs), bj = j1 - j0;
+      if (j0 > J0) {   // X[j0:, j0:j1] -= Z[j0:, J0:j0] L[j0:j1, J0:j0]^H
+        g = Zgemm();
+        g.opb = OP_C; g.M = n - j0; g.N = bj; g.K = j0 - J0; g.A = X + j0 + J0 * ldx; g.lda = ldx;
+        g.B = L + j0 + J0 * ldl; g.ldb = ldl; g.C = X + j0 + j0 * ldx; g.ldc = ldx; g.alpha = -1.0; g.beta = 1.0;
+        EIG_TRY(zgemm(c, g));
+      }
+      // in place: Z[j0:, j0:j1] = X[j0:, j0:j1] Linv_jj^H (one 64-col N tile, no split-K)
+      g = Zgemm();
+      g.opb = OP_C; g.M = n - j0; g.N = bj; g.K = bj; g.A = X + j0 + j0 * ldx; g.lda = ldx;
+      g.B = Linv + (j0 / bs) * bs * bs; g.ldb = bs; g.C = X + j0 + j0 * ldx; g.ldc = ldx; g.splitk = 1;
+      EIG_TRY(zgemm(c, g));
+    }
+  }
+  return 0;
+}
+
+// A' = L^-1 A L^-H (A' Hermitian), Algorithm 1 step 2: X = L^-1 A in
+// full, then only the lower trapezoid of X L^-H (a third of the first solve's
+// flops).
 static int hegst_run(Ctx &c, int64_t n, double2 *A, int64_t lda, const double2 *L, int64_t ldl) {
   if (n <= 0) return 0;
-  double2 *Y = (double2 *)c.ws(WS_GST, (size_t)n * n * sizeof(double2));
-  if (!Y) return EIG_ERR_NOMEM;
   EIG_TRY(herm_full(c, n, A, lda));
   EIG_TRY(trsm_ln_run(c, n, L, ldl, A, lda, n));        // X = L^-1 A
-  EIG_TRY(conj_transpose(c, n, A, lda, Y, n));          // Y = X^H
-  EIG_TRY(trsm_ln_run(c, n, L, ldl, Y, n, n));          // A' = L^-1 X^H
-  EIG_TRY(c.check(cudaMemcpy2DAsync(A, lda * sizeof(double2), Y, n * sizeof(double2), n * sizeof(double2), n,
-                                    cudaMemcpyDeviceToDevice, c.stream), "copy A'"));
+  EIG_TRY(trsm_rlh_lower(c, n, L, ldl, A, lda));        // A' = X L^-H (lower)
   return real_diag(c, n, A, lda);
 }
 
