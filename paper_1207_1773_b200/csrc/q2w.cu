@@ -25,6 +25,7 @@
 //    their ring slots are refilled with the next block's rows (cp.async)
 //    while the remaining row groups are computed.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -597,6 +598,224 @@ __global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- split kernel (small m)
+// One fragment shared by NQ warps (NQ = 4: like the quad above; NQ = 8: one
+// M-fragment / three row groups per warp), NG fragments per CTA.  For small m
+// (few fragments per SM) this keeps 8-16 warps per SM busy on the sequential
+// block chain instead of one or two.
+template <int NQ, int I>
+struct SplitSets {
+  static constexpr int NMA = 8 / NQ;   // phase A / B M-fragments per warp
+  __device__ static constexpr int ma(int u) { return NQ == 4 ? 2 * I + u : I; }
+  __device__ static constexpr int mb(int u) { return NQ == 4 ? (u == 0 ? I : 7 - I) : I; }
+  static constexpr int NLO = NQ == 4 ? 4 : 2, NHI = NQ == 4 ? 2 : 1;
+};
+template <int NQ, int I>
+struct SplitLow {
+  __device__ static constexpr int f(int u) {
+    return NQ == 4 ? (u == 0 ? I : u == 1 ? 7 - I : u == 2 ? 8 + I : 15 - I) : (u == 0 ? I : 15 - I);
+  }
+};
+template <int NQ, int I>
+struct SplitHigh {
+  __device__ static constexpr int f(int u) { return NQ == 4 ? (u == 0 ? 16 + I : 23 - I) : 16 + I; }
+};
+
+template <int NQ, int I>
+__device__ __forceinline__ void split_block(const Frag &F, const Lane &L, const double *vc, const double *tt,
+                                            double *yq, double *y2q, int barid) {
+  using S = SplitSets<NQ, I>;
+  constexpr int NMA = S::NMA;
+  const int lane = L.lane;
+  // ---------------- phase A
+  double y[NMA][2];
+#pragma unroll
+  for (int u = 0; u < NMA; u++) y[u][0] = y[u][1] = 0.0;
+  constexpr int KS0 = 2 * S::ma(0), KS1 = imin_c(48, 2 * S::ma(NMA - 1) + 34);
+#pragma unroll
+  for (int ks = KS0; ks < KS1; ks++) {
+    const int ch = ks < 16 ? F.ch0 : (ks < 32 ? F.ch1 : F.ch2);
+    const double e = F.ew[ch + L.offEB + 4 * (ks & 15)];
+#pragma unroll
+    for (int u = 0; u < NMA; u++) {
+      const int mf = S::ma(u);
+      if (ks >= 2 * mf && ks <= 2 * mf + 33) dmma_nv(y[u], xsign(vc[L.offA + 568 * mf + 4 * ks], L.negConj), e);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NMA; u++) {
+    const int refl = 4 * S::ma(u) + (L.rr >> 1);
+#pragma unroll
+    for (int c = 0; c < 2; c++) yq[2 * ((2 * (lane & 3) + c) * LDY + refl) + (L.rr & 1)] = y[u][c];
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(32 * NQ) : "memory");
+  // ---------------- phase B
+  const int offYB = 2 * ((lane >> 2) * LDY + L.kq) + (lane & 1);
+#pragma unroll
+  for (int u = 0; u < NMA; u++) {
+    const int mf = S::mb(u);
+    y[u][0] = y[u][1] = 0.0;
+#pragma unroll
+    for (int ks = 2 * mf; ks < 16; ks++) dmma_nv(y[u], xsign(tt[L.offT + 136 * ks + 8 * mf], L.negT), yq[offYB + 4 * ks]);
+  }
+#pragma unroll
+  for (int u = 0; u < NMA; u++) {
+    const int refl = 4 * S::mb(u) + (L.rr >> 1);
+#pragma unroll
+    for (int c = 0; c < 2; c++) y2q[2 * ((2 * (lane & 3) + c) * LDY + refl) + (L.rr & 1)] = y[u][c];
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(32 * NQ) : "memory");
+  // ---------------- phase C
+  double yb[16];
+#pragma unroll
+  for (int ks = 0; ks < 16; ks++) yb[ks] = y2q[offYB + 4 * ks];
+  if (I == 0 && F.more) {
+    // the padding slot (current row 95) receives the next block's row 31
+    const int c = lane >> 2;
+    const int64_t row = F.rs + W;
+    const bool ok = (lane & 3) == 0 && row < F.n && c < F.ncols;
+    if ((lane & 3) == 0) cp_async16m(&F.Ew[c * LDE + ring_slot(F.base - 1)], ok ? F.E + row + (F.c0 + c) * F.lde : F.E, ok);
+  }
+  phase_c_rows<S::NLO, SplitLow<NQ, I>, true>(F, L, vc, yb);
+  cp_async_commit();
+  phase_c_rows<S::NHI, SplitHigh<NQ, I>, false>(F, L, vc, yb);
+}
+
+template <int NQ>
+__device__ __forceinline__ void split_dispatch(int I, const Frag &F, const Lane &L, const double *vc,
+                                               const double *tt, double *yq, double *y2q, int barid) {
+  switch (I) {
+    case 0: split_block<NQ, 0>(F, L, vc, tt, yq, y2q, barid); break;
+    case 1: split_block<NQ, 1>(F, L, vc, tt, yq, y2q, barid); break;
+    case 2: split_block<NQ, 2>(F, L, vc, tt, yq, y2q, barid); break;
+    case 3: split_block<NQ, 3>(F, L, vc, tt, yq, y2q, barid); break;
+    case 4: if constexpr (NQ > 4) split_block<NQ, 4 % NQ>(F, L, vc, tt, yq, y2q, barid); break;
+    case 5: if constexpr (NQ > 5) split_block<NQ, 5 % NQ>(F, L, vc, tt, yq, y2q, barid); break;
+    case 6: if constexpr (NQ > 6) split_block<NQ, 6 % NQ>(F, L, vc, tt, yq, y2q, barid); break;
+    default: if constexpr (NQ > 7) split_block<NQ, 7 % NQ>(F, L, vc, tt, yq, y2q, barid); break;
+  }
+}
+
+template <int NQ, int NG>
+__global__ void __launch_bounds__(32 * NQ * NG, 1) apply_q2s_kernel(Q2wArgs a) {
+  constexpr int TH = 32 * NQ * NG;
+  static_assert(NG * 8 * LDE + NG * 2 * 8 * LDY <= NFS * 8 * LDE, "split layout must fit the q2w window area");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = w / NQ, I = w % NQ;
+  for (int e = threadIdx.x; e < OFF_T; e += TH) q2w_sm[e] = czero();
+  for (int e = threadIdx.x; e < NFS * 8 * LDE; e += TH) q2w_sm[OFF_E + e] = czero();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; i++) {
+      mbar_init(full_bar(i), 1);
+      *done_cnt(i) = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  BlkIt cur, ahead;
+  it_begin(a, cur);
+  ahead = cur;
+  if (w == 0) {
+    if (ahead.valid) issue_block(a, blk_src(a, ahead), 0, lane);
+    it_next(a, ahead);
+    if (ahead.valid) issue_block(a, blk_src(a, ahead), 1, lane);
+    it_next(a, ahead);
+  } else {
+    it_next(a, ahead);
+    it_next(a, ahead);
+  }
+  const int F = a.nfr_total, Gd = gridDim.x;
+  const int f0 = (int)((int64_t)F * blockIdx.x / Gd), f1 = (int)((int64_t)F * (blockIdx.x + 1) / Gd);
+  const Lane L(lane);
+  double *yq = reinterpret_cast<double *>(q2w_sm + OFF_E + NG * 8 * LDE + g * 2 * 8 * LDY);
+  double *y2q = yq + 2 * 8 * LDY;
+  const int barid = 1 + g;
+  Frag Fr;
+  Fr.Ew = q2w_sm + OFF_E + g * 8 * LDE;
+  Fr.ew = reinterpret_cast<double *>(Fr.Ew);
+  Fr.E = a.E;
+  Fr.lde = a.lde;
+  Fr.lde2 = 2 * a.lde;
+  Fr.n = a.n;
+  auto slab_k = [&](int sl) { return imax_c(0, imin_c(NG, f1 - (f0 + sl * NG))); };
+  BlkSrc asrc;
+  bool active = false;
+  int cur_sl = -1, nact = 0;
+  int64_t cnt = 0;
+  while (cur.valid) {
+    if (cur.sl != cur_sl) {
+      cur_sl = cur.sl;
+      const int k = slab_k(cur_sl);
+      nact = NQ * k;
+      active = g < k;
+      if (active) asrc = blk_src(a, ahead);
+      Fr.c0 = (int64_t)(f0 + cur_sl * NG + g) * 8;
+      Fr.ncols = active ? (int)imin64(8, a.m - Fr.c0) : 0;
+      const int cA = 2 * (lane & 3);
+      Fr.ok0 = cA < Fr.ncols;
+      Fr.ok1 = cA + 1 < Fr.ncols;
+    }
+    const int64_t i0 = cur.gi * G;
+    if (cur.j == 0) {
+      Fr.base = 0;
+      if (active) {
+        const int64_t rs = i0 + 1;
+        for (int e = lane + 32 * I; e < RING * 8; e += 32 * NQ) {
+          const int q = e % RING, c = e / RING;
+          const int64_t row = rs + q;
+          const bool ok = q < W && row < a.n && c < Fr.ncols;
+          cp_async16m(&Fr.Ew[c * LDE + q], ok ? a.E + row + (Fr.c0 + c) * a.lde : a.E, ok);
+        }
+        cp_async_commit();
+      }
+    }
+    const int bi = (int)(cnt & 1);
+    if (!active) {
+      it_next(a, cur);
+      it_next(a, ahead);
+      cnt++;
+      continue;
+    }
+    Fr.rs = i0 + 1 + cur.j * NB;
+    Fr.more = cur.j + 1 < cur.J;
+    const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long *pp = prof ? a.prof + 24 : nullptr;
+    long long tl = prof ? clock64() : 0;
+    mbar_wait(full_bar(bi), (unsigned)((cnt >> 1) & 1));
+    pmark(pp, tl, 0);
+    cp_async_wait<0>();
+    __syncwarp();
+    pmark(pp, tl, 1);
+    asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(32 * NQ) : "memory");   // the group's refills / stores
+    pmark(pp, tl, 2);
+    Fr.ch0 = 2 * 32 * ((0 + Fr.base / 32) % 3);
+    Fr.ch1 = 2 * 32 * ((1 + Fr.base / 32) % 3);
+    Fr.ch2 = 2 * 32 * ((2 + Fr.base / 32) % 3);
+    Fr.gE = reinterpret_cast<double *>(a.E + Fr.rs + (L.rr >> 1) + (Fr.c0 + 2 * (lane & 3)) * a.lde) + (L.rr & 1);
+    split_dispatch<NQ>(I, Fr, L, reinterpret_cast<const double *>(vc_buf(bi)),
+                       reinterpret_cast<const double *>(t_buf(bi)), yq, y2q, barid);
+    pmark(pp, tl, 3);
+    if (!Fr.more) __threadfence_block();
+    Fr.base = Fr.base + NB >= RING ? Fr.base + NB - RING : Fr.base + NB;
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      last = atomicAdd(done_cnt(bi), 1) == nact - 1;
+      if (last) *done_cnt(bi) = 0;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last && ahead.valid && slab_k(ahead.sl) > 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_block(a, asrc, bi, lane);
+    }
+    pmark(pp, tl, 4);
+    it_next(a, cur);
+    it_next(a, ahead);
+    asrc = blk_src(a, ahead);
+    cnt++;
+  }
+}
+
 }  // namespace
 
 size_t q2w_smem_bytes() { return (size_t)OFF_BAR * sizeof(double2) + 32; }
@@ -620,6 +839,22 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
   const int per = (a.nfr_total + grid - 1) / grid;
   a.nslab = (per + NFS - 1) / NFS;
   const size_t smem = q2w_smem_bytes();
+  // few fragments per SM: share each fragment over 8 warps (EIG_Q2W_SPLIT=0 disables)
+  static const int split_env = [] {
+    const char *e = getenv("EIG_Q2W_SPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  if (split_env && per <= 2) {
+    a.nslab = (per + 1) / 2;
+    static bool attr_s = false;
+    if (!attr_s) {
+      EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2s_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem), "q2s attr"));
+      attr_s = true;
+    }
+    apply_q2s_kernel<8, 2><<<grid, 32 * 8 * 2, smem, ctx.stream>>>(a);
+    return ctx.launched("apply_q2s_kernel");
+  }
   static bool attr = false;
   if (!attr) {
     EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),

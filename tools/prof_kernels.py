@@ -86,7 +86,8 @@ def main():
             print("  CTA0 phase cycles (load, A, B, C, commit):", [f"{x / tot * 100:.1f}%" for x in pr], tot)
             pw = s.q2_profile()[24:29]
             tw = max(sum(pw), 1)
-            print("  q2w CTA0 warp0 (wait, A, B, C, release):", [f"{x / tw * 100:.1f}%" for x in pw], tw)
+            print("  q2w CTA0 warp0 (wait, A, B, C, release) / q2s (V/T wait, E wait, group barrier, block, release):",
+                  [f"{x / tw * 100:.1f}%" for x in pw], tw)
     elif a.mode == "hb2st":
         A0 = colmajor(synth.rand_hermitian(n, 0), dev)
         s.he2hb(A0)
