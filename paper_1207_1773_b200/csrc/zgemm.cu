@@ -8,6 +8,7 @@
 // split-K with a deterministic reduction (skinny products, a4/a7/a8).
 // Used by he2hb (Fig. 1 (c) P:L97), Q1 and trsm.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 
 #include "common.cuh"
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
         src = p.A + gk + gm * p.lda;
       else
         src = (gm >= gk) ? p.A + gm + gk * p.lda : p.A + gk + gm * p.lda;
-      if (!HERM && OPA == OP_C)
+      if (mode == 1)   // A^H tile (op C, or the Hermitian upper part): k contiguous
         cp_async16(&sA[m * LDAK + k], valid ? src : p.A, valid);
       else
         cp_async16(&sA[k * LDA_S + m], valid ? src : p.A, valid);
@@ -187,25 +188,34 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
     const double *b = reinterpret_cast<const double *>(smem + st * STAGE_ELEMS + SA_ELEMS);
     const unsigned anm = (conjA ? le.a_neg_conj : le.a_neg) ^ aflip;
     const unsigned bnm = (OPB == OP_C) ? le.b_neg_conj : 0u;
+    // the A^H layout is chosen per k-tile (uniform branch: two specialised loops)
+    auto compute = [&](auto km) {
+      constexpr bool KM = decltype(km)::value;   // A tile stored [m][k]
 #pragma unroll
-    for (int ks = 0; ks < BK / 2; ks++) {
-      const int kk = ks * 2 + ((lane & 3) >> 1);
-      double af[4], bf[4];
+      for (int ks = 0; ks < BK / 2; ks++) {
+        const int kk = ks * 2 + ((lane & 3) >> 1);
+        double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const int mm = wm * 16 + i * 4 + (lane >> 3);
-        af[i] = xsign((!HERM && OPA == OP_C) ? a[(mm * LDAK + kk) * 2 + le.a_comp] : a[(kk * LDA_S + mm) * 2 + le.a_comp],
-                      anm);
+        for (int i = 0; i < 4; i++) {
+          const int mm = wm * 16 + i * 4 + (lane >> 3);
+          af[i] = xsign(KM ? a[(mm * LDAK + kk) * 2 + le.a_comp] : a[(kk * LDA_S + mm) * 2 + le.a_comp], anm);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int nn = wn * 32 + j * 8 + (lane >> 2);
+          bf[j] = xsign(OPB == OP_C ? b[(kk * LDBN + nn) * 2 + le.b_comp] : b[(nn * LDB_S + kk) * 2 + le.b_comp], bnm);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+          for (int j = 0; j < 4; j++) dmma(acc[i][j], af[i], bf[j]);
       }
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const int nn = wn * 32 + j * 8 + (lane >> 2);
-        bf[j] = xsign(OPB == OP_C ? b[(kk * LDBN + nn) * 2 + le.b_comp] : b[(nn * LDB_S + kk) * 2 + le.b_comp], bnm);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; i++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) dmma(acc[i][j], af[i], bf[j]);
+    };
+    if (HERM) {
+      if (conjA) compute(std::true_type{});
+      else compute(std::false_type{});
+    } else {
+      compute(std::integral_constant<bool, OPA == OP_C>{});
     }
   }
   cp_async_wait<0>();
