@@ -212,3 +212,27 @@ def test_config3_n10000_all_vectors_known_spectrum():
     assert np.max(np.abs(w - D)) / np.max(np.abs(D)) <= 1e-10
     res, orth = gates(A, B, torch.from_numpy(w).cuda(), Z)
     assert res <= 1e-14 and orth <= 1e-14
+
+
+@gpu
+def test_config4_n20000_fraction10_known_spectrum():
+    """BASELINE configs[4]: n = 20000, 10% of the eigenvectors (known spectrum,
+    all gates).  Exercises the large-n paths: panel CTA count bound by shared
+    memory, the split Q2 kernel (2 fragments per SM), 106-CTA bulge chase."""
+    n = 20000
+    A, B, D = _known_pencil_torch(n, 21)
+    s = _solver()
+    Ac = torch.tril(A).t().contiguous().t()
+    Bc = torch.tril(B).t().contiguous().t()
+    torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    w, Z = s.solve_gen(Ac, Bc, fraction=0.1)
+    print(f"eig_solve_gen n={n} 10% vectors: {time.perf_counter() - t0:.3f} s")
+    del Ac, Bc
+    m = Z.shape[1]
+    assert m == 2000
+    w = w.cpu().numpy()
+    assert np.max(np.abs(w - D)) / np.max(np.abs(D)) <= 1e-10
+    res, orth = gates(A, B, torch.from_numpy(w[:m]).cuda(), Z)
+    assert res <= 1e-14 and orth <= 1e-14
