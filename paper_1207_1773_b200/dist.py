@@ -20,11 +20,22 @@ def column_slice(m: int, rank: int, world: int):
     return (m * rank) // world, (m * (rank + 1)) // world
 
 
+def _dense(t):
+    """A contiguous alias of t (same storage): the column-major matrices of the
+    C ABI are transposed views, which NCCL collectives reject as
+    non-contiguous; their transpose is the contiguous row-major alias."""
+    if t.is_contiguous():
+        return t
+    if t.dim() == 2 and t.t().is_contiguous():
+        return t.t()
+    raise ValueError("broadcast needs a dense (row- or column-major) tensor")
+
+
 def broadcast_factors(tensors, src: int = 0, group=None):
     """Broadcast the read-only factors from `src` (in place, list order).
     One collective per tensor; NCCL pipelines them on its stream."""
     for t in tensors:
-        dist.broadcast(t, src=src, group=group)
+        dist.broadcast(_dense(t), src=src, group=group)
 
 
 def hotpath_sharded(solver, A, tau1, T1, V2, tau2, L, Z_slice, E_slice, group=None):
