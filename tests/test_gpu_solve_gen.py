@@ -236,3 +236,29 @@ def test_config4_n20000_fraction10_known_spectrum():
     assert np.max(np.abs(w - D)) / np.max(np.abs(D)) <= 1e-10
     res, orth = gates(A, B, torch.from_numpy(w[:m]).cuda(), Z)
     assert res <= 1e-14 and orth <= 1e-14
+
+
+@gpu
+@pytest.mark.parametrize("il,iu", [(101, 160), (1, 1), (500, 500), (250, 251)])
+def test_solve_gen_index_range(il, iu):
+    """EIG_RANGE_INDEX (S:L57-L65 index-range il..iu): all eigenvalues, eigenvectors of
+    the il-th .. iu-th only, which must pass the gates on their own."""
+    n = 500
+    A, B, D = synth.pencil_known(n, seed=12, kappa=1e2, clustered=False)
+    w, Z = _run(A, B, il=il, iu=iu)
+    assert Z.shape[1] == iu - il + 1
+    assert np.max(np.abs(w - D)) / np.max(np.abs(D)) <= 1e-10
+    res, orth = gates(A, B, w[il - 1:iu], Z)
+    assert res <= 1e-14 and orth <= 1e-14
+
+
+@gpu
+def test_solve_gen_tiny_fraction():
+    """fraction -> il = 1, iu = ceil(f n) = 1: one eigenvector, the lowest."""
+    n = 300
+    A, B, D = synth.pencil_known(n, seed=13, kappa=10.0, clustered=True)
+    w, Z = _run(A, B, fraction=0.001)
+    assert Z.shape[1] == 1
+    assert np.max(np.abs(w - D)) / np.max(np.abs(D)) <= 1e-10
+    res, orth = gates(A, B, w[:1], Z)
+    assert res <= 1e-14 and orth <= 1e-14
