@@ -36,6 +36,9 @@ constexpr int KSMEM = 12288;   // merge sizes whose (D, z) fit in shared memory 
 struct Node {
   int64_t lo, mid, hi;
 };
+// per-node counters: [0] K' (non-deflated), [1] KD (deflated), [2] NR (rotations),
+// [3] Kneed, [4] K1 / [5] K3 / [6] K2 non-deflated columns of child 1 only, mixed, child 2 only
+constexpr int NCNT = 8;
 
 struct DcBufs {
   int64_t n;
@@ -58,7 +61,8 @@ struct DcBufs {
   double *DdS;        // deflated values sorted ascending
   int *cdS;           // and their local columns
   int64_t *fposd;     // final position of sorted deflated t (at lo + t)
-  int *cnt;           // per node: [0] K', [1] KD, [2] NR, [3] Kneed
+  int *cnt;           // per node: NCNT counters (see Node)
+  int *cpos;          // non-deflated column i -> its position in type order [child 1 | mixed | child 2]
   double *rho;        // per node: rho * |u|^2
   const Node *nodes;
   int64_t il, iu;     // selection (only for the root node)
@@ -253,6 +257,10 @@ __global__ void __launch_bounds__(PT) dc_prep_kernel(DcBufs b) {
   if (tid == 0) {
     const double tol = 8.0 * DBL_EPSILON * fmax(dmax, rho2);
     int K = 0, KD = 0, NR = 0, pj = -1;
+    // column types (LAPACK dlaed2 ctot): 1 = rows of child 1 only, 2 = child 2
+    // only, 3 = mixed by a rotation; tpj is the type of the pending column pj
+    int tpj = 0;
+    auto type0 = [&](int j) { return b.perm[lo + j] < k1 ? 1 : 2; };
     for (int j = 0; j < k; j++) {
       const double zj = z[j];
       if (rho2 * fabs(zj) <= tol) {
@@ -263,6 +271,7 @@ __global__ void __launch_bounds__(PT) dc_prep_kernel(DcBufs b) {
       }
       if (pj < 0) {
         pj = j;
+        tpj = type0(j);
         continue;
       }
       double s = z[pj], c = zj;
@@ -286,26 +295,47 @@ __global__ void __launch_bounds__(PT) dc_prep_kernel(DcBufs b) {
         b.cd[lo + KD] = b.perm[lo + pj];
         KD++;
         pj = j;
+        tpj |= type0(j);
       } else {
         b.Dn[lo + K] = D[pj];
         b.zn[lo + K] = z[pj];
         b.cn[lo + K] = b.perm[lo + pj];
+        b.cpos[lo + K] = tpj;
         K++;
         pj = j;
+        tpj = type0(j);
       }
     }
     if (pj >= 0) {
       b.Dn[lo + K] = D[pj];
       b.zn[lo + K] = z[pj];
       b.cn[lo + K] = b.perm[lo + pj];
+      b.cpos[lo + K] = tpj;
       K++;
     }
+    // type order [child 1 | mixed | child 2]: the merge GEMM then skips the
+    // zero blocks of diag(Z1, Z2)
+    int K1 = 0, K3 = 0, K2 = 0;
+    for (int i = 0; i < K; i++) {
+      const int t = b.cpos[lo + i];
+      K1 += t == 1;
+      K3 += t == 3;
+      K2 += t == 2;
+    }
+    int p1 = 0, p3 = K1, p2 = K1 + K3;
+    for (int i = 0; i < K; i++) {
+      const int t = b.cpos[lo + i];
+      b.cpos[lo + i] = t == 1 ? p1++ : (t == 3 ? p3++ : p2++);
+    }
+    b.cnt[blockIdx.x * NCNT + 4] = K1;
+    b.cnt[blockIdx.x * NCNT + 5] = K3;
+    b.cnt[blockIdx.x * NCNT + 6] = K2;
     s_cnt[0] = K;
     s_cnt[1] = KD;
     s_cnt[2] = NR;
-    b.cnt[blockIdx.x * 4 + 0] = K;
-    b.cnt[blockIdx.x * 4 + 1] = KD;
-    b.cnt[blockIdx.x * 4 + 2] = NR;
+    b.cnt[blockIdx.x * NCNT + 0] = K;
+    b.cnt[blockIdx.x * NCNT + 1] = KD;
+    b.cnt[blockIdx.x * NCNT + 2] = NR;
     b.rho[blockIdx.x] = rho2;
   }
   __syncthreads();
@@ -342,7 +372,7 @@ __device__ __forceinline__ double warp_allprod(double v) {
 
 __global__ void dc_secular_kernel(DcBufs b) {
   const Node nd = b.nodes[blockIdx.y];
-  const int K = b.cnt[blockIdx.y * 4 + 0];
+  const int K = b.cnt[blockIdx.y * NCNT + 0];
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= K) return;   // warp-uniform
@@ -392,7 +422,7 @@ __global__ void dc_secular_kernel(DcBufs b) {
 // (one warp per i, strided partial products combined with a fixed butterfly)
 __global__ void dc_zhat_kernel(DcBufs b) {
   const Node nd = b.nodes[blockIdx.y];
-  const int K = b.cnt[blockIdx.y * 4 + 0];
+  const int K = b.cnt[blockIdx.y * NCNT + 0];
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (i >= K) return;   // warp-uniform
@@ -418,7 +448,7 @@ __global__ void __launch_bounds__(PT) dc_order_kernel(DcBufs b, int root_node) {
   extern __shared__ __align__(16) double sm[];
   const Node nd = b.nodes[blockIdx.x];
   const int64_t lo = nd.lo;
-  const int K = b.cnt[blockIdx.x * 4 + 0], KD = b.cnt[blockIdx.x * 4 + 1];
+  const int K = b.cnt[blockIdx.x * NCNT + 0], KD = b.cnt[blockIdx.x * NCNT + 1];
   const int tid = threadIdx.x;
   const bool root = (int)blockIdx.x == root_node;
   double *DdS = b.DdS + lo;
@@ -469,7 +499,7 @@ __global__ void __launch_bounds__(PT) dc_order_kernel(DcBufs b, int root_node) {
       const bool need = !root || (pos >= b.il - 1 && pos <= b.iu - 1);
       b.qcol[lo + j] = need ? q++ : -1;
     }
-    b.cnt[blockIdx.x * 4 + 3] = q;
+    b.cnt[blockIdx.x * NCNT + 3] = q;
   }
 }
 
@@ -478,7 +508,7 @@ __global__ void __launch_bounds__(PT) dc_qbuild_kernel(DcBufs b) {
   __shared__ double red[32];
   const Node nd = b.nodes[blockIdx.y];
   const int64_t lo = nd.lo, n = b.n;
-  const int K = b.cnt[blockIdx.y * 4 + 0];
+  const int K = b.cnt[blockIdx.y * NCNT + 0];
   const int j = blockIdx.x;
   if (j >= K) return;
   const int qc = b.qcol[lo + j];
@@ -489,7 +519,7 @@ __global__ void __launch_bounds__(PT) dc_qbuild_kernel(DcBufs b) {
   double s2 = 0.0;
   for (int i = threadIdx.x; i < K; i += PT) {
     const double v = b.zh[lo + i] / ((D[i] - Do) - tj);
-    q[i] = v;
+    q[b.cpos[lo + i]] = v;   // row in type order (matches the gathered columns)
     s2 += v * v;
   }
   const double inv = 1.0 / sqrt(block_sum(s2, red));
@@ -501,11 +531,11 @@ __global__ void dc_gather_kernel(DcBufs b) {
   const Node nd = b.nodes[blockIdx.y];
   const int64_t lo = nd.lo, n = b.n;
   const int k = (int)(nd.hi - nd.lo);
-  const int K = b.cnt[blockIdx.y * 4 + 0];
+  const int K = b.cnt[blockIdx.y * NCNT + 0];
   const int64_t total = (int64_t)k * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e % k), i = (int)(e / k);
-    b.Zg[(lo + r) + (lo + i) * n] = b.Zold[(lo + r) + (lo + b.cn[lo + i]) * n];
+    b.Zg[(lo + r) + (lo + b.cpos[lo + i]) * n] = b.Zold[(lo + r) + (lo + b.cn[lo + i]) * n];
   }
 }
 
@@ -516,7 +546,7 @@ __global__ void dc_scatter_kernel(DcBufs b, int root_node) {
   const Node nd = b.nodes[node];
   const int64_t lo = nd.lo, n = b.n;
   const int k = (int)(nd.hi - nd.lo);
-  const int K = b.cnt[node * 4 + 0], KD = b.cnt[node * 4 + 1];
+  const int K = b.cnt[node * NCNT + 0], KD = b.cnt[node * NCNT + 1];
   const bool root = node == root_node;
   const int64_t total = (int64_t)k * k;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -581,7 +611,7 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
   // ---- workspace
   const size_t nn = (size_t)n * n;
   const size_t nd = (size_t)n;
-  size_t bytes = 5 * nn * sizeof(double) + 9 * nd * sizeof(double) + 9 * nd * sizeof(int64_t) +
+  size_t bytes = 5 * nn * sizeof(double) + 9 * nd * sizeof(double) + 10 * nd * sizeof(int64_t) +
                  (size_t)(leaf_lo.size() * 2) * sizeof(int64_t) + 32 * 256;   // + alignment of each take
   char *wsp = (char *)c.ws(WS_DC, bytes);
   if (!wsp) return EIG_ERR_NOMEM;
@@ -618,6 +648,7 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
   b.org = (int *)take(nd * 4);
   b.qcol = (int *)take(nd * 4);
   b.cdS = (int *)take(nd * 4);
+  b.cpos = (int *)take(nd * 4);
   b.fpos = (int64_t *)take(nd * 8);
   b.fposd = (int64_t *)take(nd * 8);
   int64_t *d_llo = (int64_t *)take(leaf_lo.size() * 8), *d_lhi = (int64_t *)take(leaf_lo.size() * 8);
@@ -628,12 +659,12 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
   // per-level node arrays / counters (small, separate buffer)
   size_t maxnodes = 1;
   for (auto &lv : levels) maxnodes = std::max(maxnodes, lv.size());
-  char *small = (char *)c.ws(WS_DC_SMALL, maxnodes * (sizeof(Node) + 4 * sizeof(int) + sizeof(double) +
-                                                       sizeof(DgemmProb)) + 4096);
+  char *small = (char *)c.ws(WS_DC_SMALL, maxnodes * (sizeof(Node) + NCNT * sizeof(int) + sizeof(double) +
+                                                       2 * sizeof(DgemmProb)) + 4096);
   if (!small) return EIG_ERR_NOMEM;
   Node *d_nodes = (Node *)small;
   int *d_cnt = (int *)(small + ((maxnodes * sizeof(Node) + 255) & ~(size_t)255));
-  double *d_rho = (double *)((char *)d_cnt + ((maxnodes * 4 * sizeof(int) + 255) & ~(size_t)255));
+  double *d_rho = (double *)((char *)d_cnt + ((maxnodes * NCNT * sizeof(int) + 255) & ~(size_t)255));
   DgemmProb *d_probs = (DgemmProb *)((char *)d_rho + ((maxnodes * sizeof(double) + 255) & ~(size_t)255));
   b.cnt = d_cnt;
   b.rho = d_rho;
@@ -670,11 +701,11 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
     const size_t psm = 2 * (size_t)std::min<int64_t>(kmax, KSMEM) * 8;
     dc_prep_kernel<<<nn_, PT, psm, c.stream>>>(b);
     EIG_TRY(c.launched("dc_prep_kernel"));
-    cnt.resize(4 * nn_);
-    EIG_TRY(c.check(cudaMemcpyAsync(cnt.data(), d_cnt, 4 * nn_ * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "cnt"));
+    cnt.resize(NCNT * nn_);
+    EIG_TRY(c.check(cudaMemcpyAsync(cnt.data(), d_cnt, NCNT * nn_ * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "cnt"));
     EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync cnt"));
     int Kmax = 0;
-    for (int i = 0; i < nn_; i++) Kmax = std::max(Kmax, cnt[4 * i]);
+    for (int i = 0; i < nn_; i++) Kmax = std::max(Kmax, cnt[NCNT * i]);
     if (Kmax > 0) {
       dc_secular_kernel<<<dim3((Kmax + 7) / 8, nn_), 256, 0, c.stream>>>(b);   // 8 roots (warps) per CTA
       EIG_TRY(c.launched("dc_secular_kernel"));
@@ -683,7 +714,7 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
     }
     dc_order_kernel<<<nn_, PT, 0, c.stream>>>(b, top ? 0 : -1);
     EIG_TRY(c.launched("dc_order_kernel"));
-    EIG_TRY(c.check(cudaMemcpyAsync(cnt.data(), d_cnt, 4 * nn_ * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "cnt"));
+    EIG_TRY(c.check(cudaMemcpyAsync(cnt.data(), d_cnt, NCNT * nn_ * sizeof(int), cudaMemcpyDeviceToHost, c.stream), "cnt"));
     EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync cnt"));
     if (Kmax > 0) {
       dc_qbuild_kernel<<<dim3(Kmax, nn_), PT, 0, c.stream>>>(b);
@@ -694,13 +725,15 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
       probs.clear();
       int max_tiles = 0;
       for (int i = 0; i < nn_; i++) {
-        const int K = cnt[4 * i], Kn = cnt[4 * i + 3];
-        const int64_t lo = lv[i].lo, k = lv[i].hi - lv[i].lo;
+        const int K = cnt[NCNT * i], Kn = cnt[NCNT * i + 3];
+        const int K1 = cnt[NCNT * i + 4], K3 = cnt[NCNT * i + 5];
+        const int64_t lo = lv[i].lo, mid = lv[i].mid, hi = lv[i].hi;
         if (K == 0 || Kn == 0) continue;
+        // rows of child 1: columns [child 1 | mixed]; rows of child 2: [mixed | child 2]
         DgemmProb pr;
-        pr.M = k;
+        pr.M = mid - lo;
         pr.N = Kn;
-        pr.K = K;
+        pr.K = K1 + K3;
         pr.A = b.Zg + lo + lo * n;
         pr.lda = n;
         pr.B = b.Q + lo + lo * n;
@@ -708,7 +741,14 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
         pr.C = b.Zt + lo + lo * n;
         pr.ldc = n;
         probs.push_back(pr);
-        max_tiles = std::max(max_tiles, dgemm_tiles(k, Kn));
+        max_tiles = std::max(max_tiles, dgemm_tiles(pr.M, Kn));
+        pr.M = hi - mid;
+        pr.K = K - K1;
+        pr.A = b.Zg + mid + (lo + K1) * n;
+        pr.B = b.Q + (lo + K1) + lo * n;
+        pr.C = b.Zt + mid + lo * n;
+        probs.push_back(pr);
+        max_tiles = std::max(max_tiles, dgemm_tiles(pr.M, Kn));
       }
       if (!probs.empty()) {
         EIG_TRY(c.check(cudaMemcpyAsync(d_probs, probs.data(), probs.size() * sizeof(DgemmProb), cudaMemcpyHostToDevice,
