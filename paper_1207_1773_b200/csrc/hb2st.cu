@@ -163,17 +163,15 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       }
       // ---- (a) on the previous bulge (shared memory only): f, then store
       if (na > 0) {
-        if (upd && tid < 256) {   // four 16-row parts per column
-          const int q = tid & 63, h = tid >> 6;
-          const int t0 = h * 16, t1 = imin64(t0 + 16, len);
-          double2 acc = czero();
-          if (q < na)
-            for (int t = t0; t < t1; t++) acc = cadd(acc, cmulc(sv[t], sA[t + q * 64]));
-          spart[h][q] = acc;
+        if (upd) {   // one warp per column: lanes over the rows (conflict-free), shuffle reduction
+          for (int q = warp; q < na; q += HT / 32) {
+            double2 acc = czero();
+            if (lane < len) acc = cmulc(sv[lane], sA[lane + q * 64]);
+            if (lane + 32 < len) acc = cadd(acc, cmulc(sv[lane + 32], sA[lane + 32 + q * 64]));
+            acc = warp_sum2(acc);
+            if (lane == 0) sf[q] = cmul(ctau, acc);
+          }
         }
-        __syncthreads();
-        if (upd && tid < na)
-          sf[tid] = cmul(ctau, cadd(cadd(spart[0][tid], spart[1][tid]), cadd(spart[2][tid], spart[3][tid])));
         __syncthreads();
         for (int e = tid; e < na * 64; e += HT) {          // y_k - v f_k  (stored even if tau = 0:
           const int t = e & 63, k = e >> 6;               //  the previous task left this region in smem)
