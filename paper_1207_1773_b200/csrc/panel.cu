@@ -62,6 +62,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double2 sm[];
   const int nb = a.nb, R = a.R, G = a.G;
+  const int LR = R | 1;   // odd column stride of the resident rows: conflict-free column-parallel access
   const int recw = 2 * nb;
   double2 *sTau = sm;               // [nb]
   double2 *sRow = sTau + nb;        // [nb]   row j (owner's record)
@@ -86,9 +87,9 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   const int rlo = min(rows, rq * R4), rhi = min(rows, (rq + 1) * R4);
 
   for (int l = 0; l < nb; l++)
-    for (int r = tid; r < R; r += PT) sP[l * R + r] = (r < rows) ? a.P[(row0 + r) + (int64_t)l * a.lda] : czero();
+    for (int r = tid; r < R; r += PT) sP[l * LR + r] = (r < rows) ? a.P[(row0 + r) + (int64_t)l * a.lda] : czero();
   if (g == 0)
-    for (int e = tid; e < nb * nb; e += PT) sT[(e % nb) + (e / nb) * R] = czero();
+    for (int e = tid; e < nb * nb; e += PT) sT[(e % nb) + (e / nb) * LR] = czero();
   __syncthreads();
 
   const bool prof = a.prof != nullptr && g == 0 && tid == 0;
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   auto publish = [&](int jn, bool corr, double2 ctau) {
     double2 acc = czero();
     if (cl < nb) {
-      const double2 *aj = sP + jn * R, *pl = sP + cl * R;
+      const double2 *aj = sP + jn * LR, *pl = sP + cl * LR;
       for (int r = rlo; r < rhi; r++) {
         if (row0 + r <= jn) continue;
         const double2 x = aj[r];
@@ -134,8 +135,8 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     }
     if (jn >= row0 && jn < row0 + rows)
       for (int l = tid; l < nb; l += PT) {
-        double2 pv = sP[l * R + (jn - row0)];
-        if (corr && l > jn) pv = csub(pv, cmul(ctau, cmul(sP[(jn - 1) * R + (jn - row0)], sW[l])));
+        double2 pv = sP[l * LR + (jn - row0)];
+        if (corr && l > jn) pv = csub(pv, cmul(ctau, cmul(sP[(jn - 1) * LR + (jn - row0)], sW[l])));
         __stcg(&out[nb + l], pv);
       }
     __threadfence();
@@ -203,16 +204,16 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     }
     for (int r = tid; r < rows; r += PT) {
       const int64_t grow = row0 + r;
-      if (grow > j) sP[j * R + r] = cmul(sP[j * R + r], scale);
-      else if (grow == j) sP[j * R + r] = make_double2(s_beta, 0.0);
+      if (grow > j) sP[j * LR + r] = cmul(sP[j * LR + r], scale);
+      else if (grow == j) sP[j * LR + r] = make_double2(s_beta, 0.0);
     }
     __syncthreads();
-    const double2 *vj = sP + j * R;
+    const double2 *vj = sP + j * LR;
     const bool la = (j + 1 < a.nref);
     if (la) {
       // look-ahead: the next pivot column first, then publish it
       const double2 cw = cmul(ctau, sW[j + 1]);
-      double2 *pl = sP + (j + 1) * R;
+      double2 *pl = sP + (j + 1) * LR;
       for (int r = tid; r < rows; r += PT) {
         const int64_t grow = row0 + r;
         if (grow < j) continue;
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
           const int l = lo + lc;
           const int rb = (int)((int64_t)rows * part / tpc), re = (int)((int64_t)rows * (part + 1) / tpc);
           const double2 cw = cmul(ctau, sW[l]);
-          double2 *pl = sP + l * R;
+          double2 *pl = sP + l * LR;
           for (int r = rb; r < re; r++) {
             const int64_t grow = row0 + r;
             if (grow < j) continue;
@@ -250,14 +251,14 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       const int i = tid >> 2, part = tid & 3;
       double2 acc = czero();
       if (i < j)
-        for (int l = i + part; l < j; l += 4) acc = cadd(acc, cmul(sT[i + l * R], sY[l]));
+        for (int l = i + part; l < j; l += 4) acc = cadd(acc, cmul(sT[i + l * LR], sY[l]));
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
       if (i < j && part == 0)
-        sT[i + j * R] = make_double2(-(tau.x * acc.x - tau.y * acc.y), -(tau.x * acc.y + tau.y * acc.x));
-      if (tid == 0) sT[j + j * R] = tau;
+        sT[i + j * LR] = make_double2(-(tau.x * acc.x - tau.y * acc.y), -(tau.x * acc.y + tau.y * acc.x));
+      if (tid == 0) sT[j + j * LR] = tau;
     }
     __syncthreads();
     mark(5);
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   for (int l = 0; l < nb; l++)
     for (int r = tid; r < rows; r += PT) {
       const int64_t grow = row0 + r;
-      const double2 p = sP[l * R + r];
+      const double2 p = sP[l * LR + r];
       a.P[grow + (int64_t)l * a.lda] = p;
       const double2 v = (grow > l) ? p : (grow == l ? make_double2(1.0, 0.0) : czero());
       a.vout[grow + (int64_t)l * a.ldv] = v;
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     }
   if (g == 0) {
     for (int l = tid; l < nb; l += PT) a.tau[l] = (l < a.nref) ? sTau[l] : czero();
-    for (int e = tid; e < nb * nb; e += PT) a.T[e] = sT[(e % nb) + (e / nb) * R];
+    for (int e = tid; e < nb * nb; e += PT) a.T[e] = sT[(e % nb) + (e / nb) * LR];
   }
   if (prof)
     for (int k = 0; k < 6; k++) atomicAdd(&a.prof[8 + k], (unsigned long long)tacc[k]);
@@ -318,13 +319,13 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   const int gmax = gmax_env > 0 ? std::min(gmax_env, ctx.num_sms) : std::min(32, ctx.num_sms);
   int G = (int)std::min<int64_t>(gmax, (pn + nb - 1) / nb);
   G = std::max(G, 1);
-  const int rmax = (int)((220 * 1024 / sizeof(double2) - 5 * nb - NQ * 64) / nb);   // rows that fit on chip
+  const int rmax = (int)((220 * 1024 / sizeof(double2) - 5 * nb - NQ * 64) / nb) - 1;   // rows that fit on chip (odd stride)
   G = std::max<int64_t>(G, (pn + nb + rmax - 1) / rmax);
   int R = (int)((pn + nb + G - 1) / G);   // CTA 0 holds R - nb rows
   R = std::max(R, nb);
   G = (int)((pn + nb + R - 1) / R);
   const int recw = 2 * nb;
-  const size_t smem = ((size_t)5 * nb + NQ * 64 + (size_t)nb * R) * sizeof(double2);
+  const size_t smem = ((size_t)5 * nb + NQ * 64 + (size_t)nb * (R | 1)) * sizeof(double2);
   if (smem > 220 * 1024) return EIG_ERR_NOTIMPL;  // panel too tall for on-chip residency (n > ~20000 at nb=64)
   PanelArgs a;
   a.P = P;
