@@ -139,9 +139,11 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
         if (corr && l > jn) pv = csub(pv, cmul(ctau, cmul(sP[(jn - 1) * LR + (jn - row0)], sW[l])));
         __stcg(&out[nb + l], pv);
       }
-    __threadfence();
+    // the barrier orders every thread's record stores before thread 0's
+    // release increment (fence cumulativity): one release instead of a
+    // membar in every thread
     __syncthreads();
-    if (tid == 0) atomicAdd(a.cnt, 1ull);
+    if (tid == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
   };
 
   if (a.nref > 0) publish(0, false, czero());
