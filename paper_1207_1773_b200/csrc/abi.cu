@@ -146,6 +146,9 @@ static int he2hb_run(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau, d
 //   trapezoidal from row (k0+1)nb),  T = [[T_a, -T_a (V_a^H V_b) T_b], [0, T_b]]
 // merged pairwise from the per-panel T_k with the Gram matrix V^H V, so each
 // pass over E is three GEMMs with K = ga*nb instead of nb.
+// The preparation of a group (explicit V, Gram matrix, merged T) runs on the
+// side stream one group ahead of the three big GEMMs on the main stream
+// (double-buffered by group parity), so only the GEMMs are on the critical path.
 static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const double2 *T, double2 *E, int64_t lde,
                         int64_t m) {
   const int nb = c.nb;
@@ -154,49 +157,71 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
   const int ga_max = std::max(1, 256 / nb);
   const int kw = ga_max * nb;                       // aggregated width
   const int64_t ldv = n - nb;
-  double2 *Vb = (double2 *)c.ws(WS_V, (size_t)ldv * kw * sizeof(double2));
+  double2 *Vb0 = (double2 *)c.ws(WS_V, (size_t)2 * ldv * kw * sizeof(double2));
   double2 *Y = (double2 *)c.ws(WS_Y, (size_t)kw * m * sizeof(double2));
   double2 *Y2 = (double2 *)c.ws(WS_Y2, (size_t)kw * m * sizeof(double2));
-  double2 *Tg = (double2 *)c.ws(WS_TAGG, (size_t)3 * kw * kw * sizeof(double2));
-  if (!Vb || !Y || !Y2 || !Tg) return EIG_ERR_NOMEM;
-  double2 *Gm = Tg + (size_t)kw * kw, *Tmp = Gm + (size_t)kw * kw;
+  double2 *Tg0 = (double2 *)c.ws(WS_TAGG, (size_t)6 * kw * kw * sizeof(double2));
+  if (!Vb0 || !Y || !Y2 || !Tg0) return EIG_ERR_NOMEM;
   const int64_t ngroups = (K + ga_max - 1) / ga_max;
-  for (int64_t gi = ngroups - 1; gi >= 0; gi--) {
+  auto Vbuf = [&](int par) { return Vb0 + (size_t)par * ldv * kw; };
+  auto Tbuf = [&](int par) { return Tg0 + (size_t)par * 3 * kw * kw; };
+  // preparation of group gi into buffer par, on the side stream
+  auto prep = [&](int64_t gi, int par) -> int {
     const int64_t k0 = gi * ga_max;
     const int ga = (int)std::min<int64_t>(ga_max, K - k0);
     const int w = ga * nb;
     const int64_t r0 = (k0 + 1) * nb, s = n - r0;
-    EIG_TRY(extract_v(c, A + r0 + k0 * nb * lda, lda, s, w, Vb, ldv));
-    Zgemm g;
-    const double2 *Tuse = T + k0 * nb * nb;
-    int ldt = nb;
-    if (ga > 1) {
+    double2 *Vb = Vbuf(par), *Tg = Tbuf(par);
+    double2 *Gm = Tg + (size_t)kw * kw, *Tmp = Gm + (size_t)kw * kw;
+    EIG_TRY(c.check(cudaStreamWaitEvent(c.side, c.ev_q1[2 + par], 0), "q1 buffer free"));
+    const cudaStream_t keep = c.stream;
+    c.stream = c.side;
+    int rc = extract_v(c, A + r0 + k0 * nb * lda, lda, s, w, Vb, ldv);
+    if (!rc && ga > 1) {
       // aggregated T: diagonal blocks T_k, off-diagonal blocks merged pairwise
-      EIG_TRY(c.check(cudaMemsetAsync(Tg, 0, (size_t)w * w * sizeof(double2), c.stream), "memset T"));
-      for (int p = 0; p < ga; p++)
-        EIG_TRY(c.check(cudaMemcpy2DAsync(Tg + (size_t)p * nb * w + p * nb, w * sizeof(double2),
-                                          T + (k0 + p) * nb * nb, nb * sizeof(double2), nb * sizeof(double2), nb,
-                                          cudaMemcpyDeviceToDevice, c.stream), "copy T"));
-      g = Zgemm();   // Gram = V^H V
+      rc = c.check(cudaMemsetAsync(Tg, 0, (size_t)w * w * sizeof(double2), c.stream), "memset T");
+      for (int p = 0; p < ga && !rc; p++)
+        rc = c.check(cudaMemcpy2DAsync(Tg + (size_t)p * nb * w + p * nb, w * sizeof(double2), T + (k0 + p) * nb * nb,
+                                       nb * sizeof(double2), nb * sizeof(double2), nb, cudaMemcpyDeviceToDevice,
+                                       c.stream), "copy T");
+      Zgemm g;   // Gram = V^H V
       g.opa = OP_C; g.M = w; g.N = w; g.K = s; g.A = Vb; g.lda = ldv; g.B = Vb; g.ldb = ldv; g.C = Gm; g.ldc = w;
-      EIG_TRY(zgemm(c, g));
-      for (int span = nb; span < w; span *= 2)
-        for (int p0 = 0; p0 + span < w; p0 += 2 * span) {
+      if (!rc) rc = zgemm(c, g);
+      for (int span = nb; span < w && !rc; span *= 2)
+        for (int p0 = 0; p0 + span < w && !rc; p0 += 2 * span) {
           const int p1 = p0 + span, p2 = std::min(w, p1 + span);
           // Tmp = T[p0:p1, p0:p1] G[p0:p1, p1:p2];  T[p0:p1, p1:p2] = -Tmp T[p1:p2, p1:p2]
           g = Zgemm();
           g.M = span; g.N = p2 - p1; g.K = span; g.A = Tg + (size_t)p0 * w + p0; g.lda = w;
           g.B = Gm + (size_t)p1 * w + p0; g.ldb = w; g.C = Tmp; g.ldc = w;
-          EIG_TRY(zgemm(c, g));
+          rc = zgemm(c, g);
+          if (rc) break;
           g = Zgemm();
           g.M = span; g.N = p2 - p1; g.K = p2 - p1; g.A = Tmp; g.lda = w; g.B = Tg + (size_t)p1 * w + p1; g.ldb = w;
           g.C = Tg + (size_t)p1 * w + p0; g.ldc = w; g.alpha = -1.0;
-          EIG_TRY(zgemm(c, g));
+          rc = zgemm(c, g);
         }
-      Tuse = Tg;
-      ldt = w;
     }
-    g = Zgemm();   // Y = V^H E
+    c.stream = keep;
+    if (rc) return rc;
+    return c.check(cudaEventRecord(c.ev_q1[par], c.side), "q1 prep done");
+  };
+  // the side stream starts after everything already queued (he2hb's A and T)
+  EIG_TRY(c.check(cudaEventRecord(c.ev_fork, c.stream), "q1 fork"));
+  EIG_TRY(c.check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "q1 fork wait"));
+  EIG_TRY(prep(ngroups - 1, (int)((ngroups - 1) & 1)));
+  for (int64_t gi = ngroups - 1; gi >= 0; gi--) {
+    const int par = (int)(gi & 1);
+    if (gi > 0) EIG_TRY(prep(gi - 1, par ^ 1));   // overlaps this group's GEMMs
+    const int64_t k0 = gi * ga_max;
+    const int ga = (int)std::min<int64_t>(ga_max, K - k0);
+    const int w = ga * nb;
+    const int64_t r0 = (k0 + 1) * nb, s = n - r0;
+    const double2 *Vb = Vbuf(par);
+    const double2 *Tuse = ga > 1 ? Tbuf(par) : T + k0 * nb * nb;
+    const int ldt = ga > 1 ? w : nb;
+    EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_q1[par], 0), "q1 prep wait"));
+    Zgemm g;   // Y = V^H E
     g.opa = OP_C; g.M = w; g.N = m; g.K = s; g.A = Vb; g.lda = ldv; g.B = E + r0; g.ldb = lde; g.C = Y; g.ldc = w;
     EIG_TRY(zgemm(c, g));
     g = Zgemm();   // Y2 = T Y
@@ -206,6 +231,7 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
     g.M = s; g.N = m; g.K = w; g.A = Vb; g.lda = ldv; g.B = Y2; g.ldb = w; g.C = E + r0; g.ldc = lde;
     g.alpha = -1.0; g.beta = 1.0;
     EIG_TRY(zgemm(c, g));
+    EIG_TRY(c.check(cudaEventRecord(c.ev_q1[2 + par], c.stream), "q1 gemms done"));
   }
   return 0;
 }
@@ -444,6 +470,8 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
   if (!rc) rc = x->c.check(cudaStreamCreateWithFlags(&x->c.xfer, cudaStreamNonBlocking), "xfer stream");
   if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_xfer, cudaEventDisableTiming), "event");
   if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_blk, cudaEventDisableTiming), "event");
+  for (int i = 0; i < 4 && !rc; i++)
+    rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_q1[i], cudaEventDisableTiming), "event");
   if (rc) { delete x; return rc; }
   void *bar = x->c.ws(WS_BARRIER, 64);
   if (!bar) { delete x; return EIG_ERR_NOMEM; }
@@ -473,6 +501,8 @@ int eig_finalize(eig_handle h) {
   if (h->c.xfer) { cudaStreamSynchronize(h->c.xfer); cudaStreamDestroy(h->c.xfer); }
   if (h->c.ev_xfer) cudaEventDestroy(h->c.ev_xfer);
   if (h->c.ev_blk) cudaEventDestroy(h->c.ev_blk);
+  for (int i = 0; i < 4; i++)
+    if (h->c.ev_q1[i]) cudaEventDestroy(h->c.ev_q1[i]);
   for (int i = 0; i < WS_COUNT; i++) {
     if (h->c.buf[i]) cudaFree(h->c.buf[i]);
   }

@@ -13,6 +13,7 @@ enum WsId {
   WS_VXV = 0,     // s x 3nb: [V | X | V]
   WS_W,           // s x nb
   WS_PART,        // split-K partials
+  WS_PART_SIDE,   // split-K partials of GEMMs on the side stream (concurrent with the main stream's)
   WS_SMALL,       // nb x nb scratch (Mh, M)
   WS_PANEL_REC,   // panel reduction records
   WS_BARRIER,     // grid barrier words
@@ -44,6 +45,7 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t xfer = nullptr;        // host <-> device copies overlapped with compute (EIG_HOST_BUFFERS)
   cudaEvent_t ev_xfer = nullptr, ev_blk = nullptr;
+  cudaEvent_t ev_q1[4] = {nullptr, nullptr, nullptr, nullptr};   // Q1: prep done [0,1], GEMMs done [2,3]
   int nb = 64;
   int q2g = 32;
   int num_sms = 148;

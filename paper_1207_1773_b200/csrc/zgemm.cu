@@ -338,7 +338,8 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   p.part = nullptr;
   p.row0 = g.row0;
   if (split > 1) {
-    p.part = (double2 *)ctx.ws(WS_PART, (size_t)split * g.M * g.N * sizeof(double2));
+    p.part = (double2 *)ctx.ws(ctx.stream == ctx.side ? WS_PART_SIDE : WS_PART,
+                               (size_t)split * g.M * g.N * sizeof(double2));
     if (!p.part) return EIG_ERR_NOMEM;
   }
   dim3 grid((unsigned)tiles, (unsigned)split);
