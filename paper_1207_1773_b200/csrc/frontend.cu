@@ -66,19 +66,28 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double2 *A11, int64_t l
     const int r = e % b, c = e / b;
     if (r >= c) A11[r + c * lda] = L[r + c * 65];
   }
-  // inverse: column c by forward substitution
-  if (tid < b) {
-    const int c = tid;
-    for (int r = 0; r < b; r++) {
-      double2 s = (r == c) ? make_double2(1.0, 0.0) : czero();
-      if (r >= c) {
-        for (int k = c; k < r; k++) s = csub(s, cmul(L[r + k * 65], X[k + c * 65]));
-        const double2 d = L[r + r * 65];
-        s = make_double2(s.x / d.x, s.y / d.x);   // diagonal is real positive
-      } else {
-        s = czero();
+  // inverse: column c by forward substitution, four lanes per column (each
+  // sums every fourth term; two xor-shuffles combine them)
+  {
+    const int c = tid >> 2, part = tid & 3;
+    for (int r = 0; r < 64; r++) {
+      double2 acc = czero();
+      if (c < b && r < b && r > c)
+        for (int k = c + part; k < r; k += 4) acc = cadd(acc, cmul(L[r + k * 65], X[k + c * 65]));
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+      if (part == 0 && c < b && r < b) {
+        double2 v = czero();
+        if (r >= c) {
+          const double2 s = (r == c) ? make_double2(1.0 - acc.x, -acc.y) : make_double2(-acc.x, -acc.y);
+          const double d = L[r + r * 65].x;   // diagonal is real positive
+          v = make_double2(s.x / d, s.y / d);
+        }
+        X[r + c * 65] = v;
       }
-      X[r + c * 65] = s;
+      __syncwarp();
     }
   }
   __syncthreads();
