@@ -27,6 +27,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "ctx.h"
 #include "kernels.h"
@@ -816,6 +818,102 @@ __global__ void __launch_bounds__(32 * NQ * NG, 1) apply_q2s_kernel(Q2wArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- wavefront kernel (small m)
+// Block (g, j) of group g (sweeps 32g..32g+31, rows 32g+1+64j .. +94)
+// overlaps only blocks (g+1, j-1) and (g+1, j) of the group applied before it
+// (windows of 95 rows, groups 32 rows apart, steps 64 rows apart), so the
+// blocks with the same t = j + (G-1-g) are pairwise disjoint and every
+// block they depend on has a smaller t: up to ~J blocks per step instead of
+// one sequential chain per column fragment.  One cooperative
+// persistent kernel walks the ~J + 2G steps; at each step the (block,
+// fragment) items are split evenly over the CTAs, a CTA stages the V / T of a
+// block once for all its warps, and each warp runs the three contractions of
+// one fragment (loading its whole window and storing it back).
+__device__ __forceinline__ int64_t wave_J(const Q2wArgs &a, int64_t g) { return steps_of(a, g); }
+
+__global__ void __launch_bounds__(256, 1) apply_q2wave_kernel(Q2wArgs a, int64_t T) {
+  namespace cg = cooperative_groups;
+  constexpr int TH = 256, NWARP = TH / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < OFF_T; e += TH) q2w_sm[e] = czero();
+  __syncthreads();
+  const int64_t Gn = a.ngroups, F = a.nfr_total;
+  const Lane L(lane);
+  Frag Fr;
+  Fr.Ew = q2w_sm + OFF_E + w * 8 * LDE;
+  Fr.ew = reinterpret_cast<double *>(Fr.Ew);
+  Fr.E = a.E;
+  Fr.lde = a.lde;
+  Fr.lde2 = 2 * a.lde;
+  Fr.n = a.n;
+  Fr.more = false;   // every window is loaded and stored whole
+  Fr.base = 0;
+  Fr.ch0 = 0;
+  Fr.ch1 = 2 * 32;
+  Fr.ch2 = 2 * 64;
+  double2 *vc = vc_buf(0), *tb = t_buf(0);
+  cg::grid_group grid = cg::this_grid();
+  for (int64_t t = 0; t < T; t++) {
+    // blocks of this step: d = G-1-g in [dlo, dhi], j = t - d
+    const int64_t dhi = imin64(Gn - 1, t);
+    int64_t dlo = 0;
+    while (dlo <= dhi && t - dlo >= wave_J(a, Gn - 1 - dlo)) dlo++;
+    const int64_t nblk = dhi - dlo + 1;
+    if (nblk > 0) {
+      const int64_t items = nblk * F;
+      const int64_t i0c = items * blockIdx.x / gridDim.x, i1c = items * (blockIdx.x + 1) / gridDim.x;
+      for (int64_t it = i0c; it < i1c;) {
+        const int64_t bidx = it / F;                       // block within the step
+        const int64_t fa = it - bidx * F, fb = imin64(F, fa + (i1c - it));
+        const int64_t d = dlo + bidx, g = Gn - 1 - d, j = t - d, gi0 = g * G;
+        // ---- stage V (compact rows) and T of block (g, j)
+        const int nvalid = (int)imax64(0, imin64(G, a.n - 2 - j * NB - gi0 + 1));
+        const double2 *v2 = a.V2 + (a.off[j] + gi0) * NB;
+        const double2 *t2 = a.T2 + (a.first[g] + j) * G * G;
+        __syncthreads();   // the previous block's V / T are no longer read
+        for (int e = threadIdx.x; e < G * NB; e += TH) {
+          const int tt = e / NB, ss = e - tt * NB;
+          if (tt < nvalid) cp_async16(vc + vrow(tt) + PADL + ss, v2 + tt * NB + ss, true);
+        }
+        for (int e = threadIdx.x; e < G * G; e += TH) {
+          const int kk = e / G, xx = e - kk * G;
+          cp_async16(tb + tcol(kk) + xx, t2 + kk * G + xx, true);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        const double *vcd = reinterpret_cast<const double *>(vc);
+        const double *ttd = reinterpret_cast<const double *>(tb);
+        Fr.rs = gi0 + 1 + j * NB;
+        for (int64_t f = fa + w; f < fb; f += NWARP) {
+          Fr.c0 = f * 8;
+          Fr.ncols = (int)imin64(8, a.m - Fr.c0);
+          const int cA = 2 * (lane & 3);
+          Fr.ok0 = cA < Fr.ncols;
+          Fr.ok1 = cA + 1 < Fr.ncols;
+          // the whole window (rows rs .. rs + 94; row 95 is padding)
+          for (int e = lane; e < RING * 8; e += 32) {
+            const int q = e % RING, c = e / RING;
+            const int64_t row = Fr.rs + q;
+            const bool ok = q < W && row < a.n && c < Fr.ncols;
+            cp_async16m(&Fr.Ew[c * LDE + q], ok ? a.E + row + (Fr.c0 + c) * a.lde : a.E, ok);
+          }
+          cp_async_commit();
+          cp_async_wait<0>();
+          __syncwarp();
+          Fr.gE = reinterpret_cast<double *>(a.E + Fr.rs + (L.rr >> 1) + (Fr.c0 + cA) * a.lde) + (L.rr & 1);
+          long long tl = 0;
+          full_block(Fr, L, vcd, ttd, nullptr, tl);
+          __syncwarp();
+        }
+        it += fb - fa;
+      }
+    }
+    __threadfence();
+    grid.sync();
+  }
+}
+
 }  // namespace
 
 size_t q2w_smem_bytes() { return (size_t)OFF_BAR * sizeof(double2) + 32; }
@@ -839,6 +937,30 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
   const int per = (a.nfr_total + grid - 1) / grid;
   a.nslab = (per + NFS - 1) / NFS;
   const size_t smem = q2w_smem_bytes();
+  // few fragments per SM: the wavefront kernel (EIG_Q2_WAVE=0 disables)
+  static const int wave_env = [] {
+    const char *e = getenv("EIG_Q2_WAVE");
+    return e ? atoi(e) : 1;
+  }();
+  if (wave_env && per <= 2) {
+    int64_t T = 0;
+    for (int64_t g = 0; g < a.ngroups; g++) {
+      const int64_t i0 = g * G;
+      const int64_t J = (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
+      if (J > 0) T = std::max<int64_t>(T, J - 1 + (a.ngroups - 1 - g) + 1);
+    }
+    static bool attr_w = false;
+    if (!attr_w) {
+      EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem), "q2wave attr"));
+      attr_w = true;
+    }
+    const int gridw = ctx.num_sms;
+    void *args[] = {&a, &T};
+    EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)apply_q2wave_kernel, dim3(gridw), dim3(256), args, smem,
+                                                  ctx.stream), "q2wave launch"));
+    return ctx.launched("apply_q2wave_kernel");
+  }
   // few fragments per SM: share each fragment over 8 warps (EIG_Q2W_SPLIT=0 disables)
   static const int split_env = [] {
     const char *e = getenv("EIG_Q2W_SPLIT");
