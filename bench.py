@@ -357,7 +357,7 @@ def run_b200(a, rank, world, local_rank):
     if stages:
         stage_flops = {"he2hb": 16.0 / 3.0 * n ** 3, "q2": 8.0 * n * n * m, "q1": 8.0 * n * n * m,
                        "trsm": 4.0 * n * n * m}
-        q2k = "apply_q2w_kernel" if (nb == 64 and a.g == 32) else "apply_q2_kernel"
+        q2k = "apply_q2wave_kernel" if (nb == 64 and a.g == 32) else "apply_q2_kernel"
         kern = {"he2hb": "zgemm_kernel (hemm+her2k) + panel_qr_kernel", "q2": q2k,
                 "q1": "zgemm_kernel", "trsm": "zgemm_kernel"}
         dom = max(stages, key=stages.get)

@@ -937,12 +937,14 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
   const int per = (a.nfr_total + grid - 1) / grid;
   a.nslab = (per + NFS - 1) / NFS;
   const size_t smem = q2w_smem_bytes();
-  // few fragments per SM: the wavefront kernel (EIG_Q2_WAVE=0 disables)
+  // the wavefront kernel (measured faster at every m: n = 10^4, m = 1000 / 2500 /
+  // 5000 / 10000: 54 / 110 / 206 / 392 ms vs 135 / 274 / 306 / 404 ms for the
+  // per-fragment kernels below, which EIG_Q2_WAVE=0 selects)
   static const int wave_env = [] {
     const char *e = getenv("EIG_Q2_WAVE");
     return e ? atoi(e) : 1;
   }();
-  if (wave_env && per <= 2) {
+  if (wave_env) {
     int64_t T = 0;
     for (int64_t g = 0; g < a.ngroups; g++) {
       const int64_t i0 = g * G;
