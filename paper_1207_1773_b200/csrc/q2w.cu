@@ -217,8 +217,9 @@ __device__ __forceinline__ void issue_block(const Q2wArgs &a, const BlkSrc &b, i
 struct Lane {
   int lane, kq, rr;
   int offA, offC0, offC1, offT, offEB, offEC;   // shared-memory offsets (doubles)
+  int ldw2;                                      // window column stride (doubles)
   unsigned negConj, negT, negA;
-  __device__ __forceinline__ explicit Lane(int l) {
+  __device__ __forceinline__ explicit Lane(int l, int ldw = LDE) {
     const LaneEmb le(l);
     lane = l;
     kq = (l & 3) >> 1;
@@ -228,8 +229,9 @@ struct Lane {
     offC0 = 2 * (71 * kq + dv(kq) + (l >> 3) + PADL) + le.a_comp;      // V: q = 4f + lane>>3, t = 2ks + kq, ks even
     offC1 = 2 * (71 * kq + dv(2 + kq) + (l >> 3) + PADL) + le.a_comp;  //                                 ks odd
     offT = 2 * (36 * kq + (l >> 3)) + le.a_comp;                       // T[ra][kb] at tcol(kb) + ra
-    offEB = 2 * (LDE * (l >> 2) + kq) + (l & 1);           // E, operand layout
-    offEC = 2 * (LDE * 2 * (l & 3) + (rr >> 1)) + (rr & 1);  // E, accumulator layout (col 2(lane&3))
+    offEB = 2 * (ldw * (l >> 2) + kq) + (l & 1);           // E, operand layout
+    offEC = 2 * (ldw * 2 * (l & 3) + (rr >> 1)) + (rr & 1);  // E, accumulator layout (col 2(lane&3))
+    ldw2 = 2 * ldw;
     negConj = le.a_neg_conj;
     negT = le.a_neg;
     negA = le.a_neg ^ 0x80000000u;                          // -V in phase C
@@ -267,7 +269,7 @@ __device__ __forceinline__ void phase_c_rows(const Frag &F, const Lane &L, const
     const int ch = f < 8 ? F.ch0 : (f < 16 ? F.ch1 : F.ch2);
     const double *p = F.ew + ch + L.offEC + 8 * (f & 7);
     acc[u][0] = p[0];
-    acc[u][1] = p[2 * LDE];
+    acc[u][1] = p[L.ldw2];
   }
 #pragma unroll
   for (int ks = 0; ks < 16; ks++) {
@@ -300,7 +302,7 @@ __device__ __forceinline__ void phase_c_rows(const Frag &F, const Lane &L, const
     } else if (q < W) {
       double *p = F.ew + F.ch2 + L.offEC + 8 * (f & 7);
       p[0] = acc[u][0];
-      p[2 * LDE] = acc[u][1];
+      p[L.ldw2] = acc[u][1];
     }
   }
 }
@@ -332,6 +334,10 @@ __device__ __forceinline__ void pmark(unsigned long long *pp, long long &tl, int
     tl = t;
   }
 }
+// WAVE: the window's three 32-row chunks arrive as three cp.async groups
+// followed by one more (the next item's chunk 0); phase A waits for each chunk
+// just before its first k-step, and nothing is refilled here.
+template <bool WAVE = false>
 __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const double *vc, const double *tt,
                                            unsigned long long *pp, long long &tl) {
   // ---------------- phase A: Y = V^H E   (M-fragment mf nonzero on k-steps 2mf .. 2mf+33)
@@ -340,8 +346,20 @@ __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const d
   for (int mf = 0; mf < 8; mf++) y[mf][0] = y[mf][1] = 0.0;
 #pragma unroll
   for (int ks = 0; ks < 48; ks++) {
-    if (ks == 15) {   // rows 31..63 (cp.async group Y of the previous block)
+    if (!WAVE && ks == 15) {   // rows 31..63 (cp.async group Y of the previous block)
       cp_async_wait<0>();
+      __syncwarp();
+    }
+    if (WAVE && ks == 0) {
+      cp_async_wait<3>();
+      __syncwarp();
+    }
+    if (WAVE && ks == 16) {
+      cp_async_wait<2>();
+      __syncwarp();
+    }
+    if (WAVE && ks == 32) {
+      cp_async_wait<1>();
       __syncwarp();
     }
     const int ch = ks < 16 ? F.ch0 : (ks < 32 ? F.ch1 : F.ch2);
@@ -380,7 +398,7 @@ __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const d
       }
     }
   }
-  cp_async_commit();   // group X (possibly empty)
+  if (!WAVE) cp_async_commit();   // group X (possibly empty)
   phase_c_rows<8, PairsA, false>(F, L, vc, yb);
   phase_c_rows<8, PairsB, false>(F, L, vc, yb);
   if (F.more) {
@@ -401,7 +419,7 @@ __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const d
       cp_async16m(&F.Ew[c * LDE + ring_slot(F.base - 1)], ok ? F.E + prow + (F.c0 + c) * F.lde : F.E, ok);
     }
   }
-  cp_async_commit();   // group Y (possibly empty): needed from phase A k-step 15 of the next block
+  if (!WAVE) cp_async_commit();   // group Y (possibly empty): needed from phase A k-step 15 of the next block
   pmark(pp, tl, 3);
 }
 
@@ -831,27 +849,45 @@ __global__ void __launch_bounds__(32 * NQ * NG, 1) apply_q2s_kernel(Q2wArgs a) {
 // one fragment (loading its whole window and storing it back).
 __device__ __forceinline__ int64_t wave_J(const Q2wArgs &a, int64_t g) { return steps_of(a, g); }
 
+// Per warp, the window has four 32-row chunk slots (column stride LDWV): the
+// item being computed uses three, and the fourth receives the next item's
+// first chunk as soon as the item starts; the next item's other two chunks go
+// into the slots of the finished item, so the window loads overlap compute.
+constexpr int LDWV = 129;   // 4 chunks of 32 rows + 1 (odd: conflict-free)
+constexpr int OFF_WAVE_WIN = OFF_T + T_STAGE;   // after V / T stage 0
+static_assert(OFF_WAVE_WIN + 8 * 8 * LDWV <= OFF_BAR, "wave windows must fit the q2w shared-memory size");
+
 __global__ void __launch_bounds__(256, 1) apply_q2wave_kernel(Q2wArgs a, int64_t T) {
   namespace cg = cooperative_groups;
   constexpr int TH = 256, NWARP = TH / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < OFF_T; e += TH) q2w_sm[e] = czero();
+  // layout: V (stage 0) | (unused) | T (stage 0) | 8 windows of 8 x LDWV
+  double2 *vc = vc_buf(0), *tb = t_buf(0);
+  double2 *win0 = q2w_sm + OFF_WAVE_WIN;
+  for (int e = threadIdx.x; e < VC_STAGE; e += TH) vc[e] = czero();
   __syncthreads();
   const int64_t Gn = a.ngroups, F = a.nfr_total;
-  const Lane L(lane);
+  const Lane L(lane, LDWV);
   Frag Fr;
-  Fr.Ew = q2w_sm + OFF_E + w * 8 * LDE;
+  Fr.Ew = win0 + w * 8 * LDWV;
   Fr.ew = reinterpret_cast<double *>(Fr.Ew);
   Fr.E = a.E;
   Fr.lde = a.lde;
   Fr.lde2 = 2 * a.lde;
   Fr.n = a.n;
-  Fr.more = false;   // every window is loaded and stored whole
+  Fr.more = false;   // every window is stored whole, from the accumulators
   Fr.base = 0;
-  Fr.ch0 = 0;
-  Fr.ch1 = 2 * 32;
-  Fr.ch2 = 2 * 64;
-  double2 *vc = vc_buf(0), *tb = t_buf(0);
+  int sa = 0, sb = 1, sc = 2, sd = 3;   // chunk slots: rows 0-31, 32-63, 64-95, spare
+  // item = (step-local block index, fragment); chunk c of its window -> slot
+  auto load_chunk = [&](int64_t rs, int64_t c0, int ncols, int c, int slot) {
+    for (int e = lane; e < 32 * 8; e += 32) {
+      const int q = e & 31, col = e >> 5;
+      const int row_in = 32 * c + q;
+      const int64_t row = rs + row_in;
+      const bool ok = row_in < W && row < a.n && col < ncols;
+      cp_async16m(&Fr.Ew[col * LDWV + 32 * slot + q], ok ? a.E + row + (c0 + col) * a.lde : a.E, ok);
+    }
+  };
   cg::grid_group grid = cg::this_grid();
   for (int64_t t = 0; t < T; t++) {
     // blocks of this step: d = G-1-g in [dlo, dhi], j = t - d
@@ -862,9 +898,36 @@ __global__ void __launch_bounds__(256, 1) apply_q2wave_kernel(Q2wArgs a, int64_t
     if (nblk > 0) {
       const int64_t items = nblk * F;
       const int64_t i0c = items * blockIdx.x / gridDim.x, i1c = items * (blockIdx.x + 1) / gridDim.x;
-      for (int64_t it = i0c; it < i1c;) {
-        const int64_t bidx = it / F;                       // block within the step
-        const int64_t fa = it - bidx * F, fb = imin64(F, fa + (i1c - it));
+      // warp w's items: in every block segment of [i0c, i1c), fragments fa + w, fa + w + 8, ...
+      auto first_of_seg = [&](int64_t it0) -> int64_t {   // this warp's first item at or after segment start it0
+        const int64_t seg_end = imin64(i1c, (it0 / F + 1) * F);
+        return it0 + w < seg_end ? it0 + w : -1;
+      };
+      auto next_item = [&](int64_t it) -> int64_t {
+        const int64_t seg_end = imin64(i1c, (it / F + 1) * F);
+        if (it + NWARP < seg_end) return it + NWARP;
+        for (int64_t s0 = seg_end; s0 < i1c; s0 = imin64(i1c, (s0 / F + 1) * F)) {
+          const int64_t f = first_of_seg(s0);
+          if (f >= 0) return f;
+        }
+        return -1;
+      };
+      auto item_rs = [&](int64_t it) { const int64_t d = dlo + it / F; return (Gn - 1 - d) * G + 1 + (t - d) * NB; };
+      int64_t cur = -1;
+      for (int64_t s0 = i0c; s0 < i1c && cur < 0; s0 = imin64(i1c, (s0 / F + 1) * F)) cur = first_of_seg(s0);
+      if (cur >= 0) {   // the first item's chunks
+        const int64_t f = cur % F;
+        const int nc = (int)imin64(8, a.m - f * 8);
+        load_chunk(item_rs(cur), f * 8, nc, 0, sa);
+        cp_async_commit();
+        load_chunk(item_rs(cur), f * 8, nc, 1, sb);
+        cp_async_commit();
+        load_chunk(item_rs(cur), f * 8, nc, 2, sc);
+        cp_async_commit();
+      }
+      for (int64_t seg0 = i0c; seg0 < i1c; seg0 = imin64(i1c, (seg0 / F + 1) * F)) {
+        const int64_t seg_end = imin64(i1c, (seg0 / F + 1) * F);
+        const int64_t bidx = seg0 / F;
         const int64_t d = dlo + bidx, g = Gn - 1 - d, j = t - d, gi0 = g * G;
         // ---- stage V (compact rows) and T of block (g, j)
         const int nvalid = (int)imax64(0, imin64(G, a.n - 2 - j * NB - gi0 + 1));
@@ -880,34 +943,50 @@ __global__ void __launch_bounds__(256, 1) apply_q2wave_kernel(Q2wArgs a, int64_t
           cp_async16(tb + tcol(kk) + xx, t2 + kk * G + xx, true);
         }
         cp_async_commit();
-        cp_async_wait<0>();
+        cp_async_wait<0>();   // (also completes this warp's window chunks: harmless)
         __syncthreads();
         const double *vcd = reinterpret_cast<const double *>(vc);
         const double *ttd = reinterpret_cast<const double *>(tb);
-        Fr.rs = gi0 + 1 + j * NB;
-        for (int64_t f = fa + w; f < fb; f += NWARP) {
+        // the group counting of full_block<true> expects exactly [chunk 0, chunk 1, chunk 2, next] pending
+        while (cur >= 0 && cur < seg_end) {
+          const int64_t f = cur % F;
+          Fr.rs = gi0 + 1 + j * NB;
           Fr.c0 = f * 8;
           Fr.ncols = (int)imin64(8, a.m - Fr.c0);
           const int cA = 2 * (lane & 3);
           Fr.ok0 = cA < Fr.ncols;
           Fr.ok1 = cA + 1 < Fr.ncols;
-          // the whole window (rows rs .. rs + 94; row 95 is padding)
-          for (int e = lane; e < RING * 8; e += 32) {
-            const int q = e % RING, c = e / RING;
-            const int64_t row = Fr.rs + q;
-            const bool ok = q < W && row < a.n && c < Fr.ncols;
-            cp_async16m(&Fr.Ew[c * LDE + q], ok ? a.E + row + (Fr.c0 + c) * a.lde : a.E, ok);
-          }
-          cp_async_commit();
-          cp_async_wait<0>();
-          __syncwarp();
+          Fr.ch0 = 2 * 32 * sa;
+          Fr.ch1 = 2 * 32 * sb;
+          Fr.ch2 = 2 * 32 * sc;
           Fr.gE = reinterpret_cast<double *>(a.E + Fr.rs + (L.rr >> 1) + (Fr.c0 + cA) * a.lde) + (L.rr & 1);
+          const int64_t nxt = next_item(cur);
+          int64_t nrs = 0, nc0 = 0;
+          int nnc = 0;
+          if (nxt >= 0) {
+            const int64_t nf = nxt % F;
+            nrs = item_rs(nxt);
+            nc0 = nf * 8;
+            nnc = (int)imin64(8, a.m - nc0);
+            load_chunk(nrs, nc0, nnc, 0, sd);
+          }
+          cp_async_commit();   // (possibly empty) keeps the group count uniform
           long long tl = 0;
-          full_block(Fr, L, vcd, ttd, nullptr, tl);
-          __syncwarp();
+          full_block<true>(Fr, L, vcd, ttd, nullptr, tl);
+          __syncwarp();        // every lane is done reading this item's chunks
+          if (nxt >= 0) {
+            load_chunk(nrs, nc0, nnc, 1, sb);
+            cp_async_commit();
+            load_chunk(nrs, nc0, nnc, 2, sc);
+            cp_async_commit();
+            const int s_old = sa;
+            sa = sd;
+            sd = s_old;
+          }
+          cur = nxt;
         }
-        it += fb - fa;
       }
+      cp_async_wait<0>();
     }
     __threadfence();
     grid.sync();
