@@ -157,13 +157,13 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
   const int ga_max = std::max(1, 256 / nb);
   const int kw = ga_max * nb;                       // aggregated width
   const int64_t ldv = n - nb;
-  double2 *Vb0 = (double2 *)c.ws(WS_V, (size_t)2 * ldv * kw * sizeof(double2));
+  double2 *Vb0 = (double2 *)c.ws(WS_V, (size_t)4 * ldv * kw * sizeof(double2));   // V and V T, per parity
   double2 *Y = (double2 *)c.ws(WS_Y, (size_t)kw * m * sizeof(double2));
-  double2 *Y2 = (double2 *)c.ws(WS_Y2, (size_t)kw * m * sizeof(double2));
   double2 *Tg0 = (double2 *)c.ws(WS_TAGG, (size_t)6 * kw * kw * sizeof(double2));
-  if (!Vb0 || !Y || !Y2 || !Tg0) return EIG_ERR_NOMEM;
+  if (!Vb0 || !Y || !Tg0) return EIG_ERR_NOMEM;
   const int64_t ngroups = (K + ga_max - 1) / ga_max;
   auto Vbuf = [&](int par) { return Vb0 + (size_t)par * ldv * kw; };
+  auto VTbuf = [&](int par) { return Vb0 + (size_t)(2 + par) * ldv * kw; };
   auto Tbuf = [&](int par) { return Tg0 + (size_t)par * 3 * kw * kw; };
   // preparation of group gi into buffer par, on the side stream
   auto prep = [&](int64_t gi, int par) -> int {
@@ -202,6 +202,12 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
           rc = zgemm(c, g);
         }
     }
+    if (!rc) {   // V T (so that the main stream's update is one GEMM: E -= (V T) (V^H E))
+      Zgemm g;
+      g.M = s; g.N = w; g.K = w; g.A = Vb; g.lda = ldv; g.B = ga > 1 ? Tg : T + k0 * nb * nb; g.ldb = ga > 1 ? w : nb;
+      g.C = VTbuf(par); g.ldc = ldv;
+      rc = zgemm(c, g);
+    }
     c.stream = keep;
     if (rc) return rc;
     return c.check(cudaEventRecord(c.ev_q1[par], c.side), "q1 prep done");
@@ -218,17 +224,12 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
     const int w = ga * nb;
     const int64_t r0 = (k0 + 1) * nb, s = n - r0;
     const double2 *Vb = Vbuf(par);
-    const double2 *Tuse = ga > 1 ? Tbuf(par) : T + k0 * nb * nb;
-    const int ldt = ga > 1 ? w : nb;
     EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_q1[par], 0), "q1 prep wait"));
     Zgemm g;   // Y = V^H E
     g.opa = OP_C; g.M = w; g.N = m; g.K = s; g.A = Vb; g.lda = ldv; g.B = E + r0; g.ldb = lde; g.C = Y; g.ldc = w;
     EIG_TRY(zgemm(c, g));
-    g = Zgemm();   // Y2 = T Y
-    g.M = w; g.N = m; g.K = w; g.A = Tuse; g.lda = ldt; g.B = Y; g.ldb = w; g.C = Y2; g.ldc = w;
-    EIG_TRY(zgemm(c, g));
-    g = Zgemm();   // E -= V Y2
-    g.M = s; g.N = m; g.K = w; g.A = Vb; g.lda = ldv; g.B = Y2; g.ldb = w; g.C = E + r0; g.ldc = lde;
+    g = Zgemm();   // E -= (V T) Y
+    g.M = s; g.N = m; g.K = w; g.A = VTbuf(par); g.lda = ldv; g.B = Y; g.ldb = w; g.C = E + r0; g.ldc = lde;
     g.alpha = -1.0; g.beta = 1.0;
     EIG_TRY(zgemm(c, g));
     EIG_TRY(c.check(cudaEventRecord(c.ev_q1[2 + par], c.stream), "q1 gemms done"));
