@@ -236,3 +236,34 @@ def test_hotpath_parity(n, nb, g, m):
     Eh = np.zeros((n, m), complex, order="F")
     s.hotpath_host(np.asfortranarray(A), V2, tau2, np.asfortranarray(L), np.asfortranarray(Z), Eh)
     assert _rel(Eh, E_o) < TOL
+
+
+@gpu
+def test_apply_q2_per_fragment_kernels_subprocess():
+    """EIG_Q2_WAVE=0 selects the per-fragment Q2 kernels (apply_q2w_kernel for
+    >= 3 fragments per SM, apply_q2s_kernel below); the switch is read once per
+    process, so the check runs in a child process (same oracle comparison)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle, synth
+from paper_1207_1773_b200 import Solver, colmajor, empty_colmajor
+s = Solver(0, nb=64, q2_group=32)
+for n, m in [(517, 130), (300, 5000), (129, 1333)]:
+    V2, tau2 = synth.synthetic_v2(n, 64, 6)
+    Z = synth.real_orthonormalish(n, m, 6)
+    dE = empty_colmajor(n, m)
+    s.apply_q2(torch.from_numpy(V2).cuda(), torch.from_numpy(tau2).cuda(), dE, Z=colmajor(Z, torch.device("cuda:0")))
+    cols = sorted({0, 1, 8, m // 2, m - 1})
+    ref = oracle.apply_q2(V2, tau2, 64, Z[:, cols].astype(complex))
+    got = dE.cpu().numpy()[:, cols]
+    err = np.max(np.abs(got - ref)) / np.max(np.abs(ref))
+    assert err < 1e-11, (n, m, err)
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EIG_Q2_WAVE="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
