@@ -854,15 +854,18 @@ __device__ __forceinline__ int64_t wave_J(const Q2wArgs &a, int64_t g) { return 
 // first chunk as soon as the item starts; the next item's other two chunks go
 // into the slots of the finished item, so the window loads overlap compute.
 constexpr int LDWV = 129;   // 4 chunks of 32 rows + 1 (odd: conflict-free)
-constexpr int OFF_WAVE_WIN = OFF_T + T_STAGE;   // after V / T stage 0
-static_assert(OFF_WAVE_WIN + 8 * 8 * LDWV <= OFF_BAR, "wave windows must fit the q2w shared-memory size");
+constexpr int WAVE_WARPS = 10;                       // 2-3 per SM sub-partition; items are claimed dynamically
+constexpr int OFF_WAVE_T = VC_STAGE;                 // layout: V | T | windows
+constexpr int OFF_WAVE_WIN = OFF_WAVE_T + T_STAGE;
+static_assert(OFF_WAVE_WIN + WAVE_WARPS * 8 * LDWV <= OFF_BAR, "wave windows must fit the q2w shared-memory size");
 
-__global__ void __launch_bounds__(256, 1) apply_q2wave_kernel(Q2wArgs a, int64_t T) {
+__global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArgs a, int64_t T) {
   namespace cg = cooperative_groups;
-  constexpr int TH = 256, NWARP = TH / 32;
+  constexpr int TH = 32 * WAVE_WARPS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // layout: V (stage 0) | (unused) | T (stage 0) | 8 windows of 8 x LDWV
-  double2 *vc = vc_buf(0), *tb = t_buf(0);
+  __shared__ int s_claim;   // next unclaimed item of this CTA's share of the step
+  // layout: V | T | one window of 8 x LDWV per warp
+  double2 *vc = q2w_sm, *tb = q2w_sm + OFF_WAVE_T;
   double2 *win0 = q2w_sm + OFF_WAVE_WIN;
   for (int e = threadIdx.x; e < VC_STAGE; e += TH) vc[e] = czero();
   __syncthreads();
@@ -898,23 +901,18 @@ __global__ void __launch_bounds__(256, 1) apply_q2wave_kernel(Q2wArgs a, int64_t
     if (nblk > 0) {
       const int64_t items = nblk * F;
       const int64_t i0c = items * blockIdx.x / gridDim.x, i1c = items * (blockIdx.x + 1) / gridDim.x;
-      // warp w's items: in every block segment of [i0c, i1c), fragments fa + w, fa + w + 8, ...
-      auto first_of_seg = [&](int64_t it0) -> int64_t {   // this warp's first item at or after segment start it0
-        const int64_t seg_end = imin64(i1c, (it0 / F + 1) * F);
-        return it0 + w < seg_end ? it0 + w : -1;
-      };
-      auto next_item = [&](int64_t it) -> int64_t {
-        const int64_t seg_end = imin64(i1c, (it / F + 1) * F);
-        if (it + NWARP < seg_end) return it + NWARP;
-        for (int64_t s0 = seg_end; s0 < i1c; s0 = imin64(i1c, (s0 / F + 1) * F)) {
-          const int64_t f = first_of_seg(s0);
-          if (f >= 0) return f;
-        }
-        return -1;
+      // items are claimed in order (block-major) from a shared counter, so the
+      // warps of the busier sub-partitions simply take fewer of them
+      if (threadIdx.x == 0) s_claim = 0;
+      __syncthreads();
+      auto claim = [&]() -> int64_t {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(&s_claim, 1);
+        v = __shfl_sync(0xffffffffu, v, 0);
+        return i0c + v < i1c ? i0c + v : -1;
       };
       auto item_rs = [&](int64_t it) { const int64_t d = dlo + it / F; return (Gn - 1 - d) * G + 1 + (t - d) * NB; };
-      int64_t cur = -1;
-      for (int64_t s0 = i0c; s0 < i1c && cur < 0; s0 = imin64(i1c, (s0 / F + 1) * F)) cur = first_of_seg(s0);
+      int64_t cur = claim();
       if (cur >= 0) {   // the first item's chunks
         const int64_t f = cur % F;
         const int nc = (int)imin64(8, a.m - f * 8);
@@ -960,7 +958,7 @@ __global__ void __launch_bounds__(256, 1) apply_q2wave_kernel(Q2wArgs a, int64_t
           Fr.ch1 = 2 * 32 * sb;
           Fr.ch2 = 2 * 32 * sc;
           Fr.gE = reinterpret_cast<double *>(a.E + Fr.rs + (L.rr >> 1) + (Fr.c0 + cA) * a.lde) + (L.rr & 1);
-          const int64_t nxt = next_item(cur);
+          const int64_t nxt = claim();
           int64_t nrs = 0, nc0 = 0;
           int nnc = 0;
           if (nxt >= 0) {
@@ -1038,7 +1036,7 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
     }
     const int gridw = ctx.num_sms;
     void *args[] = {&a, &T};
-    EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)apply_q2wave_kernel, dim3(gridw), dim3(256), args, smem,
+    EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)apply_q2wave_kernel, dim3(gridw), dim3(32 * WAVE_WARPS), args, smem,
                                                   ctx.stream), "q2wave launch"));
     return ctx.launched("apply_q2wave_kernel");
   }
