@@ -35,6 +35,7 @@ struct HbArgs {
   double2 *V2, *tau2;     // outputs (V2 layout)
   const int64_t *off;     // slot offsets per step j
   int *progress;          // [n] steps completed per sweep
+  int *progressA;         // [n] steps whose reflector outputs (V2, tau2, target column) are stored
   unsigned long long *prof;  // optional: CTA 0 phase cycles [16..21] (wait, refl, a, b, c, flag)
 };
 
@@ -80,13 +81,19 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       tm = now;
     }
   };
-  // sweep i-1 must have finished step j+2 before task (i, j) touches D_j / Cblk_j
+  // Before task (i, j) touches D_j / Cblk_j, sweep i-1 must have finished its
+  // steps <= j+1; of its step j+2 only the target column matters (the single
+  // element M(r0_{j+2}, c_{j+2}) = beta is the one overlap with task (i, j)'s
+  // region), and that is stored right after its reflector, so the
+  // sweep-to-sweep lag is two steps plus a reflector instead of three steps.
   auto wait_prev = [&](int64_t i, int64_t j) {
     if (i > 0 && tid == 0) {
       const int64_t prev = i - 1;
-      const int64_t jprev_max = (n - 2 - prev) / nb;
-      const int need = (int)imin64(j + 3, jprev_max + 1);
+      const int64_t nprev = (n - 2 - prev) / nb + 1;
+      const int need = (int)imin64(j + 2, nprev), need_a = (int)imin64(j + 3, nprev);
       while (ld_acquire_i32(a.progress + prev) < need) {
+      }
+      while (ld_acquire_i32(a.progressA + prev) < need_a) {
       }
     }
     __syncthreads();
@@ -160,6 +167,11 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
         for (int t = tid; t < nb; t += HT) a.V2[slot * nb + t] = (t < len) ? sv[t] : czero();
         if (tid == 0) a.tau2[slot] = tau;
         for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta : czero();
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        st_release_i32(a.progressA + i, (int)(j + 1));
       }
       // ---- (a) on the previous bulge (shared memory only): f, then store
       if (na > 0) {
@@ -286,9 +298,9 @@ int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d,
   if (nb > 64) return EIG_ERR_NOTIMPL;
   const int ldab = 2 * nb + 2;
   double2 *AB = (double2 *)ctx.ws(WS_BAND, (size_t)ldab * n * sizeof(double2));
-  int *prog = (int *)ctx.ws(WS_HBPROG, (size_t)n * sizeof(int));
+  int *prog = (int *)ctx.ws(WS_HBPROG, (size_t)2 * n * sizeof(int));   // progress | progressA
   if (!AB || !prog) return EIG_ERR_NOMEM;
-  EIG_TRY(ctx.check(cudaMemsetAsync(prog, 0, (size_t)n * sizeof(int), ctx.stream), "memset progress"));
+  EIG_TRY(ctx.check(cudaMemsetAsync(prog, 0, (size_t)2 * n * sizeof(int), ctx.stream), "memset progress"));
   const int64_t total = n * (int64_t)ldab;
   band_in_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 8LL * ctx.num_sms), 256, 0, ctx.stream>>>(
       n, nb, A, lda, AB, ldab);
@@ -303,9 +315,11 @@ int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d,
     a.tau2 = tau2;
     a.off = d_off;
     a.progress = prog;
+    a.progressA = prog + n;
     a.prof = ctx.q2_prof;
     const int64_t J = (n - 2) / nb + 1;   // steps of sweep 0
-    const int P = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, std::min<int64_t>(n - 1, J / 3 + 2)));
+    // ~J / 2.3 sweeps are active at once (lag of two steps plus a reflector)
+    const int P = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, std::min<int64_t>(n - 1, J / 2 + 2)));
     void *args[] = {&a};
     const size_t smem = ((size_t)64 * LDD + 2 * 64 * 64 + 64) * sizeof(double2);
     static bool attr = false;
