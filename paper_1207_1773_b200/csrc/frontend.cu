@@ -155,14 +155,33 @@ int potrf_lower(Ctx &c, int64_t n, double2 *B, int64_t ldb, int64_t *d_info) {
     c.stream = keep;
     return rc;
   };
-  EIG_TRY(factor_block(0, c.stream));
-  for (int64_t k = 0; k < n; k += FB) {
-    const int b = (int)std::min<int64_t>(FB, n - k);
+  // outer blocks of PB = 128 columns (two 64-column diagonal factorisations
+  // each), so the trailing update has K = 128
+  constexpr int PB = 2 * FB;
+  auto factor_outer = [&](int64_t k, cudaStream_t st) -> int {
+    const int b = (int)std::min<int64_t>(PB, n - k);
+    EIG_TRY(factor_block(k, st));
+    if (b <= FB) return 0;
+    // second sub-column (rows >= k + FB) -= L21a L21a[0:b-FB]^H, then its factorisation
+    Zgemm g;
+    g.opb = OP_C; g.lower_c = 2; g.M = n - k - FB; g.N = b - FB; g.K = FB; g.A = B + (k + FB) + k * ldb; g.lda = ldb;
+    g.B = B + (k + FB) + k * ldb; g.ldb = ldb; g.C = B + (k + FB) + (k + FB) * ldb; g.ldc = ldb;
+    g.alpha = -1.0; g.beta = 1.0;
+    const cudaStream_t keep = c.stream;
+    c.stream = st;
+    const int rc = zgemm(c, g);
+    c.stream = keep;
+    EIG_TRY(rc);
+    return factor_block(k + FB, st);
+  };
+  EIG_TRY(factor_outer(0, c.stream));
+  for (int64_t k = 0; k < n; k += PB) {
+    const int b = (int)std::min<int64_t>(PB, n - k);
     const int64_t s = n - k - b;
     if (s <= 0) break;
     if (k > 0) EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_join, 0), "potrf join"));
     double2 *A11 = B + k + k * ldb, *L21 = A11 + b, *A22 = A11 + b + b * ldb;
-    const int b2 = (int)std::min<int64_t>(FB, s);
+    const int b2 = (int)std::min<int64_t>(PB, s);
     Zgemm g;
     if (s > b2) {
       // (i) the next block column: A22[:, 0:b2] -= L21 L21[0:b2]^H (rows >= cols)
@@ -171,7 +190,7 @@ int potrf_lower(Ctx &c, int64_t n, double2 *B, int64_t ldb, int64_t *d_info) {
       EIG_TRY(zgemm(c, g));
       EIG_TRY(c.check(cudaEventRecord(c.ev_fork, c.stream), "potrf fork"));
       EIG_TRY(c.check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "potrf fork wait"));
-      EIG_TRY(factor_block(k + b, c.side));
+      EIG_TRY(factor_outer(k + b, c.side));
       EIG_TRY(c.check(cudaEventRecord(c.ev_join, c.side), "potrf join rec"));
       // (ii) the rest of the trailing lower triangle
       g = Zgemm();
@@ -183,7 +202,7 @@ int potrf_lower(Ctx &c, int64_t n, double2 *B, int64_t ldb, int64_t *d_info) {
       g.opb = OP_C; g.lower_c = 1; g.M = s; g.N = s; g.K = b; g.A = L21; g.lda = ldb; g.B = L21; g.ldb = ldb;
       g.C = A22; g.ldc = ldb; g.alpha = -1.0; g.beta = 1.0;
       EIG_TRY(zgemm(c, g));
-      EIG_TRY(factor_block(k + b, c.stream));
+      EIG_TRY(factor_outer(k + b, c.stream));
       break;
     }
   }
