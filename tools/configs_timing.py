@@ -42,5 +42,5 @@ def run(n, frac):
 
 
 if __name__ == "__main__":
-    for n, fr in [(2000, 1.0), (5000, 0.10), (5000, 0.25), (10000, 1.0), (10000, 0.10), (20000, 0.10), (20000, 0.5)]:
+    for n, fr in [(2000, 1.0), (5000, 0.10), (5000, 0.25), (10000, 1.0), (10000, 0.10), (20000, 0.10), (20000, 0.5), (20000, 1.0)]:
         run(n, fr)
