@@ -14,10 +14,18 @@
 // barrier: every CTA publishes (||x_local||^2, conj(P[:,j])^H P[:,l] partial
 // dots, row j) and every CTA reduces all records in a fixed order (so the
 // result is deterministic), computes beta/tau/v locally and updates its rows.
+// Panels short enough for one thread-block cluster (CL = true: at most
+// EIG_PANEL_CLUSTER CTAs; opt-in) keep the records in each CTA's own shared
+// memory and exchange them through distributed shared memory; the split
+// barrier.cluster arrive (after publishing) / wait (before reducing) replaces
+// the L2 counter.  These are the late panels, whose latency the shrinking
+// trailing update no longer hides.
 // Because v = (a_j - beta e_j)/(alpha - beta), v^H P[:,l] follows from the raw
 // dots a_j^H P[:,l] without a second reduction.
 #include <algorithm>
 #include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -59,6 +67,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // so the trailing-column update and the T column
 //   T[0:j, j] = -tau_j T[0:j, 0:j] y   (zlarft, forward/columnwise)
 // need no second reduction.
+template <bool CL>
 __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double2 sm[];
   const int nb = a.nb, R = a.R, G = a.G;
@@ -66,11 +75,12 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   const int recw = 2 * nb;
   double2 *sTau = sm;               // [nb]
   double2 *sRow = sTau + nb;        // [nb]   row j (owner's record)
-  double2 *sS = sRow + nb;          // [nb]   reduced s_l
+  double2 *sS = sRow + nb;          // [nb]   (unused slot; keeps the layout)
   double2 *sW = sS + nb;            // [nb]   w_l / y_i
   double2 *sY = sW + nb;            // [nb]   y_i (T column)
   double2 *sPart = sY + nb;         // [4][64]
-  double2 *sP = sPart + NQ * 64;    // [nb][R], column l at sP + l*R
+  double2 *sRec = sPart + NQ * 64;  // CL: [2][recw] this CTA's records
+  double2 *sP = sRec + (CL ? 2 * recw : 0);   // [nb][R], column l at sP + l*R
   // CTA 0: T (nb x nb, column stride R) in the unused tail rows R0..R-1 of sP
   double2 *sT = sP + a.R0;
   __shared__ double2 s_tau, s_scale;
@@ -119,7 +129,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     }
     sPart[rq * 64 + cl] = acc;
     __syncthreads();
-    double2 *out = a.rec + ((int64_t)(jn & 1) * G + g) * recw;
+    double2 *out = CL ? sRec + (jn & 1) * recw : a.rec + ((int64_t)(jn & 1) * G + g) * recw;
     if (tid < nb) {
       double2 t = sPart[tid];
 #pragma unroll
@@ -131,53 +141,79 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
         for (int q = 1; q < NQ; q++) c1 = cadd(c1, sPart[q * 64 + jp]);
         t = csub(t, cmul(ctau, cmul(sW[tid], c1)));
       }
-      __stcg(&out[tid], t);
+      if (CL) out[tid] = t;
+      else __stcg(&out[tid], t);
     }
     if (jn >= row0 && jn < row0 + rows)
       for (int l = tid; l < nb; l += PT) {
         double2 pv = sP[l * LR + (jn - row0)];
         if (corr && l > jn) pv = csub(pv, cmul(ctau, cmul(sP[(jn - 1) * LR + (jn - row0)], sW[l])));
-        __stcg(&out[nb + l], pv);
+        if (CL) out[nb + l] = pv;
+        else __stcg(&out[nb + l], pv);
       }
     // the barrier orders every thread's record stores before thread 0's
     // release increment (fence cumulativity): one release instead of a
-    // membar in every thread
+    // membar in every thread; it also keeps the bulk update below from
+    // overwriting row jn before it is recorded
     __syncthreads();
-    if (tid == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
+    if (CL) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    else if (tid == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
+  };
+  // record q (CTA q) of the exchange for column j
+  auto rec_of = [&](int q, int j) -> const double2 * {
+    if (CL) return cooperative_groups::this_cluster().map_shared_rank(sRec + (j & 1) * recw, q);
+    return a.rec + ((int64_t)(j & 1) * G + q) * recw;
   };
 
   if (a.nref > 0) publish(0, false, czero());
   mark(4);
   for (int j = 0; j < a.nref; j++) {
-    if (tid == 0) {
-      const unsigned long long target = a.epoch0 + (unsigned long long)G * (j + 1);
-      while (ld_acquire_u64(a.cnt) < target) {
+    if (CL) {
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+      if (tid == 0) {
+        const unsigned long long target = a.epoch0 + (unsigned long long)G * (j + 1);
+        while (ld_acquire_u64(a.cnt) < target) {
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
     mark(0);
-    const double2 *recs = a.rec + (int64_t)(j & 1) * G * recw;
     {
       // s_l for l >= j (every CTA: norm, w_l); s_i for i < j only feed T (CTA 0)
       double2 acc = czero();
+      // the loads of a batch are issued together (one L2 round trip per 4
+      // records instead of one per record); the sum keeps the order q = rq,
+      // rq + NQ, ... so the result is unchanged
       if (cl < nb && (cl >= j || g == 0))
-        for (int q = rq; q < G; q += NQ) acc = cadd(acc, __ldcg(&recs[(int64_t)q * recw + cl]));
+        for (int q0 = rq; q0 < G; q0 += 4 * NQ) {
+          double2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int q = q0 + u * NQ;
+            v[u] = q < G ? (CL ? rec_of(q, j)[cl] : __ldcg(rec_of(q, j) + cl)) : czero();
+          }
+#pragma unroll
+          for (int u = 0; u < 4; u++)
+            if (q0 + u * NQ < G) acc = cadd(acc, v[u]);
+        }
       sPart[rq * 64 + cl] = acc;
       const int owner = j < a.R0 ? 0 : 1 + (j - a.R0) / R;
-      if (tid < nb) sRow[tid] = __ldcg(&recs[(int64_t)owner * recw + nb + tid]);
+      if (tid < nb) sRow[tid] = CL ? rec_of(owner, j)[nb + tid] : __ldcg(rec_of(owner, j) + nb + tid);
     }
     __syncthreads();
+    // thread l < nb keeps the reduced s_l in a register; thread j (which holds
+    // ||x||^2 and has row j) forms beta / tau / scale: one CTA barrier fewer
+    double2 sl = czero();
     if (tid < nb) {
-      double2 t = sPart[tid];
+      sl = sPart[tid];
 #pragma unroll
-      for (int q = 1; q < NQ; q++) t = cadd(t, sPart[q * 64 + tid]);
-      sS[tid] = t;
+      for (int q = 1; q < NQ; q++) sl = cadd(sl, sPart[q * 64 + tid]);
     }
-    __syncthreads();
     mark(1);
-    if (tid == 0) {
+    if (tid == j) {
       const double2 alpha = sRow[j];
-      const double xnorm2 = sS[j].x;
+      const double xnorm2 = sl.x;
       double2 tau, scale;
       double beta;
       if (xnorm2 == 0.0 && alpha.y == 0.0) {
@@ -201,8 +237,8 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     const double2 tau = s_tau, scale = s_scale;
     const double2 ctau = cconj(tau);
     if (tid < nb) {
-      if (tid > j) sW[tid] = cadd(sRow[tid], cmulc(scale, sS[tid]));                  // w_l = v^H P[:,l]
-      else if (tid < j) sY[tid] = cadd(cconj(sRow[tid]), cmul(scale, cconj(sS[tid])));  // y_i = V_i^H v
+      if (tid > j) sW[tid] = cadd(sRow[tid], cmulc(scale, sl));                  // w_l = v^H P[:,l]
+      else if (tid < j) sY[tid] = cadd(cconj(sRow[tid]), cmul(scale, cconj(sl)));  // y_i = V_i^H v
     }
     for (int r = tid; r < rows; r += PT) {
       const int64_t grow = row0 + r;
@@ -282,6 +318,11 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   }
   if (prof)
     for (int k = 0; k < 6; k++) atomicAdd(&a.prof[8 + k], (unsigned long long)tacc[k]);
+  if (CL) {
+    // no CTA leaves while another may still read its records
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
 }
 
 // Explicit unit-lower V (s x nb) from the he2hb storage of one panel.
@@ -318,15 +359,58 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
     const char *e = getenv("EIG_PANEL_CTAS");
     return e ? atoi(e) : 0;
   }();
+  // cluster path (opt-in): panels whose rows fit in at most EIG_PANEL_CLUSTER
+  // CTAs (<= 8 portable, up to 16 non-portable; default 0 = off).  Measured
+  // he2hb n = 2000 / 10^4: off 15.5 / 241.3 ms, 4: 15.9 / 241.7, 8: 16.5 /
+  // 242.3, 16: 15.2 / 242.8 -- the ~7 us per column is not the exchange.
+  static const int clmax = [] {
+    const char *e = getenv("EIG_PANEL_CLUSTER");
+    return std::min(16, std::max(0, e ? atoi(e) : 0));
+  }();
+  const int recw = 2 * nb;
+  const int words = 220 * 1024 / (int)sizeof(double2);
+  const int64_t rows_nb = (pn + nb - 1) / nb;
+  {
+    const int rmax_cl = (words - 5 * nb - NQ * 64 - 2 * recw) / nb - 1;
+    const int64_t gmin = (pn + nb + rmax_cl - 1) / rmax_cl;
+    if (gmin <= clmax) {
+      int G = (int)std::max<int64_t>(gmin, std::min<int64_t>(clmax, rows_nb));
+      int R = (int)std::max<int64_t>((pn + nb + G - 1) / G, nb);
+      G = (int)((pn + nb + R - 1) / R);
+      PanelArgs a{P, lda, pn, nb, nref, R, R - nb, G, tau, T, vout, vout2, ldv, nullptr, nullptr, 0, ctx.q2_prof};
+      const size_t smem = ((size_t)5 * nb + NQ * 64 + 2 * recw + (size_t)nb * (R | 1)) * sizeof(double2);
+      static bool attr_cl = false;
+      if (!attr_cl) {
+        EIG_TRY(ctx.check(cudaFuncSetAttribute(panel_qr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               220 * 1024), "panel attr"));
+        EIG_TRY(ctx.check(cudaFuncSetAttribute(panel_qr_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                          "panel cluster attr"));
+        attr_cl = true;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(PT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      EIG_TRY(ctx.check(cudaLaunchKernelEx(&cfg, panel_qr_kernel<true>, a), "panel_qr_kernel<cluster> launch"));
+      return ctx.launched("panel_qr_kernel");
+    }
+  }
   const int gmax = gmax_env > 0 ? std::min(gmax_env, ctx.num_sms) : std::min(32, ctx.num_sms);
-  int G = (int)std::min<int64_t>(gmax, (pn + nb - 1) / nb);
+  int G = (int)std::min<int64_t>(gmax, rows_nb);
   G = std::max(G, 1);
-  const int rmax = (int)((220 * 1024 / sizeof(double2) - 5 * nb - NQ * 64) / nb) - 1;   // rows that fit on chip (odd stride)
+  const int rmax = (words - 5 * nb - NQ * 64) / nb - 1;   // rows that fit on chip (odd stride)
   G = std::max<int64_t>(G, (pn + nb + rmax - 1) / rmax);
   int R = (int)((pn + nb + G - 1) / G);   // CTA 0 holds R - nb rows
   R = std::max(R, nb);
   G = (int)((pn + nb + R - 1) / R);
-  const int recw = 2 * nb;
   const size_t smem = ((size_t)5 * nb + NQ * 64 + (size_t)nb * (R | 1)) * sizeof(double2);
   if (smem > 220 * 1024) return EIG_ERR_NOTIMPL;  // panel too tall for on-chip residency (n > ~20000 at nb=64)
   PanelArgs a;
@@ -350,12 +434,12 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   if (!a.rec || !a.cnt) return EIG_ERR_NOMEM;
   static bool attr = false;
   if (!attr) {
-    EIG_TRY(ctx.check(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024),
-                      "panel attr"));
+    EIG_TRY(ctx.check(cudaFuncSetAttribute(panel_qr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           220 * 1024), "panel attr"));
     attr = true;
   }
   void *args[] = {&a};
-  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel, dim3(G), dim3(PT), args, smem, stream),
+  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel<false>, dim3(G), dim3(PT), args, smem, stream),
                     "panel_qr_kernel launch"));
   ctx.bar_epoch += (unsigned long long)G * nref;   // arrivals this launch performs
   return ctx.launched("panel_qr_kernel");

@@ -267,3 +267,39 @@ print("ok")
     env = dict(os.environ, EIG_Q2_WAVE="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@gpu
+def test_he2hb_cluster_panel_subprocess():
+    """EIG_PANEL_CLUSTER=c runs the panels that fit in c CTAs as one
+    thread-block cluster (records exchanged through distributed shared
+    memory); the switch is read once per process, so the oracle comparison
+    runs in child processes (c = 8 portable, c = 16 non-portable)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle, synth
+from paper_1207_1773_b200 import Solver, colmajor, num_panels
+for n, nb in [(517, 64), (300, 32), (1100, 64), (97, 8)]:
+    s = Solver(0, nb=nb)
+    A = synth.rand_hermitian(n, 4)
+    dA = colmajor(A, torch.device("cuda:0"))
+    tau, T = s.he2hb(dA)
+    A_o, tau_o = oracle.he2hb(A, nb)
+    r, c = np.indices((n, n))
+    low = r >= c
+    Ag = dA.cpu().numpy()
+    err = np.max(np.abs(Ag[low] - A_o[low])) / np.max(np.abs(A_o[low]))
+    K = num_panels(n, nb)
+    et = np.max(np.abs(tau.cpu().numpy()[:K * nb] - tau_o[:K * nb]))
+    assert err < 1e-11 * max(1, n / 256) and et < 1e-11 * max(1, n / 256), (n, nb, err, et)
+    s.close()
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for c in ("8", "16"):
+        env = dict(os.environ, EIG_PANEL_CLUSTER=c)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0 and "ok" in r.stdout, c + ": " + r.stdout + r.stderr
