@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   const int recw = 2 * nb;
   double2 *sTau = sm;               // [nb]
   double2 *sRow = sTau + nb;        // [nb]   row j (owner's record)
-  double2 *sS = sRow + nb;          // [nb]   (unused slot; keeps the layout)
+  double2 *sS = sRow + nb;          // [nb]   conj(tau) w_l for the column updates
   double2 *sW = sS + nb;            // [nb]   w_l / y_i
   double2 *sY = sW + nb;            // [nb]   y_i (T column)
   double2 *sPart = sY + nb;         // [4][64]
@@ -237,7 +237,10 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     const double2 tau = s_tau, scale = s_scale;
     const double2 ctau = cconj(tau);
     if (tid < nb) {
-      if (tid > j) sW[tid] = cadd(sRow[tid], cmulc(scale, sl));                  // w_l = v^H P[:,l]
+      if (tid > j) {
+        sW[tid] = cadd(sRow[tid], cmulc(scale, sl));                  // w_l = v^H P[:,l]
+        sS[tid] = cmul(cconj(tau), sW[tid]);                          // conj(tau) w_l
+      }
       else if (tid < j) sY[tid] = cadd(cconj(sRow[tid]), cmul(scale, cconj(sl)));  // y_i = V_i^H v
     }
     for (int r = tid; r < rows; r += PT) {
@@ -263,23 +266,25 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       publish(j + 1, true, ctau);
       mark(4);
     }
-    // bulk update of the remaining trailing columns (overlaps the other CTAs' exchange)
+    // bulk update of the remaining trailing columns (overlaps the other CTAs'
+    // exchange).  One work item = one row x up to 16 columns: v[r] is loaded
+    // once per item and a warp touches 32 consecutive rows of a column
+    // (conflict-free); the loop is bound by shared-memory bandwidth
     {
       const int lo = la ? j + 2 : j + 1;
       const int c = nb - lo;
       if (c > 0) {
-        const int tpc = PT / c;                         // threads per column
-        const int lc = tid / tpc, part = tid - lc * tpc;
-        if (lc < c) {
-          const int l = lo + lc;
-          const int rb = (int)((int64_t)rows * part / tpc), re = (int)((int64_t)rows * (part + 1) / tpc);
-          const double2 cw = cmul(ctau, sW[l]);
-          double2 *pl = sP + l * LR;
-          for (int r = rb; r < re; r++) {
-            const int64_t grow = row0 + r;
-            if (grow < j) continue;
-            const double2 v = (grow == j) ? make_double2(1.0, 0.0) : vj[r];
-            pl[r] = csub(pl[r], cmul(v, cw));
+        constexpr int CH = 16;
+        const int nch = (c + CH - 1) / CH;
+        const int rstart = (int)max((int64_t)0, (int64_t)j - row0);   // rows at or below j
+        const int nr = max(0, rows - rstart);
+        for (int it = tid; it < nr * nch; it += PT) {
+          const int ch = it / nr, r = rstart + (it - ch * nr);
+          const double2 v = (row0 + r == j) ? make_double2(1.0, 0.0) : vj[r];
+          const int l0 = lo + ch * CH, l1 = min(nb, l0 + CH);
+          for (int l = l0; l < l1; l++) {
+            double2 *pl = sP + l * LR;
+            pl[r] = csub(pl[r], cmul(v, sS[l]));
           }
         }
       }
