@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       sl = sPart[tid];
 #pragma unroll
       for (int q = 1; q < NQ; q++) sl = cadd(sl, sPart[q * 64 + tid]);
+      sPart[tid] = sl;   // every thread forms w_{j+1} from it below
     }
     mark(1);
     if (tid == j) {
@@ -243,25 +244,27 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       }
       else if (tid < j) sY[tid] = cadd(cconj(sRow[tid]), cmul(scale, cconj(sl)));  // y_i = V_i^H v
     }
-    for (int r = tid; r < rows; r += PT) {
-      const int64_t grow = row0 + r;
-      if (grow > j) sP[j * LR + r] = cmul(sP[j * LR + r], scale);
-      else if (grow == j) sP[j * LR + r] = make_double2(s_beta, 0.0);
-    }
-    __syncthreads();
+    // scale column j into v and, with look-ahead, apply H_j to the next pivot
+    // column in the same pass (same rows per thread: no barrier between)
     const double2 *vj = sP + j * LR;
     const bool la = (j + 1 < a.nref);
-    if (la) {
-      // look-ahead: the next pivot column first, then publish it
-      const double2 cw = cmul(ctau, sW[j + 1]);
-      double2 *pl = sP + (j + 1) * LR;
-      for (int r = tid; r < rows; r += PT) {
-        const int64_t grow = row0 + r;
-        if (grow < j) continue;
-        const double2 v = (grow == j) ? make_double2(1.0, 0.0) : vj[r];
-        pl[r] = csub(pl[r], cmul(v, cw));
+    const double2 cw = la ? cmul(ctau, cadd(sRow[j + 1], cmulc(scale, sPart[j + 1]))) : czero();
+    double2 *pn1 = sP + (j + 1) * LR;
+    for (int r = tid; r < rows; r += PT) {
+      const int64_t grow = row0 + r;
+      if (grow < j) continue;
+      double2 v;
+      if (grow > j) {
+        v = cmul(sP[j * LR + r], scale);
+        sP[j * LR + r] = v;
+      } else {
+        sP[j * LR + r] = make_double2(s_beta, 0.0);
+        v = make_double2(1.0, 0.0);
       }
-      __syncthreads();
+      if (la) pn1[r] = csub(pn1[r], cmul(v, cw));
+    }
+    __syncthreads();
+    if (la) {
       mark(3);
       publish(j + 1, true, ctau);
       mark(4);
