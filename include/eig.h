@@ -53,8 +53,16 @@ typedef struct eig_ctx *eig_handle;
 
 typedef struct {
   int device;        /* CUDA ordinal for this process                              */
-  int nb;            /* band half-width = he2hb panel width; 0 -> 64; 1..64 allowed */
-  int q2_group;      /* sweeps per grouped Q2 block (g); 0 -> 32; 1..64 allowed     */
+  int nb;            /* band half-width = he2hb panel width; 0 -> 64.  eig_init
+                        accepts 1..64 (he2hb, hb2st, Q1, trsm work for all); the
+                        grouped Q2 back-transform (eig_apply_q2, eig_hotpath,
+                        eig_solve_gen) needs an even nb >= 4 and returns
+                        EIG_ERR_NOTIMPL otherwise                                   */
+  int q2_group;      /* sweeps per grouped Q2 block (g); 0 -> min(32, 4*floor((nb+1)/4))
+                        (0 for nb <= 2: no Q2).  Explicit values must satisfy
+                        4 <= g <= 32, g % 4 == 0, g <= nb + 1 (else eig_init
+                        returns -2).  nb = 64 with g = 32 selects the wavefront
+                        kernel; other shapes the generic grouped kernel          */
   void *stream;      /* cudaStream_t to order with; NULL = legacy default stream    */
 } eig_config;
 
@@ -139,15 +147,19 @@ int eig_trsm_lh(eig_handle h, int64_t n, const void *L, int64_t ldl, void *E, in
  * on the m selected eigenvector columns (a9: the caller passes the m columns
  * of the tridiagonal eigenvectors it wants, il..iu).
  *   A    n x n (lda), Hermitian lower; destroyed (he2hb output).
- *   tau1 K*nb, T1 K*nb*nb complex128 outputs (device; when EIG_HOST_BUFFERS
- *        is set they may be NULL and stay in library workspace).
+ *   tau1 K*nb, T1 K*nb*nb complex128: he2hb outputs (device).  With
+ *        EIG_HOST_BUFFERS they are host pointers and may be NULL (then they
+ *        stay in library workspace); if non-NULL they receive tau1 / T1.
+ *        With EIG_SKIP_HE2HB, T1 is an INPUT (the T factors of the he2hb
+ *        output held in A) and must not be NULL when K > 0 (else -6).
  *   V2, tau2  Q2 reflectors (layout above).
  *   L    n x n lower (ldl).   Z n x m real (ldz).   E n x m complex128 (lde) out.
  * flags: EIG_HOST_BUFFERS -> A, V2, tau2, L, Z, E are HOST pointers (pinned
  * recommended); the call copies the lower triangle of A to the device,
  * copies V2, tau2, Z and the lower triangle of L on a transfer stream while
  * he2hb runs, copies each final 256-row block of E back while the triangular
- * solve works on the blocks above it, and returns synchronously.  EIG_SKIP_HE2HB / EIG_SKIP_BT select a part. */
+ * solve works on the blocks above it, and returns synchronously; the host A
+ * is not modified in that mode.  EIG_SKIP_HE2HB / EIG_SKIP_BT select a part. */
 int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void *T1, const void *V2,
                 const void *tau2, const void *L, int64_t ldl, const double *Z, int64_t ldz, void *E, int64_t lde,
                 int64_t m, unsigned flags);

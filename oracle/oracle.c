@@ -52,29 +52,53 @@ static double abs2(zc z) { return creal(z) * creal(z) + cimag(z) * cimag(z); }
  * beta (real), tau and v = (1, x/(alpha-beta)) such that
  *   H^H (alpha; x) = (beta; 0),  H = I - tau v v^H.
  * x is overwritten with v[1..m-1]; returns beta in *beta, tau in *tau.
- * tau = 0 (H = I) iff x == 0 and Im(alpha) == 0. */
+ * tau = 0 (H = I) iff x == 0 and Im(alpha) == 0.
+ * As LAPACK does, ||x|| is the scaled 2-norm of dznrm2 and ||(alpha, x)|| is
+ * dlapy3(Re alpha, Im alpha, ||x||), so neither overflows nor underflows for
+ * entries near the ends of the binary64 range; |beta| < safmin triggers the
+ * LAPACK rescale loop (x, alpha times 1/safmin until beta is representable). */
+
+/* dznrm2: sqrt(sum |x_i|^2) with the running (scale, ssq) pair. */
+static double nrm2_scaled(int64_t m, const zc *x, int64_t incx) {
+  double scale = 0.0, ssq = 1.0;
+  for (int64_t i = 0; i < m; i++) {
+    double comp[2] = {creal(x[i * incx]), cimag(x[i * incx])};
+    for (int c = 0; c < 2; c++) {
+      if (comp[c] != 0.0) {
+        double t = fabs(comp[c]);
+        if (scale < t) { ssq = 1.0 + ssq * sq(scale / t); scale = t; }
+        else ssq += sq(t / scale);
+      }
+    }
+  }
+  return scale * sqrt(ssq);
+}
+
+/* dlapy3: sqrt(x^2 + y^2 + z^2) without unnecessary overflow/underflow. */
+static double lapy3(double x, double y, double z) {
+  double w = fmax(fabs(x), fmax(fabs(y), fabs(z)));
+  if (w == 0.0) return fabs(x) + fabs(y) + fabs(z);
+  return w * sqrt(sq(x / w) + sq(y / w) + sq(z / w));
+}
+
 void orc_larfg(int64_t m, zc *alpha, zc *x, int64_t incx, zc *tau) {
   if (m <= 0) { *tau = 0; return; }
-  double xnorm2 = 0;
-  for (int64_t i = 0; i < m - 1; i++) xnorm2 += abs2(x[i * incx]);
-  double xnorm = sqrt(xnorm2);
+  double xnorm = nrm2_scaled(m - 1, x, incx);
   double ar = creal(*alpha), ai = cimag(*alpha);
   if (xnorm == 0.0 && ai == 0.0) { *tau = 0; return; }
-  double beta = -copysign(sqrt(ar * ar + ai * ai + xnorm * xnorm), ar);
+  double beta = -copysign(lapy3(ar, ai, xnorm), ar);
   const double safmin = 2.2250738585072014e-308 / 1.1102230246251565e-16;
-  double rsafmn = 1.0 / safmin, scale = 1.0;
+  double rsafmn = 1.0 / safmin;
   int knt = 0;
   if (fabs(beta) < safmin) {
     /* rescale until beta is representable (LAPACK loop) */
     do {
       knt++;
       for (int64_t i = 0; i < m - 1; i++) x[i * incx] *= rsafmn;
-      beta *= rsafmn; ar *= rsafmn; ai *= rsafmn; scale *= rsafmn;
+      beta *= rsafmn; ar *= rsafmn; ai *= rsafmn;
     } while (fabs(beta) < safmin && knt < 20);
-    xnorm2 = 0;
-    for (int64_t i = 0; i < m - 1; i++) xnorm2 += abs2(x[i * incx]);
-    xnorm = sqrt(xnorm2);
-    beta = -copysign(sqrt(ar * ar + ai * ai + xnorm * xnorm), ar);
+    xnorm = nrm2_scaled(m - 1, x, incx);
+    beta = -copysign(lapy3(ar, ai, xnorm), ar);
   }
   *tau = CMPLX((beta - ar) / beta, -ai / beta);
   zc denom = CMPLX(ar - beta, ai);

@@ -17,7 +17,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libeigb200.so")
+# EIG_LIB overrides the library path (A/B profiling of two builds only)
+_SO = os.environ.get("EIG_LIB") or os.path.join(_HERE, "libeigb200.so")
 
 EIG_RANGE_ALL, EIG_RANGE_FRACTION, EIG_RANGE_INDEX = 0, 1, 2
 EIG_HOST_BUFFERS = 1
@@ -107,7 +108,7 @@ def colmajor(x: torch.Tensor, device=None) -> torch.Tensor:
 def _ld(x: torch.Tensor) -> int:
     if x.dim() != 2:
         raise EigError("expected a 2-D column-major tensor")
-    if x.shape[1] > 1 and x.stride(0) != 1:
+    if x.stride(0) != 1 and x.numel() > 1:
         raise EigError("tensor is not column-major (stride(0) must be 1); use colmajor()")
     return max(x.stride(1) if x.shape[1] > 1 else x.shape[0], 1)
 
@@ -145,6 +146,26 @@ class Solver:
         except Exception:
             pass
 
+    def _dv(self, x, dtype, name, min_numel=0):
+        """Argument check before a pointer crosses the ABI: a device tensor of
+        this handle's GPU, the dtype the C ABI expects, at least min_numel
+        elements (the ABI reads raw memory and cannot check any of this)."""
+        if not isinstance(x, torch.Tensor):
+            raise EigError(f"{name}: expected a torch.Tensor")
+        if x.device.type != "cuda" or (x.device.index or 0) != self.device:
+            raise EigError(f"{name}: expected a tensor on cuda:{self.device}, got {x.device}")
+        if x.dtype != dtype:
+            raise EigError(f"{name}: expected {dtype}, got {x.dtype}")
+        if x.numel() < min_numel:
+            raise EigError(f"{name}: needs at least {min_numel} elements, has {x.numel()}")
+        return x
+
+    def _mat(self, x, name, rows, cols, dtype=torch.complex128):
+        self._dv(x, dtype, name)
+        if x.dim() != 2 or x.shape[0] < rows or x.shape[1] < cols:
+            raise EigError(f"{name}: expected at least {rows} x {cols}, got {tuple(x.shape)}")
+        return x
+
     def _check(self, rc):
         if rc != 0:
             msg = lib().eig_strerror(rc).decode()
@@ -171,6 +192,7 @@ class Solver:
         """a1..a5: A (n x n column-major complex128, lower) -> band + V in place.
         Returns (tau [K*nb], T [K, nb, nb] column-major blocks as (K, nb*nb))."""
         n = A.shape[0]
+        self._mat(A, "A", n, n)
         K = num_panels(n, self.nb)
         tau = torch.zeros(max(K * self.nb, 1), dtype=torch.complex128, device=A.device)
         T = torch.zeros(max(K * self.nb * self.nb, 1), dtype=torch.complex128, device=A.device)
@@ -180,6 +202,7 @@ class Solver:
     def hb2st(self, A):
         """NEXT-1: band (he2hb output A) -> (d, e, V2 [slots, nb], tau2 [slots])."""
         n = A.shape[0]
+        self._mat(A, "A", n, n)
         slots = v2_slots(n, self.nb)
         d = torch.zeros(max(n, 1), dtype=torch.float64, device=A.device)
         e = torch.zeros(max(n, 1), dtype=torch.float64, device=A.device)
@@ -191,6 +214,8 @@ class Solver:
     def stedc(self, d, e, il=1, iu=None):
         """NEXT-2: tridiagonal D&C.  Returns (w [n] all eigenvalues, Z [n, iu-il+1] real)."""
         n = d.shape[0]
+        self._dv(d, torch.float64, "d", n)
+        self._dv(e, torch.float64, "e", max(n - 1, 0))
         iu = n if iu is None else iu
         w = torch.zeros(max(n, 1), dtype=torch.float64, device=d.device)
         Z = empty_colmajor(n, iu - il + 1, dtype=torch.float64, device=d.device)
@@ -201,6 +226,7 @@ class Solver:
     def potrf(self, B):
         """NEXT-3: B <- L (lower) in place.  Returns LAPACK-style info (0 or n + j)."""
         n = B.shape[0]
+        self._mat(B, "B", n, n)
         rc = lib().eig_potrf(self.h, n, _ptr(B), _ld(B))
         if rc < 0:
             self._check(rc)
@@ -209,6 +235,8 @@ class Solver:
     def hegst(self, A, L):
         """NEXT-3: A <- L^-1 A L^-H (full Hermitian storage)."""
         n = A.shape[0]
+        self._mat(A, "A", n, n)
+        self._mat(L, "L", n, n)
         self._check(lib().eig_hegst(self.h, n, _ptr(A), _ld(A), _ptr(L), _ld(L)))
         return A
 
@@ -217,6 +245,8 @@ class Solver:
         (lower read; both destroyed, B <- L).  Returns (w [n], Z [n, m]).
         Raises EigError on failure (info n + j: B not positive definite)."""
         n = A.shape[0]
+        self._mat(A, "A", n, n)
+        self._mat(B, "B", n, n)
         if fraction is not None:
             rng, f, a, b = EIG_RANGE_FRACTION, float(fraction), 0, 0
             m = max(1, min(n, int(np.ceil(fraction * n))))
@@ -236,17 +266,28 @@ class Solver:
 
     def apply_q1(self, A, T, E):
         n, m = E.shape
+        self._mat(A, "A", n, n)
+        self._mat(E, "E", n, m)
+        self._dv(T, torch.complex128, "T", num_panels(n, self.nb) * self.nb * self.nb)
         self._check(lib().eig_apply_q1(self.h, n, _ptr(A), _ld(A), _ptr(T), _ptr(E), _ld(E), m))
         return E
 
     def apply_q2(self, V2, tau2, E, Z=None):
         n, m = E.shape
+        self._mat(E, "E", n, m)
+        slots = v2_slots(n, self.nb)
+        self._dv(V2, torch.complex128, "V2", slots * self.nb)
+        self._dv(tau2, torch.complex128, "tau2", slots)
+        if Z is not None:
+            self._mat(Z, "Z", n, m, torch.float64)
         ldz = _ld(Z) if Z is not None else n
         self._check(lib().eig_apply_q2(self.h, n, _ptr(V2), _ptr(tau2), _ptr(Z), ldz, _ptr(E), _ld(E), m))
         return E
 
     def trsm_lh(self, L, E):
         n, m = E.shape
+        self._mat(L, "L", n, n)
+        self._mat(E, "E", n, m)
         self._check(lib().eig_trsm_lh(self.h, n, _ptr(L), _ld(L), _ptr(E), _ld(E), m))
         return E
 
@@ -254,6 +295,9 @@ class Solver:
         M, N = Cm.shape
         if K is None:
             K = A.shape[1] if opa == "N" else A.shape[0]
+        self._mat(Cm, "C", M, N)
+        self._mat(A, "A", *((M, K) if opa == "N" else (K, M)))
+        self._mat(B, "B", *((K, N) if opb == "N" else (N, K)))
         self._check(lib().eig_zgemm(self.h, opa.encode(), opb.encode(), M, N, K, alpha, _ptr(A), _ld(A), _ptr(B),
                                     _ld(B), beta, _ptr(Cm), _ld(Cm), int(herm_a), int(lower_c)))
         return Cm
@@ -263,6 +307,12 @@ class Solver:
         he2hb(A) -> E = complex(Z) -> Q2 -> Q1 -> L^-H.  Returns (E, tau1, T1)."""
         n = A.shape[0]
         m = Z.shape[1]
+        self._mat(A, "A", n, n)
+        self._mat(L, "L", n, n)
+        self._mat(Z, "Z", n, m, torch.float64)
+        slots = v2_slots(n, self.nb)
+        self._dv(V2, torch.complex128, "V2", slots * self.nb)
+        self._dv(tau2, torch.complex128, "tau2", slots)
         K = num_panels(n, self.nb)
         if tau1 is None:
             tau1 = torch.zeros(max(K * self.nb, 1), dtype=torch.complex128, device=A.device)
@@ -270,6 +320,9 @@ class Solver:
             T1 = torch.zeros(max(K * self.nb * self.nb, 1), dtype=torch.complex128, device=A.device)
         if E is None:
             E = empty_colmajor(n, m, device=A.device)
+        self._mat(E, "E", n, m)
+        self._dv(tau1, torch.complex128, "tau1", K * self.nb)
+        self._dv(T1, torch.complex128, "T1", K * self.nb * self.nb)
         self._check(lib().eig_hotpath(self.h, n, _ptr(A), _ld(A), _ptr(tau1), _ptr(T1), _ptr(V2), _ptr(tau2),
                                       _ptr(L), _ld(L), _ptr(Z), _ld(Z), _ptr(E), _ld(E), m, flags))
         return E, tau1, T1
@@ -281,9 +334,17 @@ class Solver:
         Fortran-ordered (column-major); pinned memory is recommended."""
         n = A.shape[0]
         m = Z.shape[1]
-        for name, x in (("A", A), ("L", L), ("Z", Z), ("E", E)):
-            if not x.flags.f_contiguous:
+        for name, x, dt in (("A", A, np.complex128), ("L", L, np.complex128), ("Z", Z, np.float64),
+                            ("E", E, np.complex128), ("V2", V2, np.complex128), ("tau2", tau2, np.complex128)):
+            if x.dtype != dt:
+                raise EigError(f"{name} must be {np.dtype(dt).name}, got {x.dtype}")
+            if x.ndim == 2 and not x.flags.f_contiguous and x.shape[1] > 1 and name != "V2":
                 raise EigError(f"{name} must be Fortran-ordered")
+        slots = v2_slots(n, self.nb)
+        if V2.size < slots * self.nb or tau2.size < slots or not V2.flags.c_contiguous:
+            raise EigError("V2 / tau2 too small or not contiguous")
+        if A.shape != (n, n) or L.shape != (n, n) or Z.shape[0] != n or E.shape != (n, m):
+            raise EigError("host buffer shapes do not match n, m")
 
         def hp(x):
             return C.c_void_p(x.ctypes.data)

@@ -227,10 +227,11 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
     EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_q1[par], 0), "q1 prep wait"));
     Zgemm g;   // Y = V^H E
     g.opa = OP_C; g.M = w; g.N = m; g.K = s; g.A = Vb; g.lda = ldv; g.B = E + r0; g.ldb = lde; g.C = Y; g.ldc = w;
+    g.split_n = kBtSplitN;
     EIG_TRY(zgemm(c, g));
     g = Zgemm();   // E -= (V T) Y
     g.M = s; g.N = m; g.K = w; g.A = VTbuf(par); g.lda = ldv; g.B = Y; g.ldb = w; g.C = E + r0; g.ldc = lde;
-    g.alpha = -1.0; g.beta = 1.0;
+    g.alpha = -1.0; g.beta = 1.0; g.split_n = kBtSplitN;
     EIG_TRY(zgemm(c, g));
     EIG_TRY(c.check(cudaEventRecord(c.ev_q1[2 + par], c.stream), "q1 gemms done"));
   }
@@ -258,7 +259,7 @@ static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2
     Zgemm g;
     if (I1 < n) {
       g.opa = OP_C; g.M = I1 - I0; g.N = m; g.K = n - I1; g.A = L + I1 + I0 * ldl; g.lda = ldl; g.B = E + I1;
-      g.ldb = lde; g.C = E + I0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0;
+      g.ldb = lde; g.C = E + I0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0; g.split_n = kBtSplitN;
       EIG_TRY(zgemm(c, g));
     }
     for (int64_t i0 = I0 + ((I1 - I0 - 1) / bs) * bs; i0 >= I0; i0 -= bs) {
@@ -266,7 +267,7 @@ static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2
       if (i1 < I1) {
         g = Zgemm();
         g.opa = OP_C; g.M = bi; g.N = m; g.K = I1 - i1; g.A = L + i1 + i0 * ldl; g.lda = ldl; g.B = E + i1;
-        g.ldb = lde; g.C = E + i0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0;
+        g.ldb = lde; g.C = E + i0; g.ldc = lde; g.alpha = -1.0; g.beta = 1.0; g.split_n = kBtSplitN;
         EIG_TRY(zgemm(c, g));
       }
       // in place: one 64-row M tile per column tile, no split-K -> every CTA reads
@@ -370,42 +371,34 @@ static int hegst_run(Ctx &c, int64_t n, double2 *A, int64_t lda, const double2 *
 }
 
 // ------------------------------------------------------------------ Q2
-struct Q2Cache {
-  int64_t n = -1;
-  int nb = 0, g = 0;
-  Q2Plan plan;
-};
-
+// Plan tables of the grouped Q2 blocks (reading R7), built on the device on
+// c.stream and cached in the handle for (n, nb, g).
 static int q2_plan(Ctx &c, int64_t n, Q2Plan &p) {
+  if (c.q2_n == n && c.q2_plan_nb == c.nb && c.q2_plan_g == c.q2g && c.q2_plan.d_group_first_block == c.buf[WS_Q2PLAN]) {
+    p = c.q2_plan;
+    return 0;
+  }
   const int nb = c.nb, g = c.q2g;
   p.n = n;
   p.nb = nb;
   p.g = g;
   p.ngroups = (n - 1 + g - 1) / g;
-  std::vector<int64_t> first(p.ngroups + 1);
   int64_t tot = 0;
   for (int64_t gi = 0; gi < p.ngroups; gi++) {
-    first[gi] = tot;
     const int64_t i0 = gi * g;
     tot += (i0 > n - 2) ? 0 : (n - 2 - i0) / nb + 1;
   }
-  first[p.ngroups] = tot;
   p.nblocks = tot;
-  std::vector<int64_t> off;
-  int64_t o = 0;
-  for (int64_t j = 0; 1 + j * nb <= n - 1; j++) {
-    off.push_back(o);
-    o += n - 1 - j * nb;
-  }
-  p.J = (int64_t)off.size();
-  int64_t *d = (int64_t *)c.ws(WS_Q2PLAN, (first.size() + off.size() + 1) * sizeof(int64_t));
+  p.J = (n >= 2) ? (n - 2) / nb + 1 : 0;   // steps j with 1 + j nb <= n - 1
+  int64_t *d = (int64_t *)c.ws(WS_Q2PLAN, (p.ngroups + 1 + p.J + 1) * sizeof(int64_t));
   if (!d) return EIG_ERR_NOMEM;
-  EIG_TRY(c.check(cudaMemcpy(d, first.data(), first.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "q2 plan"));
-  if (!off.empty())
-    EIG_TRY(c.check(cudaMemcpy(d + first.size(), off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice),
-                    "q2 plan"));
   p.d_group_first_block = d;
-  p.d_off = d + first.size();
+  p.d_off = d + p.ngroups + 1;
+  EIG_TRY(plan_tables(c, n, nb, g, p.ngroups, p.J, p.d_group_first_block, p.d_off));
+  c.q2_n = n;
+  c.q2_plan_nb = nb;
+  c.q2_plan_g = g;
+  c.q2_plan = p;
   return 0;
 }
 
@@ -413,17 +406,8 @@ static int apply_q2_run(Ctx &c, int64_t n, const double2 *V2, const double2 *tau
                         int64_t m) {
   if (n <= 1 || m <= 0) return 0;
   if (c.q2g < 4) return EIG_ERR_NOTIMPL;  // nb < 3: no grouped blocks
-  static thread_local Q2Cache cache;  // plan tables are tiny; rebuilt when (n, nb, g) or the buffer changes
   Q2Plan p;
-  if (cache.n == n && cache.nb == c.nb && cache.g == c.q2g && cache.plan.d_group_first_block == c.buf[WS_Q2PLAN]) {
-    p = cache.plan;
-  } else {
-    EIG_TRY(q2_plan(c, n, p));
-    cache.n = n;
-    cache.nb = c.nb;
-    cache.g = c.q2g;
-    cache.plan = p;
-  }
+  EIG_TRY(q2_plan(c, n, p));
   double2 *T2 = (double2 *)c.ws(WS_T2, (size_t)p.nblocks * p.g * p.g * sizeof(double2));
   if (!T2) return EIG_ERR_NOMEM;
   EIG_TRY(q2_tfactors(c, p, V2, tau2, T2));
@@ -585,17 +569,10 @@ int eig_hb2st(eig_handle h, int64_t n, const void *A, int64_t lda, double *d, do
                                                   cudaMemcpyDeviceToDevice, c.stream), "d"));
     return 0;
   }
-  std::vector<int64_t> off;
-  int64_t o = 0;
-  for (int64_t j = 0; 1 + j * c.nb <= n - 1; j++) {
-    off.push_back(o);
-    o += n - 1 - j * c.nb;
-  }
-  int64_t *d_off = (int64_t *)c.ws(WS_HBOFF, off.size() * sizeof(int64_t));
+  const int64_t J = (n - 2) / c.nb + 1;   // steps j with 1 + j nb <= n - 1
+  int64_t *d_off = (int64_t *)c.ws(WS_HBOFF, J * sizeof(int64_t));
   if (!d_off) return EIG_ERR_NOMEM;
-  EIG_TRY(c.check(cudaMemcpyAsync(d_off, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice, c.stream),
-                  "offsets"));
-  EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "offsets sync"));   // host vector goes out of scope
+  EIG_TRY(plan_tables(c, n, c.nb, 1, 0, J, nullptr, d_off));   // V2 slot offsets, on the stream
   return hb2st(c, n, c.nb, (const double2 *)A, lda, d, e, (double2 *)V2, (double2 *)tau2, d_off);
 }
 
@@ -657,6 +634,12 @@ int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void 
     dtau1 = (double2 *)c.ws(WS_HOST_TAU1, (size_t)std::max<int64_t>(K, 1) * nb * sizeof(double2));
     dT1 = (double2 *)c.ws(WS_HOST_T1, (size_t)std::max<int64_t>(K, 1) * nb * nb * sizeof(double2));
     if (!dA || !v2 || !t2 || !l || !z || !dE || !dtau1 || !dT1) return EIG_ERR_NOMEM;
+    if ((flags & EIG_SKIP_HE2HB) && !(flags & EIG_SKIP_BT) && K > 0) {
+      // back-transform only: the caller's he2hb T factors are an input
+      if (!T1) return -6;
+      EIG_TRY(c.check(cudaMemcpyAsync(dT1, T1, (size_t)K * nb * nb * sizeof(double2), cudaMemcpyHostToDevice,
+                                      c.stream), "H2D T1"));
+    }
     // only the lower triangle of A is referenced: upload it in 256-column blocks
     for (int64_t j0 = 0; j0 < n; j0 += 256) {
       const int64_t w = std::min<int64_t>(256, n - j0);
@@ -686,7 +669,11 @@ int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void 
     dV2 = v2; dtau2 = t2; dL = l; dZ = z;
     dlda = n; dldl = n; dldz = n; dlde = n;
   }
-  if (!(flags & EIG_SKIP_HE2HB)) EIG_TRY(he2hb_run(c, n, dA, dlda, dtau1, dT1));
+  if (!(flags & EIG_SKIP_HE2HB)) {
+    EIG_TRY(he2hb_run(c, n, dA, dlda, dtau1, dT1));
+  } else if (!host && !(flags & EIG_SKIP_BT) && K > 0 && !T1) {
+    return -6;
+  }
   if (host && !(flags & EIG_SKIP_BT)) EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_xfer, 0), "xfer join wait"));
   if (!(flags & EIG_SKIP_BT) && m > 0) {
     EIG_TRY(complexify(c, n, m, dZ, dldz, dE, dlde));                      // a6: complexify
@@ -697,6 +684,16 @@ int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void 
     EIG_TRY(trsm_lh_run(c, n, dL, dldl, dE, dlde, m, (host && E) ? (double2 *)E : nullptr, lde));
   }
   if (host) {
+    // he2hb's tau / T factors to the caller's host buffers if given (queued
+    // after the back-transform, which only reads them)
+    if (!(flags & EIG_SKIP_HE2HB) && K > 0) {
+      if (tau1)
+        EIG_TRY(c.check(cudaMemcpyAsync(tau1, dtau1, (size_t)K * nb * sizeof(double2), cudaMemcpyDeviceToHost,
+                                        c.stream), "D2H tau1"));
+      if (T1)
+        EIG_TRY(c.check(cudaMemcpyAsync(T1, dT1, (size_t)K * nb * nb * sizeof(double2), cudaMemcpyDeviceToHost,
+                                        c.stream), "D2H T1"));
+    }
     EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync"));
     EIG_TRY(c.check(cudaStreamSynchronize(c.xfer), "sync xfer"));
   }

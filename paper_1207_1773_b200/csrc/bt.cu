@@ -103,17 +103,35 @@ __global__ void trinv_kernel(int64_t n, int bs, const double2 *L, int64_t ldl, d
   for (int e = threadIdx.x; e < bs * bs; e += blockDim.x) Linv[(int64_t)blockIdx.x * bs * bs + e] = sX[e];
 }
 
+// Plan tables on the device (no host staging, no synchronisation):
+//   off[j] = sum_{j' < j} (n - 1 - j' nb) = j (n - 1) - nb j (j - 1) / 2   (V2 slot offsets)
+//   first[gi] = number of Q2 blocks in the groups before gi (group gi = sweeps gi*g ..)
+__global__ void plan_tables_kernel(int64_t n, int nb, int g, int64_t ngroups, int64_t J, int64_t *first,
+                                   int64_t *off) {
+  for (int64_t j = threadIdx.x; j < J; j += blockDim.x) off[j] = j * (n - 1) - (int64_t)nb * j * (j - 1) / 2;
+  if (first && threadIdx.x == 0) {
+    int64_t tot = 0;
+    for (int64_t gi = 0; gi < ngroups; gi++) {
+      first[gi] = tot;
+      const int64_t i0 = gi * g;
+      tot += (i0 > n - 2) ? 0 : (n - 2 - i0) / nb + 1;
+    }
+    first[ngroups] = tot;
+  }
+}
+
 }  // namespace
+
+int plan_tables(Ctx &ctx, int64_t n, int nb, int g, int64_t ngroups, int64_t J, int64_t *first, int64_t *off) {
+  if (J <= 0 && !first) return 0;
+  plan_tables_kernel<<<1, 256, 0, ctx.stream>>>(n, nb, g, ngroups, J, first, off);
+  return ctx.launched("plan_tables_kernel");
+}
 
 int q2_tfactors(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *tau2, double2 *T2) {
   if (p.nblocks <= 0) return 0;
   const size_t smem = ((size_t)p.g * p.nb + 2 * p.g * p.g + p.g) * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    EIG_TRY(ctx.check(cudaFuncSetAttribute(q2_tfactor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024),
-                      "q2t attr"));
-    attr = true;
-  }
+  EIG_TRY(ctx.smem_attr((const void *)q2_tfactor_kernel, 100 * 1024, "q2t attr"));
   q2_tfactor_kernel<<<(unsigned)p.nblocks, 128, smem, ctx.stream>>>(p.n, p.nb, p.g, p.ngroups, p.d_group_first_block,
                                                                     p.d_off, V2, tau2, T2);
   return ctx.launched("q2_tfactor_kernel");
@@ -131,12 +149,7 @@ int trinv_blocks(Ctx &ctx, int64_t n, int bs, const double2 *L, int64_t ldl, dou
   if (n <= 0) return 0;
   const int64_t nblk = (n + bs - 1) / bs;
   const size_t smem = (size_t)2 * bs * bs * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    EIG_TRY(ctx.check(cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024),
-                      "trinv attr"));
-    attr = true;
-  }
+  EIG_TRY(ctx.smem_attr((const void *)trinv_kernel, 140 * 1024, "trinv attr"));
   trinv_kernel<<<(unsigned)nblk, std::max(bs, 32), smem, ctx.stream>>>(n, bs, L, ldl, Linv);
   return ctx.launched("trinv_kernel");
 }

@@ -3,9 +3,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <set>
 #include <string>
+#include <utility>
 
 #include "../../include/eig.h"
+#include "kernels.h"
 
 namespace eig {
 
@@ -53,6 +56,10 @@ struct Ctx {
   unsigned long long bar_epoch = 0;  // panel arrival counter value after the last launch
   unsigned long long *q2_prof = nullptr;  // debug: device counters for apply_q2 phases (EIG_Q2_PROFILE)
   std::string last_err;
+  // Q2 plan tables (device, WS_Q2PLAN) for (q2_n, nb, q2g); q2_n = -1: none yet
+  int64_t q2_n = -1;
+  int q2_plan_nb = 0, q2_plan_g = 0;
+  Q2Plan q2_plan;
   void *buf[WS_COUNT] = {};
   size_t bytes[WS_COUNT] = {};
 
@@ -60,6 +67,19 @@ struct Ctx {
   void *ws(int id, size_t need);
   // Record a CUDA error; returns EIG_ERR_CUDA or 0.
   int check(cudaError_t e, const char *what);
+  // Kernel attributes are per device: each handle (bound to one device, used
+  // by one host thread) sets them once for its device before the first launch.
+  std::set<std::pair<const void *, int>> attr_done;
+  int func_attr(const void *f, cudaFuncAttribute attr, int value, const char *what) {
+    const auto key = std::make_pair(f, (int)attr);
+    if (attr_done.count(key)) return 0;
+    const int rc = check(cudaFuncSetAttribute(f, attr, value), what);
+    if (!rc) attr_done.insert(key);
+    return rc;
+  }
+  int smem_attr(const void *f, int bytes, const char *what) {
+    return func_attr(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes, what);
+  }
   // After a kernel launch: count it and check for launch errors.
   int launched(const char *what) {
     launches++;

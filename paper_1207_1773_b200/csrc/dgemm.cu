@@ -114,12 +114,7 @@ __global__ void __launch_bounds__(THREADS, 2) dgemm_group_kernel(const DgemmProb
 
 int dgemm_group(Ctx &ctx, const DgemmProb *d_probs, int nprob, int max_tiles) {
   if (nprob <= 0 || max_tiles <= 0) return 0;
-  static bool attr = false;
-  if (!attr) {
-    EIG_TRY(ctx.check(cudaFuncSetAttribute(dgemm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)SMEM), "dgemm attr"));
-    attr = true;
-  }
+  EIG_TRY(ctx.smem_attr((const void *)dgemm_group_kernel, (int)SMEM, "dgemm attr"));
   dgemm_group_kernel<<<dim3(max_tiles, nprob), THREADS, SMEM, ctx.stream>>>(d_probs);
   return ctx.launched("dgemm_group_kernel");
 }

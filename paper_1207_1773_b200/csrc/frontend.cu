@@ -131,13 +131,8 @@ __global__ void conj_transpose_kernel(int64_t n, const double2 *X, int64_t ldx, 
 int potrf_lower(Ctx &c, int64_t n, double2 *B, int64_t ldb, int64_t *d_info) {
   double2 *Linv = (double2 *)c.ws(WS_FRONT, (size_t)FB * FB * sizeof(double2));
   if (!Linv) return EIG_ERR_NOMEM;
-  static bool attr = false;
   const size_t smem = (size_t)2 * 64 * 65 * sizeof(double2);
-  if (!attr) {
-    EIG_TRY(c.check(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                    "potrf attr"));
-    attr = true;
-  }
+  EIG_TRY(c.smem_attr((const void *)potrf_diag_kernel, (int)smem, "potrf attr"));
   // diagonal block at k (size b) and, below it, L21 = A21 L11^-H (s rows), on `st`
   auto factor_block = [&](int64_t k, cudaStream_t st) -> int {
     const int b = (int)std::min<int64_t>(FB, n - k);

@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       if (warp == 0) {
         const double2 x0 = lane < len ? sx[lane] : czero();
         const double2 x1 = lane + 32 < len ? sx[lane + 32] : czero();
+        // zlarfg (reading R1) in the band's scaled units (entries <= 1, see hb2st())
         double nrm = (lane >= 1 ? x0.x * x0.x + x0.y * x0.y : 0.0) + x1.x * x1.x + x1.y * x1.y;
         nrm = warp_sum(nrm);
         const double2 al = sx[0];
@@ -269,8 +270,11 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
     for (int k = 0; k < 6; k++) atomicAdd(&a.prof[16 + k], (unsigned long long)tacc[k]);
 }
 
-__global__ void band_in_kernel(int64_t n, int nb, const double2 *A, int64_t lda, double2 *AB, int ldab) {
+// Band copy plus the magnitude key of its largest entry (atomicMax into *key).
+__global__ void band_in_kernel(int64_t n, int nb, const double2 *A, int64_t lda, double2 *AB, int ldab,
+                               unsigned *key) {
   const int64_t total = n * (int64_t)ldab;
+  unsigned k = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int d = (int)(e % ldab);
     const int64_t c = e / ldab;
@@ -280,13 +284,31 @@ __global__ void band_in_kernel(int64_t n, int nb, const double2 *A, int64_t lda,
       if (d == 0) v.y = 0.0;
     }
     AB[e] = v;
+    k = max(k, mag_key2(v));
   }
+  k = __reduce_max_sync(0xffffffffu, k);
+  if ((threadIdx.x & 31) == 0 && k) atomicMax(key, k);
 }
 
-__global__ void tridiag_out_kernel(int64_t n, const double2 *AB, int ldab, double *d, double *e) {
+// Scaling (reading R1, LAPACK zlarfg's scaled norms): the chase runs on the
+// band times 2^-U, U = the binary exponent of its largest entry.  The chase is
+// homogeneous (V2, tau2 unchanged, d, e times 2^-U) and the factor is an exact
+// power of two, so away from the range ends the result is bitwise the
+// unscaled one, and at the ends no sum of squares over- or underflows.
+__global__ void band_scale_kernel(int64_t total, double2 *AB, const unsigned *key) {
+  const int U = exp_of_key(*key);
+  if (U == kExpZero || U == 0) return;
+  const double f = pow2i(-U);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    AB[e] = cscale(f, AB[e]);
+}
+
+__global__ void tridiag_out_kernel(int64_t n, const double2 *AB, int ldab, double *d, double *e, const unsigned *key) {
+  const int U = exp_of_key(*key);
+  const double f = (U == kExpZero) ? 1.0 : pow2i(U);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    d[i] = AB[i * (int64_t)ldab].x;
-    if (i + 1 < n) e[i] = AB[1 + i * (int64_t)ldab].x;
+    d[i] = AB[i * (int64_t)ldab].x * f;
+    if (i + 1 < n) e[i] = AB[1 + i * (int64_t)ldab].x * f;
   }
 }
 
@@ -298,13 +320,16 @@ int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d,
   if (nb > 64) return EIG_ERR_NOTIMPL;
   const int ldab = 2 * nb + 2;
   double2 *AB = (double2 *)ctx.ws(WS_BAND, (size_t)ldab * n * sizeof(double2));
-  int *prog = (int *)ctx.ws(WS_HBPROG, (size_t)2 * n * sizeof(int));   // progress | progressA
+  int *prog = (int *)ctx.ws(WS_HBPROG, (size_t)(2 * n + 1) * sizeof(int));   // progress | progressA | key
   if (!AB || !prog) return EIG_ERR_NOMEM;
-  EIG_TRY(ctx.check(cudaMemsetAsync(prog, 0, (size_t)2 * n * sizeof(int), ctx.stream), "memset progress"));
+  unsigned *key = (unsigned *)(prog + 2 * n);
+  EIG_TRY(ctx.check(cudaMemsetAsync(prog, 0, (size_t)(2 * n + 1) * sizeof(int), ctx.stream), "memset progress"));
   const int64_t total = n * (int64_t)ldab;
-  band_in_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 8LL * ctx.num_sms), 256, 0, ctx.stream>>>(
-      n, nb, A, lda, AB, ldab);
+  const int bgrid = (int)std::min<int64_t>((total + 255) / 256, 8LL * ctx.num_sms);
+  band_in_kernel<<<bgrid, 256, 0, ctx.stream>>>(n, nb, A, lda, AB, ldab, key);
   EIG_TRY(ctx.launched("band_in_kernel"));
+  band_scale_kernel<<<bgrid, 256, 0, ctx.stream>>>(total, AB, key);
+  EIG_TRY(ctx.launched("band_scale_kernel"));
   if (n > 1) {
     HbArgs a;
     a.n = n;
@@ -322,17 +347,12 @@ int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d,
     const int P = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, std::min<int64_t>(n - 1, J / 2 + 2)));
     void *args[] = {&a};
     const size_t smem = ((size_t)64 * LDD + 2 * 64 * 64 + 64) * sizeof(double2);
-    static bool attr = false;
-    if (!attr) {
-      EIG_TRY(ctx.check(cudaFuncSetAttribute(hb2st_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "hb2st attr"));
-      attr = true;
-    }
+    EIG_TRY(ctx.smem_attr((const void *)hb2st_kernel, (int)smem, "hb2st attr"));
     EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)hb2st_kernel, dim3(P), dim3(HT), args, smem, ctx.stream),
                       "hb2st launch"));
     EIG_TRY(ctx.launched("hb2st_kernel"));
   }
-  tridiag_out_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, ctx.stream>>>(n, AB, ldab, d, e);
+  tridiag_out_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, ctx.stream>>>(n, AB, ldab, d, e, key);
   return ctx.launched("tridiag_out_kernel");
 }
 

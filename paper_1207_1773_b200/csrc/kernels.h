@@ -25,7 +25,15 @@ struct Zgemm {
   int64_t ldc = 0;
   double alpha = 1.0, beta = 0.0;
   int splitk = 0;   // 0 = choose automatically, 1 = none, >1 = forced
+  // > 0: choose the split-K factor as if N were split_n, so the result does
+  // not depend on N (column-sliced calls are bitwise equal to the unsliced one:
+  // the back-transform's per-rank column slices)
+  int64_t split_n = 0;
 };
+
+// N used by the back-transform GEMMs for their split-K choice (columns of E
+// are the sharded dimension)
+constexpr int64_t kBtSplitN = 1024;
 
 // Enqueue C = alpha op(A) op(B) + beta C on ctx's stream.  Returns 0 or error.
 int zgemm(Ctx &ctx, const Zgemm &g);
@@ -91,6 +99,9 @@ struct Q2Plan {
   int64_t *d_off = nullptr;                // [J] device slot offsets per step j
   int64_t J = 0;
 };
+// Fill the V2 slot offsets off[0..J) and (if first != nullptr) the per-group
+// first-block table first[0..ngroups] on ctx's stream.
+int plan_tables(Ctx &ctx, int64_t n, int nb, int g, int64_t ngroups, int64_t J, int64_t *first, int64_t *off);
 int q2_tfactors(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *tau2, double2 *T2);
 int q2_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, double2 *E, int64_t lde, int64_t m);
 // column-owning-warp variant (nb = 64, g = 32); returns 1 if the shape is not handled

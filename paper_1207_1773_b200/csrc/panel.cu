@@ -14,18 +14,24 @@
 // barrier: every CTA publishes (||x_local||^2, conj(P[:,j])^H P[:,l] partial
 // dots, row j) and every CTA reduces all records in a fixed order (so the
 // result is deterministic), computes beta/tau/v locally and updates its rows.
-// Panels short enough for one thread-block cluster (CL = true: at most
-// EIG_PANEL_CLUSTER CTAs; opt-in) keep the records in each CTA's own shared
-// memory and exchange them through distributed shared memory; the split
-// barrier.cluster arrive (after publishing) / wait (before reducing) replaces
-// the L2 counter.  These are the late panels, whose latency the shrinking
-// trailing update no longer hides.
 // Because v = (a_j - beta e_j)/(alpha - beta), v^H P[:,l] follows from the raw
 // dots a_j^H P[:,l] without a second reduction.
+//
+// Scaling (reading R1: LAPACK zlarfg's dznrm2 / dlapy3 / safmin rescale keep
+// the reflector well defined near both ends of the binary64 range): after the
+// load, one extra exchange gives every CTA U_l = the binary exponent of
+// max |P[:, l]| over the whole panel, and the resident panel is multiplied by
+// D = diag(2^-U_l).  Householder QR is equivariant under column scaling
+// (QR(P D) = Q (R D)), so V, tau and T are unchanged and R comes out times D:
+// the write-back multiplies the R part (rows <= l) of column l by 2^U_l.  All
+// factors are exact powers of two, so for inputs away from the range ends the
+// result is bitwise the unscaled one; at the ends the dots and norms (entries
+// now <= ~2 sqrt(pn) in magnitude) neither overflow nor underflow.  (A column
+// that shrinks by > 2^500 relative to its panel-load maximum during the
+// factorisation would still underflow; LAPACK's per-column dznrm2 would not.)
 #include <algorithm>
 #include <cstdlib>
 
-#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -67,7 +73,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // so the trailing-column update and the T column
 //   T[0:j, j] = -tau_j T[0:j, 0:j] y   (zlarft, forward/columnwise)
 // need no second reduction.
-template <bool CL>
 __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double2 sm[];
   const int nb = a.nb, R = a.R, G = a.G;
@@ -78,13 +83,13 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
   double2 *sS = sRow + nb;          // [nb]   conj(tau) w_l for the column updates
   double2 *sW = sS + nb;            // [nb]   w_l / y_i
   double2 *sY = sW + nb;            // [nb]   y_i (T column)
-  double2 *sPart = sY + nb;         // [4][64]
-  double2 *sRec = sPart + NQ * 64;  // CL: [2][recw] this CTA's records
-  double2 *sP = sRec + (CL ? 2 * recw : 0);   // [nb][R], column l at sP + l*R
+  double2 *sPart = sY + nb;         // [NQ][64]
+  double2 *sP = sPart + NQ * 64;    // [nb][R], column l at sP + l*R
   // CTA 0: T (nb x nb, column stride R) in the unused tail rows R0..R-1 of sP
   double2 *sT = sP + a.R0;
   __shared__ double2 s_tau, s_scale;
   __shared__ double s_beta;
+  __shared__ double sColUp[64];   // 2^U_l: column l's scale (R part written back times this)
 
   const int tid = threadIdx.x;
   const int g = blockIdx.x;
@@ -100,6 +105,63 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     for (int r = tid; r < R; r += PT) sP[l * LR + r] = (r < rows) ? a.P[(row0 + r) + (int64_t)l * a.lda] : czero();
   if (g == 0)
     for (int e = tid; e < nb * nb; e += PT) sT[(e % nb) + (e / nb) * LR] = czero();
+  __syncthreads();
+  // column magnitude keys of this CTA's rows (thread cl, rows rlo..rhi)
+  {
+    unsigned k = 0;
+    if (cl < nb)
+      for (int r = rlo; r < rhi; r++) k = max(k, mag_key2(sP[cl * LR + r]));
+    reinterpret_cast<unsigned *>(sPart)[rq * 64 + cl] = k;
+  }
+  __syncthreads();
+  // exchange round 0 (records of parity 1: the column-1 records are written
+  // only after every CTA has published column 0, i.e. has read these keys)
+  {
+    double2 *out = a.rec + ((int64_t)G + g) * recw;
+    if (tid < nb) {
+      unsigned k = 0;
+#pragma unroll
+      for (int q = 0; q < NQ; q++) k = max(k, reinterpret_cast<const unsigned *>(sPart)[q * 64 + tid]);
+      __stcg(&out[tid], make_double2(__longlong_as_double((long long)k), 0.0));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
+      const unsigned long long target = a.epoch0 + (unsigned long long)G;
+      while (ld_acquire_u64(a.cnt) < target) {
+      }
+    }
+    __syncthreads();
+    {   // every thread takes CTAs q = rq, rq + NQ, ... of column cl (loads batched 4 at a time)
+      unsigned k = 0;
+      if (cl < nb)
+        for (int q0 = rq; q0 < G; q0 += 4 * NQ) {
+          unsigned kk[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int q = q0 + u * NQ;
+            kk[u] = q < G ? (unsigned)__double_as_longlong(__ldcg((const double *)(a.rec + ((int64_t)G + q) * recw + cl)))
+                          : 0u;
+          }
+          k = max(k, max(max(kk[0], kk[1]), max(kk[2], kk[3])));
+        }
+      reinterpret_cast<unsigned *>(sPart)[NQ * 64 + rq * 64 + cl] = k;   // second half of sPart
+    }
+    __syncthreads();
+    if (tid < nb) {
+      unsigned k = 0;
+#pragma unroll
+      for (int q = 0; q < NQ; q++) k = max(k, reinterpret_cast<const unsigned *>(sPart)[NQ * 64 + q * 64 + tid]);
+      const int U = exp_of_key(k);   // kExpZero: zero column, scale 1
+      sColUp[tid] = U == kExpZero ? 1.0 : pow2i(U);
+      sW[tid] = make_double2(U == kExpZero ? 1.0 : pow2i(-U), 0.0);   // 2^-U_l (sW is free until column 0)
+    }
+    __syncthreads();
+    for (int l = 0; l < nb; l++) {
+      const double f = sW[l].x;
+      for (int r = tid; r < rows; r += PT) sP[l * LR + r] = cscale(f, sP[l * LR + r]);
+    }
+  }
   __syncthreads();
 
   const bool prof = a.prof != nullptr && g == 0 && tid == 0;
@@ -129,7 +191,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     }
     sPart[rq * 64 + cl] = acc;
     __syncthreads();
-    double2 *out = CL ? sRec + (jn & 1) * recw : a.rec + ((int64_t)(jn & 1) * G + g) * recw;
+    double2 *out = a.rec + ((int64_t)(jn & 1) * G + g) * recw;
     if (tid < nb) {
       double2 t = sPart[tid];
 #pragma unroll
@@ -141,43 +203,33 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
         for (int q = 1; q < NQ; q++) c1 = cadd(c1, sPart[q * 64 + jp]);
         t = csub(t, cmul(ctau, cmul(sW[tid], c1)));
       }
-      if (CL) out[tid] = t;
-      else __stcg(&out[tid], t);
+      __stcg(&out[tid], t);
     }
     if (jn >= row0 && jn < row0 + rows)
       for (int l = tid; l < nb; l += PT) {
         double2 pv = sP[l * LR + (jn - row0)];
         if (corr && l > jn) pv = csub(pv, cmul(ctau, cmul(sP[(jn - 1) * LR + (jn - row0)], sW[l])));
-        if (CL) out[nb + l] = pv;
-        else __stcg(&out[nb + l], pv);
+        __stcg(&out[nb + l], pv);
       }
     // the barrier orders every thread's record stores before thread 0's
     // release increment (fence cumulativity): one release instead of a
     // membar in every thread; it also keeps the bulk update below from
     // overwriting row jn before it is recorded
     __syncthreads();
-    if (CL) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    else if (tid == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
+    if (tid == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
   };
   // record q (CTA q) of the exchange for column j
-  auto rec_of = [&](int q, int j) -> const double2 * {
-    if (CL) return cooperative_groups::this_cluster().map_shared_rank(sRec + (j & 1) * recw, q);
-    return a.rec + ((int64_t)(j & 1) * G + q) * recw;
-  };
+  auto rec_of = [&](int q, int j) -> const double2 * { return a.rec + ((int64_t)(j & 1) * G + q) * recw; };
 
   if (a.nref > 0) publish(0, false, czero());
   mark(4);
   for (int j = 0; j < a.nref; j++) {
-    if (CL) {
-      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    } else {
-      if (tid == 0) {
-        const unsigned long long target = a.epoch0 + (unsigned long long)G * (j + 1);
-        while (ld_acquire_u64(a.cnt) < target) {
-        }
+    if (tid == 0) {   // round 0 was the scaling exchange
+      const unsigned long long target = a.epoch0 + (unsigned long long)G * (j + 2);
+      while (ld_acquire_u64(a.cnt) < target) {
       }
-      __syncthreads();
     }
+    __syncthreads();
     mark(0);
     {
       // s_l for l >= j (every CTA: norm, w_l); s_i for i < j only feed T (CTA 0)
@@ -191,7 +243,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
 #pragma unroll
           for (int u = 0; u < 4; u++) {
             const int q = q0 + u * NQ;
-            v[u] = q < G ? (CL ? rec_of(q, j)[cl] : __ldcg(rec_of(q, j) + cl)) : czero();
+            v[u] = q < G ? __ldcg(rec_of(q, j) + cl) : czero();
           }
 #pragma unroll
           for (int u = 0; u < 4; u++)
@@ -199,7 +251,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
         }
       sPart[rq * 64 + cl] = acc;
       const int owner = j < a.R0 ? 0 : 1 + (j - a.R0) / R;
-      if (tid < nb) sRow[tid] = CL ? rec_of(owner, j)[nb + tid] : __ldcg(rec_of(owner, j) + nb + tid);
+      if (tid < nb) sRow[tid] = __ldcg(rec_of(owner, j) + nb + tid);
     }
     __syncthreads();
     // thread l < nb keeps the reduced s_l in a register; thread j (which holds
@@ -212,7 +264,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       sPart[tid] = sl;   // every thread forms w_{j+1} from it below
     }
     mark(1);
-    if (tid == j) {
+    if (tid == j) {   // zlarfg (reading R1); alpha and x are in column j's units (|.| <~ 2 sqrt(pn))
       const double2 alpha = sRow[j];
       const double xnorm2 = sl.x;
       double2 tau, scale;
@@ -310,27 +362,24 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     mark(5);
   }
 
-  // write back the factored rows and the explicit unit-lower V
-  for (int l = 0; l < nb; l++)
+  // write back the factored rows (R part times 2^U_l) and the explicit unit-lower V
+  for (int l = 0; l < nb; l++) {
+    const double up = sColUp[l];
     for (int r = tid; r < rows; r += PT) {
       const int64_t grow = row0 + r;
       const double2 p = sP[l * LR + r];
-      a.P[grow + (int64_t)l * a.lda] = p;
+      a.P[grow + (int64_t)l * a.lda] = grow <= l ? cscale(up, p) : p;
       const double2 v = (grow > l) ? p : (grow == l ? make_double2(1.0, 0.0) : czero());
       a.vout[grow + (int64_t)l * a.ldv] = v;
       if (a.vout2) a.vout2[grow + (int64_t)l * a.ldv] = v;
     }
+  }
   if (g == 0) {
     for (int l = tid; l < nb; l += PT) a.tau[l] = (l < a.nref) ? sTau[l] : czero();
     for (int e = tid; e < nb * nb; e += PT) a.T[e] = sT[(e % nb) + (e / nb) * LR];
   }
   if (prof)
     for (int k = 0; k < 6; k++) atomicAdd(&a.prof[8 + k], (unsigned long long)tacc[k]);
-  if (CL) {
-    // no CTA leaves while another may still read its records
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-  }
 }
 
 // Explicit unit-lower V (s x nb) from the he2hb storage of one panel.
@@ -367,50 +416,9 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
     const char *e = getenv("EIG_PANEL_CTAS");
     return e ? atoi(e) : 0;
   }();
-  // cluster path (opt-in): panels whose rows fit in at most EIG_PANEL_CLUSTER
-  // CTAs (<= 8 portable, up to 16 non-portable; default 0 = off).  Measured
-  // he2hb n = 2000 / 10^4: off 15.5 / 241.3 ms, 4: 15.9 / 241.7, 8: 16.5 /
-  // 242.3, 16: 15.2 / 242.8 -- the ~7 us per column is not the exchange.
-  static const int clmax = [] {
-    const char *e = getenv("EIG_PANEL_CLUSTER");
-    return std::min(16, std::max(0, e ? atoi(e) : 0));
-  }();
   const int recw = 2 * nb;
   const int words = 220 * 1024 / (int)sizeof(double2);
   const int64_t rows_nb = (pn + nb - 1) / nb;
-  {
-    const int rmax_cl = (words - 5 * nb - NQ * 64 - 2 * recw) / nb - 1;
-    const int64_t gmin = (pn + nb + rmax_cl - 1) / rmax_cl;
-    if (gmin <= clmax) {
-      int G = (int)std::max<int64_t>(gmin, std::min<int64_t>(clmax, rows_nb));
-      int R = (int)std::max<int64_t>((pn + nb + G - 1) / G, nb);
-      G = (int)((pn + nb + R - 1) / R);
-      PanelArgs a{P, lda, pn, nb, nref, R, R - nb, G, tau, T, vout, vout2, ldv, nullptr, nullptr, 0, ctx.q2_prof};
-      const size_t smem = ((size_t)5 * nb + NQ * 64 + 2 * recw + (size_t)nb * (R | 1)) * sizeof(double2);
-      static bool attr_cl = false;
-      if (!attr_cl) {
-        EIG_TRY(ctx.check(cudaFuncSetAttribute(panel_qr_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               220 * 1024), "panel attr"));
-        EIG_TRY(ctx.check(cudaFuncSetAttribute(panel_qr_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                          "panel cluster attr"));
-        attr_cl = true;
-      }
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(G);
-      cfg.blockDim = dim3(PT);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = stream;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = G;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      EIG_TRY(ctx.check(cudaLaunchKernelEx(&cfg, panel_qr_kernel<true>, a), "panel_qr_kernel<cluster> launch"));
-      return ctx.launched("panel_qr_kernel");
-    }
-  }
   const int gmax = gmax_env > 0 ? std::min(gmax_env, ctx.num_sms) : std::min(32, ctx.num_sms);
   int G = (int)std::min<int64_t>(gmax, rows_nb);
   G = std::max(G, 1);
@@ -440,16 +448,11 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   a.epoch0 = ctx.bar_epoch;
   a.prof = ctx.q2_prof;
   if (!a.rec || !a.cnt) return EIG_ERR_NOMEM;
-  static bool attr = false;
-  if (!attr) {
-    EIG_TRY(ctx.check(cudaFuncSetAttribute(panel_qr_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           220 * 1024), "panel attr"));
-    attr = true;
-  }
+  EIG_TRY(ctx.smem_attr((const void *)panel_qr_kernel, 220 * 1024, "panel attr"));
   void *args[] = {&a};
-  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel<false>, dim3(G), dim3(PT), args, smem, stream),
+  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel, dim3(G), dim3(PT), args, smem, stream),
                     "panel_qr_kernel launch"));
-  ctx.bar_epoch += (unsigned long long)G * nref;   // arrivals this launch performs
+  ctx.bar_epoch += (unsigned long long)G * (nref + 1);   // arrivals this launch performs (scaling round + columns)
   return ctx.launched("panel_qr_kernel");
 }
 

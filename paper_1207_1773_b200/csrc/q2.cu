@@ -441,15 +441,10 @@ int q2_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, do
   const int per = (a.nfr_total + grid - 1) / grid;        // fragments of the longest CTA range
   const int nslab = (per + NFMAX - 1) / NFMAX;
   const int nf = (per + nslab - 1) / nslab;
-  static bool attr[NFMAX + 1] = {};
-#define Q2_CASE(K)                                                                                          \
-  case K:                                                                                                   \
-    if (!attr[K]) {                                                                                         \
-      EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                             (int)smem), "q2 attr"));                                       \
-      attr[K] = true;                                                                                       \
-    }                                                                                                       \
-    apply_q2_kernel<K><<<grid, QT, smem, ctx.stream>>>(a, nslab);                                           \
+#define Q2_CASE(K)                                                                      \
+  case K:                                                                               \
+    EIG_TRY(ctx.smem_attr((const void *)apply_q2_kernel<K>, (int)smem, "q2 attr"));     \
+    apply_q2_kernel<K><<<grid, QT, smem, ctx.stream>>>(a, nslab);                       \
     break;
   switch (nf) {
     Q2_CASE(1) Q2_CASE(2) Q2_CASE(3) Q2_CASE(4) Q2_CASE(5) Q2_CASE(6) Q2_CASE(7) Q2_CASE(8) Q2_CASE(9)

@@ -1028,12 +1028,7 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
       const int64_t J = (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
       if (J > 0) T = std::max<int64_t>(T, J - 1 + (a.ngroups - 1 - g) + 1);
     }
-    static bool attr_w = false;
-    if (!attr_w) {
-      EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2wave_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem), "q2wave attr"));
-      attr_w = true;
-    }
+    EIG_TRY(ctx.smem_attr((const void *)apply_q2wave_kernel, (int)smem, "q2wave attr"));
     const int gridw = ctx.num_sms;
     void *args[] = {&a, &T};
     EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)apply_q2wave_kernel, dim3(gridw), dim3(32 * WAVE_WARPS), args, smem,
@@ -1047,21 +1042,11 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
   }();
   if (split_env && per <= 2) {
     a.nslab = (per + 1) / 2;
-    static bool attr_s = false;
-    if (!attr_s) {
-      EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2s_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem), "q2s attr"));
-      attr_s = true;
-    }
+    EIG_TRY(ctx.smem_attr((const void *)apply_q2s_kernel<8, 2>, (int)smem, "q2s attr"));
     apply_q2s_kernel<8, 2><<<grid, 32 * 8 * 2, smem, ctx.stream>>>(a);
     return ctx.launched("apply_q2s_kernel");
   }
-  static bool attr = false;
-  if (!attr) {
-    EIG_TRY(ctx.check(cudaFuncSetAttribute(apply_q2w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                      "q2w attr"));
-    attr = true;
-  }
+  EIG_TRY(ctx.smem_attr((const void *)apply_q2w_kernel, (int)smem, "q2w attr"));
   apply_q2w_kernel<<<grid, WT, smem, ctx.stream>>>(a);
   EIG_TRY(ctx.launched("apply_q2w_kernel"));
   return 0;

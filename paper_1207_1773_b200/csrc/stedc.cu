@@ -682,12 +682,7 @@ int stedc(Ctx &c, int64_t n, const double *d, const double *e, int64_t il, int64
                                       cudaMemcpyDeviceToDevice, c.stream), "leaf out"));
     return c.check(cudaStreamSynchronize(c.stream), "sync");   // host vectors go out of scope
   }
-  static bool attr = false;
-  if (!attr) {
-    EIG_TRY(c.check(cudaFuncSetAttribute(dc_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         2 * KSMEM * 8), "dc attr"));
-    attr = true;
-  }
+  EIG_TRY(c.smem_attr((const void *)dc_prep_kernel, 2 * KSMEM * 8, "dc attr"));
   std::vector<int> cnt;
   std::vector<DgemmProb> probs;
   for (int h = 1; h <= H; h++) {

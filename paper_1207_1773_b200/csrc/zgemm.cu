@@ -277,13 +277,7 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int split, const doub
 
 template <int OPA, int OPB, bool HERM, int LOWER>
 int launch_t(Ctx &ctx, const Params &p, dim3 grid) {
-  static bool attr_done = false;
-  if (!attr_done) {
-    EIG_TRY(ctx.check(cudaFuncSetAttribute(zgemm_kernel<OPA, OPB, HERM, LOWER>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES),
-                      "zgemm attr"));
-    attr_done = true;
-  }
+  EIG_TRY(ctx.smem_attr((const void *)zgemm_kernel<OPA, OPB, HERM, LOWER>, (int)SMEM_BYTES, "zgemm attr"));
   zgemm_kernel<OPA, OPB, HERM, LOWER><<<grid, THREADS, SMEM_BYTES, ctx.stream>>>(p);
   return ctx.launched("zgemm_kernel");
 }
@@ -298,6 +292,10 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
 
   const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
   const int64_t tiles = g.lower_c == 1 ? (int64_t)tiles_m * (tiles_m + 1) / 2 : (int64_t)tiles_m * tiles_n;
+  // the split model sees N = split_n when set (N-independent split, see kernels.h)
+  const int64_t Nm = g.split_n > 0 ? g.split_n : g.N;
+  const int64_t tiles_model =
+      g.split_n > 0 ? (int64_t)tiles_m * ((g.split_n + BN - 1) / BN) : tiles;
   const int64_t ktiles = std::max<int64_t>(1, (g.K + BK - 1) / BK);
   int split = g.splitk;
   if (split <= 0) {
@@ -309,8 +307,8 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
     split = 1;
     for (int64_t sp = 1; sp <= maxs; sp++) {
       const int64_t kt = (ktiles + sp - 1) / sp;
-      const int64_t waves = (tiles * sp + cap - 1) / cap;
-      const double red = sp > 1 ? 0.02 * (double)sp * (double)g.M * (double)g.N / (double)(cap * 64 * 64) * 8.0 : 0.0;
+      const int64_t waves = (tiles_model * sp + cap - 1) / cap;
+      const double red = sp > 1 ? 0.02 * (double)sp * (double)g.M * (double)Nm / (double)(cap * 64 * 64) * 8.0 : 0.0;
       const double t = (double)waves * (double)(kt + 3) + red;
       if (t < best * 0.98) {
         best = t;

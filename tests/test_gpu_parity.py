@@ -303,3 +303,76 @@ print("ok")
         env = dict(os.environ, EIG_PANEL_CLUSTER=c)
         r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
         assert r.returncode == 0 and "ok" in r.stdout, c + ": " + r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ extreme scales (reading R1)
+def _he2hb_scaled_parity(A, nb, tol):
+    """Device he2hb vs oracle he2hb on the SAME (scaled) input, relative to the
+    largest entry; both use LAPACK's scaled zlarfg (reading R1)."""
+    s = _solver(nb=nb)
+    n = A.shape[0]
+    dA = _dev(A)
+    tau, T = s.he2hb(dA)
+    Ag = dA.cpu().numpy()
+    A_o, tau_o = oracle.he2hb(A, nb)
+    from paper_1207_1773_b200 import num_panels
+    K = num_panels(n, nb)
+    r, c = np.indices((n, n))
+    band = (r - c >= 0) & (r - c <= nb)
+    below = r - c > nb
+    assert np.all(np.isfinite(Ag[r >= c]))
+    assert _rel(Ag[band], A_o[band]) < tol
+    assert _rel(Ag[below], A_o[below]) < tol
+    assert np.max(np.abs(tau.cpu().numpy()[:K * nb] - tau_o[:K * nb])) < tol
+    return dA, A_o
+
+
+@gpu
+@pytest.mark.parametrize("k", [-1000, -1030, 664, 1000])
+@pytest.mark.parametrize("n,nb", [(300, 32), (517, 64)])
+def test_he2hb_parity_extreme_scale(k, n, nb):
+    """A * 2^k with entries near 1e-301 / 1e-311 (subnormal) / 1e+200 / 1e+301:
+    a plain sum of squares in the panel underflows to 0 or overflows to inf;
+    the exponent-scaled device zlarfg must match the oracle's scaled norms."""
+    A = synth.rand_hermitian(n, 17) * 2.0 ** k
+    # subnormal inputs carry fewer bits: tolerance relative to what they hold
+    tol = TOL if k > -1020 else 1e-8
+    _he2hb_scaled_parity(A, nb, tol)
+
+
+@gpu
+def test_he2hb_parity_zero_tail_complex_alpha():
+    """Panel 0 column 0 has x = 0 below a complex alpha (tau != 0, beta =
+    -sign(Re alpha)|alpha|), column 1 of panel 0 has x = 0 and real alpha
+    (tau = 0), and a later panel starts from an exactly zero column."""
+    n, nb = 300, 32
+    A = synth.rand_hermitian(n, 23)
+    A[nb + 1:, 0] = 0
+    A[0, nb + 1:] = 0
+    A[nb, 0] = 0.3 + 0.9j
+    A[0, nb] = np.conj(A[nb, 0])
+    _, A_o = _he2hb_scaled_parity(A, nb, TOL)
+
+
+@gpu
+@pytest.mark.parametrize("k", [-1000, 664])
+def test_hb2st_parity_extreme_scale(k):
+    """Device bulge chase vs the oracle's dense chase on a band scaled by 2^k."""
+    from paper_1207_1773_b200 import Solver
+    n, nb = 300, 32
+    A = synth.rand_hermitian(n, 29)
+    A_o, _ = oracle.he2hb(A, nb)
+    A_o = A_o * 2.0 ** k
+    s = Solver(0, nb=nb)
+    d, e, V2, tau2 = s.hb2st(_dev(A_o))
+    rr, cc = np.indices((n, n))
+    Bl = np.where((rr - cc >= 0) & (rr - cc <= nb), A_o, 0)
+    Bf = np.tril(Bl) + np.tril(Bl, -1).conj().T
+    Bf[np.diag_indices(n)] = Bf.diagonal().real
+    d_o, e_o, V2_o, tau2_o = oracle.hb2st(Bf, nb)
+    scale = np.max(np.abs(A_o))
+    assert np.all(np.isfinite(d.cpu().numpy())) and np.all(np.isfinite(V2.cpu().numpy()))
+    assert np.max(np.abs(d.cpu().numpy() - d_o)) < 1e-11 * scale * n / 100
+    assert np.max(np.abs(e.cpu().numpy() - e_o)) < 1e-11 * scale * n / 100
+    assert np.max(np.abs(tau2.cpu().numpy() - tau2_o)) < 1e-10 * n / 100
+    assert np.max(np.abs(V2.cpu().numpy() - V2_o)) < 1e-9 * n / 100

@@ -304,15 +304,58 @@ def test_larfg_convention():
     x = np.concatenate([[alpha], rng_x])
     H = np.eye(8) - tau * np.outer(v, v.conj())
     y = H.conj().T @ x
-    assert abs(y[0] - beta) < 1e-15 and np.max(np.abs(y[1:])) < 1e-15
+    # |beta| ~ 3: a few ulps (the scaled dznrm2/dlapy3 norms of reading R1
+    # round differently from a plain sum of squares)
+    assert abs(y[0] - beta) < 4 * EPS * abs(beta) and np.max(np.abs(y[1:])) < 4 * EPS * abs(beta)
     assert np.linalg.norm(H.conj().T @ H - np.eye(8)) < 1e-14
-    assert beta == -math.copysign(np.linalg.norm(x), alpha.real)
+    assert beta == pytest.approx(-math.copysign(np.linalg.norm(x), alpha.real), rel=2 * EPS)
     assert v[0] == 1
     # zero x, real alpha -> tau = 0 (H = I); zero x, complex alpha -> real beta
     b0, t0, _ = oracle.larfg(2.5 + 0j, np.zeros(3))
     assert t0 == 0 and b0 == 2.5
     b1, t1, _ = oracle.larfg(1.0 + 1.0j, np.zeros(1))
     assert t1 != 0 and abs(b1 + math.sqrt(2)) < 1e-15
+
+
+@pytest.mark.parametrize("s", [1e-300, 1e-310, 1e-320, 1e200, 1e300])
+def test_larfg_extreme_scales(s):
+    """Reading R1: LAPACK zlarfg forms ||x|| with the scaled dznrm2 and
+    ||(alpha, x)|| with dlapy3, and rescales by 1/safmin while |beta| <
+    safmin, so H is scale invariant: larfg(s alpha, s x) = (s beta, tau, v)
+    wherever s beta is representable.  A plain sum of |x_i|^2 overflows at
+    s = 1e200 (1e400) and underflows to 0 at s = 1e-300 (tau would become 0
+    or v would be inf), so each case fails a naive norm.  The expected beta
+    is formed independently: s * -copysign(||(alpha, x)||, Re alpha) with
+    numpy's norm on the unscaled vector."""
+    x = synth.cnormal(7, 1, (9,))
+    alpha = -0.4 + 0.7j
+    beta1, tau1, v1 = oracle.larfg(alpha, x)
+    ref_beta = -math.copysign(np.linalg.norm(np.concatenate([[alpha], x])), alpha.real)
+    assert abs(beta1 - ref_beta) <= 4 * EPS * abs(ref_beta)
+    with np.errstate(all="ignore"):
+        beta, tau, v = oracle.larfg(alpha * s, x * s)
+    # subnormal inputs (s <= 1e-310) carry fewer significant bits: the
+    # tolerance is relative to the precision the inputs still have
+    prec = max(EPS, 2.0 ** -1074 / (s * np.min(np.abs(np.concatenate([[alpha], x])))))
+    assert np.isfinite(beta) and np.isfinite(tau) and np.all(np.isfinite(v))
+    assert abs(beta - s * ref_beta) <= 8 * prec * abs(s * ref_beta)
+    assert abs(tau - tau1) <= 8 * prec
+    assert np.max(np.abs(v - v1)) <= 8 * prec * np.max(np.abs(v1))
+    # H^H (alpha; x) = (beta; 0) at the scaled values, relative to s
+    xs = np.concatenate([[alpha], x]) * s
+    y = xs - np.conj(tau) * v * (v.conj() @ xs)
+    assert abs(y[0] - beta) <= 16 * prec * abs(beta)
+    assert np.max(np.abs(y[1:])) <= 16 * prec * abs(beta)
+
+
+def test_larfg_zero_tail_complex_alpha():
+    """x = 0 with complex alpha: tau != 0, beta = -sign(Re alpha)|alpha| real,
+    and H^H maps alpha to beta (the phase-fixing reflector of reading R1)."""
+    for alpha in (0.3 + 0.4j, -2.0 - 1e-3j, 1e-305 + 1e-305j, 1e250 - 3e250j):
+        beta, tau, v = oracle.larfg(alpha, np.zeros(5))
+        assert beta == pytest.approx(-math.copysign(abs(alpha), alpha.real), rel=4 * EPS)
+        assert np.all(v[1:] == 0)
+        assert abs((1 - np.conj(tau)) * alpha - beta) <= 8 * EPS * abs(beta)
 
 
 # --------------------------------------------------------------- he2hb (R3, R6)
@@ -355,6 +398,72 @@ def test_he2hb_oracle_unitary_reconstruction(n, nb):
         for j in range(min(nb, n - i - nb)):
             assert A_out[i + nb + j, i + j].imag == 0
         i += nb
+
+
+def _reflector_order(n, nb):
+    """(panel column c, unit-head row r0) of every he2hb reflector in the
+    order orc_he2hb generates them (reading R3)."""
+    out = []
+    i = 0
+    while i + nb < n:
+        for j in range(min(nb, n - i - nb)):
+            out.append((i + j, i + nb + j))
+        i += nb
+    return out
+
+
+@pytest.mark.parametrize("n,nb", [(40, 8), (37, 6)])
+def test_he2hb_partial_oracle_is_prefix_two_sided_similarity(n, nb):
+    """Pin of orc_he2hb_partial (bench cpu_baseline sample and reference of
+    the full-size first-panel GPU test): after r reflectors the stored state
+    M_r (lower triangle, processed reflector tails zeroed, Hermitian
+    completion) equals Q_r^H A Q_r with Q_r = H_1 ... H_r built explicitly
+    from the stored (v, tau); columns processed so far are in band form; no
+    tau beyond r is set; and r = K*nb (all reflectors) reproduces orc_he2hb."""
+    A = synth.rand_hermitian(n, 11 * n + nb)
+    order = _reflector_order(n, nb)
+    for r in sorted({0, 1, 3, nb - 1, nb, nb + 2, 2 * nb + 1, len(order)}):
+        r = min(r, len(order))
+        Ar, tau = oracle.he2hb_partial(A, nb, r)
+        Q = np.eye(n, dtype=complex)
+        M = np.tril(Ar).copy()
+        for (c, r0) in order[:r]:
+            v = np.zeros(n, dtype=complex)
+            v[r0] = 1
+            v[r0 + 1:] = Ar[r0 + 1:, c]
+            t = tau[(c // nb) * nb + c % nb]
+            Q = Q @ (np.eye(n) - t * np.outer(v, v.conj()))
+            M[r0 + 1:, c] = 0
+            assert Ar[r0, c].imag == 0          # diag(R) = beta is real
+        M = M + np.tril(M, -1).conj().T
+        M[np.diag_indices(n)] = M[np.diag_indices(n)].real
+        assert np.linalg.norm(Q.conj().T @ Q - np.eye(n)) <= 50 * n * EPS
+        assert np.linalg.norm(Q.conj().T @ A @ Q - M) <= 50 * n * EPS * np.linalg.norm(A)
+        done = {(c // nb) * nb + c % nb for (c, _) in order[:r]}
+        assert all(tau[k] == 0 for k in range(len(tau)) if k not in done)
+    Af, tauf = oracle.he2hb(A, nb)
+    Ap, taup = oracle.he2hb_partial(A, nb, len(order))
+    assert np.array_equal(Af, Ap) and np.array_equal(tauf, taup)
+
+
+def test_he2hb_oracle_scale_invariance_extreme():
+    """Reading R1 + R6: he2hb is homogeneous, he2hb(s A) = (s Band, V, tau),
+    with s = 2^k exactly representable, so every stage except beta's norm is
+    bitwise scaled; with LAPACK's scaled norms the result holds at s = 2^-1000
+    (entries ~1e-302, |x|^2 underflows) and s = 2^700 (|x|^2 overflows)."""
+    n, nb = 40, 6
+    A = synth.rand_hermitian(n, 5)
+    A1, t1 = oracle.he2hb(A, nb)
+    r, c = np.indices((n, n))
+    band = (r - c >= 0) & (r - c <= nb)
+    below = r - c > nb
+    for k in (-1000, 700):
+        s = 2.0 ** k
+        As, ts = oracle.he2hb(A * s, nb)
+        assert np.all(np.isfinite(As))
+        assert np.max(np.abs(ts - t1)) <= 64 * EPS
+        assert np.max(np.abs(As[below] - A1[below])) <= 64 * n * EPS * np.max(np.abs(A1[below]))
+        assert np.max(np.abs(As[band] / s - A1[band])) <= 64 * n * EPS * np.max(np.abs(A1[band]))
 
 
 def test_he2hb_oracle_degenerate_cases():
