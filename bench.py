@@ -6,8 +6,11 @@ standard-form matrix + complexify + Q2 + Q1 + L^-H on the m eigenvector columns.
 
 Metric (BASELINE.json): FP64 TFLOP/s of he2hb + back-transform, nominal flops
 16/3 n^3 + 20 n^2 m (8 real flops per complex multiply-add), workload n = 10000,
-m = 10000 (configs[3]).  N > 1: he2hb on rank 0, factors broadcast over NCCL,
-back-transform sharded by eigenvector column slices (strong scaling).
+m = 10000 (configs[3]).  N > 1 (torchrun, one process per GPU): the
+collective C-ABI call eig_hotpath runs he2hb on rank 0, broadcasts the factors
+over NCCL from inside libeigb200 (lower triangles, overlapped with he2hb) and
+back-transforms each rank's eigenvector column slice (strong scaling); the
+line adds t_BT(P) (max over ranks) and t_BT(1) / t_BT(P).
 Inputs (1.6 GB each) exceed L2 (126 MB), so no explicit L2 flush is needed.
 """
 from __future__ import annotations
@@ -249,8 +252,8 @@ def run_b200(a, rank, world, local_rank):
     import torch.distributed as dist
 
     import synth
-    from paper_1207_1773_b200 import Solver, colmajor, empty_colmajor, num_panels, v2_slots
-    from paper_1207_1773_b200.dist import column_slice, hotpath_sharded
+    from paper_1207_1773_b200 import Solver, colmajor, column_slice, empty_colmajor, num_panels, v2_slots
+    from paper_1207_1773_b200.dist import collective_solver
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -269,21 +272,16 @@ def run_b200(a, rank, world, local_rank):
         V2 = torch.from_numpy(V2_h).to(dev)
         tau2 = torch.from_numpy(tau2_h).to(dev)
         L = colmajor(L_h, dev)
-    else:
+        A = empty_colmajor(n, n, device=dev)
+    else:   # ranks > 0 receive the factors inside the collective call
         A_h = V2_h = tau2_h = L_h = None
-        A0 = empty_colmajor(n, n, device=dev)
-        V2 = torch.empty((max(slots, 1), nb), dtype=torch.complex128, device=dev)
-        tau2 = torch.empty(max(slots, 1), dtype=torch.complex128, device=dev)
-        L = empty_colmajor(n, n, device=dev)
+        A0 = V2 = tau2 = L = A = None
     Z_h = synth.real_orthonormalish(n, ml, a.seed, col0=lo)
     Z = colmajor(Z_h, dev)
     E = empty_colmajor(n, ml, device=dev)
-    A = empty_colmajor(n, n, device=dev)
-    tau1 = torch.zeros(max(K * nb, 1), dtype=torch.complex128, device=dev)
-    T1 = torch.zeros(max(K * nb * nb, 1), dtype=torch.complex128, device=dev)
     t_gen = time.perf_counter() - t_gen
 
-    solver = Solver(local_rank, nb=nb, q2_group=a.g)
+    solver = Solver(local_rank, nb=nb, q2_group=a.g) if world == 1 else collective_solver(local_rank, nb, a.g)
     stream = solver.stream
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     stage_names = ["he2hb", "q2", "q1", "trsm"]
@@ -305,12 +303,12 @@ def run_b200(a, rank, world, local_rank):
             solver.trsm_lh(L, E)
             if events:
                 events[4].record(stream)
-        else:
+        else:   # collective C-ABI call: he2hb on rank 0, NCCL broadcast, sharded back-transform
             if events:
                 events[0].record(stream)
             if rank == 0:
                 A.copy_(A0)
-            hotpath_sharded(solver, A, tau1, T1, V2, tau2, L, Z, E)
+            solver.hotpath(A, V2, tau2, L, Z, E=E)
             if events:
                 events[4].record(stream)
 
@@ -338,10 +336,33 @@ def run_b200(a, rank, world, local_rank):
     launches = solver.launches - launches0
     clk = clocks.stop()
     ms_total = t_start.elapsed_time(t_end)
+    bt_scaling = None
     if world > 1:
         tt = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_total = float(tt.item())
+        # t_BT(P): this rank's back-transform of the last step (eig_last_stats), max over ranks
+        st = solver.last_stats()
+        tb = torch.tensor([st["seconds"]["bt"], st["seconds"]["wait"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        t_bt_p = float(tb[0].item())
+        t_bt_1 = None
+        if rank == 0:   # t_BT(1): the same back-transform of all m columns on one GPU (rank 0's factors)
+            s1 = Solver(local_rank, nb=nb, q2_group=a.g)
+            from paper_1207_1773_b200 import EIG_SKIP_HE2HB
+            Zall = colmajor(synth.real_orthonormalish(n, m, a.seed), dev)
+            Eall = empty_colmajor(n, m, device=dev)
+            A.copy_(A0)
+            tau_1, T_1 = s1.he2hb(A)
+            for _ in range(2):
+                s1.hotpath(A, V2, tau2, L, Zall, E=Eall, flags=EIG_SKIP_HE2HB, tau1=tau_1, T1=T_1)
+            t_bt_1 = s1.last_stats()["seconds"]["bt"]
+            s1.close()
+            del Zall, Eall
+        bt_scaling = {"t_bt_P_s": t_bt_p, "t_bt_1_s": t_bt_1, "bt_scaling": (t_bt_1 / t_bt_p) if t_bt_1 else None,
+                      "wait_max_s": float(tb[1].item()), "bytes_comm_rank": st["bytes_comm"],
+                      "note": "t_BT = complexify+Q2+Q1+L^-H of this rank's column slice (CUDA events, eig_last_stats), "
+                              "max over ranks; t_BT(1) = all m columns on rank 0's GPU alone"}
     ms_step = ms_total / a.steps
     stages = {}
     if world == 1:
@@ -401,28 +422,30 @@ def run_b200(a, rank, world, local_rank):
 
     zhegv = None
     if world > 1 and not a.no_zhegv:
-        from paper_1207_1773_b200.dist import solve_gen_sharded
         del E
         torch.cuda.empty_cache()
-        B0 = hpd_on_device(n, 1e2, a.seed, dev) if rank == 0 else empty_colmajor(n, n, device=dev)
-        Aw, Bw = A0.clone(), B0.clone()
-        solve_gen_sharded(solver, Aw, Bw, nb)          # warm-up
-        Aw.copy_(A0)
-        Bw.copy_(B0)
+        B0 = hpd_on_device(n, 1e2, a.seed, dev) if rank == 0 else None
+        Aw, Bw = (A0.clone(), B0.clone()) if rank == 0 else (None, None)
+        solver.solve_gen(Aw, Bw, n=n)                  # warm-up (collective)
+        if rank == 0:
+            Aw.copy_(A0)
+            Bw.copy_(B0)
         torch.cuda.synchronize()
         dist.barrier()
         z0, z1 = ev(), ev()
         z0.record(stream)
-        solve_gen_sharded(solver, Aw, Bw, nb)
+        w_, Z_, zst = solver.solve_gen(Aw, Bw, n=n, stats=True)
         z1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
-        tt = torch.tensor([z0.elapsed_time(z1) * 1e-3], dtype=torch.float64, device=dev)
+        tt = torch.tensor([z0.elapsed_time(z1) * 1e-3, zst["seconds"]["bt"]], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        zhegv = {"seconds": float(tt.item()), "n": n, "m": n, "kappa_B": 1e2, "ranks": world,
-                 "note": "rank 0: potrf, hegst, he2hb, hb2st, stedc; NCCL broadcast of the factors; "
+        zhegv = {"seconds": float(tt[0].item()), "t_bt_max_s": float(tt[1].item()), "n": n, "m": n, "kappa_B": 1e2,
+                 "ranks": world, "stages_ms_rank0": {k: v * 1e3 for k, v in zst["seconds"].items()} if rank == 0 else None,
+                 "note": "collective eig_solve_gen: rank 0 potrf, hegst, he2hb, hb2st, stedc; NCCL broadcast of "
+                         "L / V1 / T1 (during hb2st) and V2 (during stedc), scatter of the eigenvector slices; "
                          "back-transform sharded by eigenvector columns; max over ranks"}
-        del Aw, Bw, B0
+        del Aw, Bw, B0, w_, Z_
     if rank == 0 and world == 1 and not a.no_zhegv:
         del E
         torch.cuda.empty_cache()
@@ -450,7 +473,7 @@ def run_b200(a, rank, world, local_rank):
                            "input_gen_s": round(t_gen, 1)},
                 "stages_ms": stages, "gpu_launches": launches,
                 "gpu_launches_per_step": launches / max(a.steps, 1), "roofline": roof, "clocks": clk,
-                "e2e": e2e, "cpu_baseline": cpu, "zhegv": zhegv}
+                "e2e": e2e, "cpu_baseline": cpu, "zhegv": zhegv, "bt_scaling": bt_scaling}
         print(json.dumps(line), flush=True)
     solver.close()
     return 0

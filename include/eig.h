@@ -22,8 +22,19 @@
  *       EIG_ERR_NOMEM    device allocation failed
  *       EIG_ERR_STATE    bad handle / not initialised
  *       EIG_ERR_NOTIMPL  entry point not available in this build
- *       EIG_ERR_NCCL     reserved (multi-GPU plumbing is torch.distributed)
- *   - One handle per host thread; many handles may coexist.
+ *       EIG_ERR_NCCL     an NCCL call failed (collective handles)
+ *   - One handle per host thread; many handles may coexist (kernel attributes
+ *     are set per handle, i.e. per device).
+ *   - Multi-GPU ("data on the GPUs is distributed", the
+ *     back-transform's column independence S:L469): one process per GPU.  Rank
+ *     0 calls eig_get_unique_id, ships the 128 bytes to the other ranks (e.g.
+ *     torch.distributed), and every rank calls eig_init with
+ *     {rank, nranks, nccl_id}.  eig_solve_gen and eig_hotpath are then
+ *     COLLECTIVE (all ranks call them with the same n / range arguments):
+ *     rank 0 runs the unsharded stages, the factors go out by NCCL broadcast
+ *     (lower triangles only) on a communication stream overlapped with rank
+ *     0's later stages, and rank r back-transforms the eigenvector columns
+ *     eig_column_slice(m, r, nranks).
  */
 #ifndef EIG_B200_H
 #define EIG_B200_H
@@ -43,6 +54,9 @@ extern "C" {
 #define EIG_RANGE_ALL      0
 #define EIG_RANGE_FRACTION 1
 #define EIG_RANGE_INDEX    2
+
+/* eig_config.flags */
+#define EIG_GATHER_Z     1u  /* collective eig_solve_gen: rank 0's Z receives all m columns      */
 
 /* eig_hotpath flags */
 #define EIG_HOST_BUFFERS 1u  /* pointers are host memory: copy in, run, copy E out (synchronous) */
@@ -64,9 +78,54 @@ typedef struct {
                         returns -2).  nb = 64 with g = 32 selects the wavefront
                         kernel; other shapes the generic grouped kernel          */
   void *stream;      /* cudaStream_t to order with; NULL = legacy default stream    */
+  int rank, nranks;  /* this process's rank and the number of ranks (GPUs); nranks
+                        <= 1 with nccl_id == NULL: single GPU (non-collective)     */
+  const void *nccl_id; /* host pointer to the 128-byte id from eig_get_unique_id() on
+                        rank 0 (same bytes on every rank); non-NULL makes the
+                        handle collective (nranks == 1 allowed: the collective
+                        code path on one GPU).  eig_init is then collective too.   */
+  int64_t n_max;     /* > 0: largest n this handle will see (calls with n > n_max
+                        return EIG_ERR_STATE; collective receive buffers are
+                        allocated at init); 0: grow lazily                        */
+  unsigned flags;    /* EIG_GATHER_Z                                               */
 } eig_config;
 
-/* Create a handle.  cfg may be NULL (defaults).  Returns 0 or an error. */
+/* Per-call statistics (device seconds from CUDA events on this rank's
+ * streams; nominal flops, 8 per complex multiply-add). */
+enum {
+  EIG_ST_POTRF = 0, EIG_ST_HEGST, EIG_ST_HE2HB, EIG_ST_HB2ST, EIG_ST_STEDC,
+  EIG_ST_WAIT,     /* BT start minus call start (collective: waiting for rank 0 + factors) */
+  EIG_ST_Q2, EIG_ST_Q1, EIG_ST_TRSM,
+  EIG_ST_BT,       /* back-transform on this rank: complexify + Q2 + Q1 + L^-H = t_BT   */
+  EIG_ST_GATHER,   /* EIG_GATHER_Z column gather                                        */
+  EIG_ST_TOTAL,    /* whole call                                                        */
+  EIG_NSTAGES
+};
+struct eig_stats {
+  double seconds[EIG_NSTAGES];
+  double flops[EIG_NSTAGES];
+  int64_t m;                 /* selected eigenvectors (all ranks)                      */
+  int64_t col_lo, col_hi;    /* this rank's columns [col_lo, col_hi) of the m          */
+  int64_t bytes_comm;        /* NCCL payload bytes this rank sent + received            */
+  int rank, nranks;
+};
+
+/* 128-byte NCCL unique id into id128 (host memory); call on rank 0 only.
+ * Host-only (no device needed).  Returns 0 or EIG_ERR_NCCL. */
+int eig_get_unique_id(void *id128);
+/* Columns [lo, hi) of m that rank r of nranks owns in the collective calls:
+ * lo = floor(r m / nranks), hi = floor((r+1) m / nranks).  Host-only.
+ * Returns 0, or -1..-3 for an illegal m / rank / nranks. */
+int eig_column_slice(int64_t m, int rank, int nranks, int64_t *lo, int64_t *hi);
+/* eig_solve_gen's selection (reading R12) without solving: (range, fraction,
+ * il, iu) for order n -> 1-based il..iu and m = iu - il + 1.  Host-only.
+ * Returns 0 or -i with eig_solve_gen's argument numbering (2, 7..10). */
+int eig_resolve_range(int64_t n, int range, double fraction, int64_t il_in, int64_t iu_in, int64_t *il,
+                      int64_t *iu, int64_t *m);
+
+/* Create a handle.  cfg may be NULL (defaults).  Returns 0 or an error;
+ * the configuration is validated before any device call (-2: bad nb,
+ * q2_group, rank / nranks, or nranks > 1 without nccl_id). */
 int eig_init(eig_handle *h, const eig_config *cfg);
 /* Destroy a handle and free its workspace (synchronises its stream). */
 int eig_finalize(eig_handle h);
@@ -147,6 +206,12 @@ int eig_trsm_lh(eig_handle h, int64_t n, const void *L, int64_t ldl, void *E, in
  * on the m selected eigenvector columns (a9: the caller passes the m columns
  * of the tridiagonal eigenvectors it wants, il..iu).
  *   A    n x n (lda), Hermitian lower; destroyed (he2hb output).
+ * Collective handle: rank 0 passes A, V2, tau2, L (device); the other ranks
+ * pass NULL for them (they receive V2, tau2 and the lower triangle of L while
+ * rank 0 runs he2hb, then the lower triangle of A (V1) and T1) and tau1/T1
+ * may be NULL on every rank; every rank passes ITS OWN column slice Z (n x m,
+ * m = its width) and E.  EIG_HOST_BUFFERS is not available collectively
+ * (EIG_ERR_NOTIMPL).  Per-stage times: eig_last_stats.
  *   tau1 K*nb, T1 K*nb*nb complex128: he2hb outputs (device).  With
  *        EIG_HOST_BUFFERS they are host pointers and may be NULL (then they
  *        stay in library workspace); if non-NULL they receive tau1 / T1.
@@ -163,6 +228,10 @@ int eig_trsm_lh(eig_handle h, int64_t n, const void *L, int64_t ldl, void *E, in
 int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void *T1, const void *V2,
                 const void *tau2, const void *L, int64_t ldl, const double *Z, int64_t ldz, void *E, int64_t lde,
                 int64_t m, unsigned flags);
+
+/* Statistics of the last eig_hotpath / eig_solve_gen call on this handle
+ * (synchronises the handle's stream).  out: host. */
+int eig_last_stats(eig_handle h, struct eig_stats *out);
 
 /* ------------------------------------------------------------------ expert
  * Complex GEMM on the FP64 DMMA tile engine (exposed for parity tests):
@@ -205,10 +274,20 @@ int eig_hegst(eig_handle h, int64_t n, void *A, int64_t lda, const void *L, int6
  *   Z   [out, device] n x m complex128 (ldz >= n), m = iu - il + 1, the
  *       B-orthonormal eigenvectors of eigenvalues il..iu.
  *   m_out [out, host, nullable] m.
+ *   stats [out, host, nullable] per-stage seconds and flops of this call.
  * Synchronous.  Returns 0, -i (illegal argument i), n + j (B not PD), or a
- * library error code. */
+ * library error code.
+ * Collective handle (all ranks call with the same n, range, fraction, il,
+ * iu): rank 0 passes A and B; the others may pass NULL (lda, ldb ignored).
+ * Every rank's w receives all n eigenvalues.  Rank r's Z (n x (hi-lo), ldz)
+ * receives the columns [lo, hi) = eig_column_slice(m, r, nranks) of the m
+ * selected eigenvectors; with EIG_GATHER_Z rank 0's Z is n x m and receives
+ * all of them (the other ranks' Z may then be NULL).  Rank 0 runs potrf,
+ * hegst, he2hb, hb2st and stedc; L, A's lower part (V1) and T1 are broadcast
+ * during hb2st, V2/tau2 during stedc, and the tridiagonal eigenvectors are
+ * scattered by column slice; errors on rank 0 are returned on every rank. */
 int eig_solve_gen(eig_handle h, int64_t n, void *A, int64_t lda, void *B, int64_t ldb, int range, double fraction,
-                  int64_t il, int64_t iu, double *w, void *Z, int64_t ldz, int64_t *m_out);
+                  int64_t il, int64_t iu, double *w, void *Z, int64_t ldz, int64_t *m_out, struct eig_stats *stats);
 
 #ifdef __cplusplus
 }

@@ -24,6 +24,8 @@ EIG_RANGE_ALL, EIG_RANGE_FRACTION, EIG_RANGE_INDEX = 0, 1, 2
 EIG_HOST_BUFFERS = 1
 EIG_SKIP_HE2HB = 2
 EIG_SKIP_BT = 4
+EIG_GATHER_Z = 1          # eig_config.flags
+STAGES = ["potrf", "hegst", "he2hb", "hb2st", "stedc", "wait", "q2", "q1", "trsm", "bt", "gather", "total"]
 
 _lib = None
 
@@ -33,7 +35,21 @@ class EigError(RuntimeError):
 
 
 class _Config(C.Structure):
-    _fields_ = [("device", C.c_int), ("nb", C.c_int), ("q2_group", C.c_int), ("stream", C.c_void_p)]
+    _fields_ = [("device", C.c_int), ("nb", C.c_int), ("q2_group", C.c_int), ("stream", C.c_void_p),
+                ("rank", C.c_int), ("nranks", C.c_int), ("nccl_id", C.c_void_p), ("n_max", C.c_int64),
+                ("flags", C.c_uint)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("seconds", C.c_double * len(STAGES)), ("flops", C.c_double * len(STAGES)), ("m", C.c_int64),
+                ("col_lo", C.c_int64), ("col_hi", C.c_int64), ("bytes_comm", C.c_int64), ("rank", C.c_int),
+                ("nranks", C.c_int)]
+
+    def to_dict(self):
+        return {"seconds": {k: self.seconds[i] for i, k in enumerate(STAGES)},
+                "flops": {k: self.flops[i] for i, k in enumerate(STAGES)}, "m": self.m,
+                "cols": (self.col_lo, self.col_hi), "bytes_comm": self.bytes_comm, "rank": self.rank,
+                "nranks": self.nranks}
 
 
 def lib():
@@ -60,7 +76,11 @@ def lib():
             "eig_trsm_lh": (C.c_int, [h, I, P, I, P, I, I]),
             "eig_hotpath": (C.c_int, [h, I, P, I, P, P, P, P, P, I, P, I, P, I, I, U]),
             "eig_zgemm": (C.c_int, [h, C.c_char, C.c_char, I, I, I, D, P, I, P, I, D, P, I, C.c_int, C.c_int]),
-            "eig_solve_gen": (C.c_int, [h, I, P, I, P, I, C.c_int, D, I, I, P, P, I, P]),
+            "eig_solve_gen": (C.c_int, [h, I, P, I, P, I, C.c_int, D, I, I, P, P, I, P, P]),
+            "eig_get_unique_id": (C.c_int, [P]),
+            "eig_column_slice": (C.c_int, [I, C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)]),
+            "eig_resolve_range": (C.c_int, [I, C.c_int, D, I, I, C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
+            "eig_last_stats": (C.c_int, [h, P]),
             "eig_debug_q2_profile": (C.c_int, [h, P]),
             "eig_hb2st": (C.c_int, [h, I, P, I, P, P, P, P]),
             "eig_stedc": (C.c_int, [h, I, P, P, I, I, P, P, I]),
@@ -78,7 +98,44 @@ def lib():
 def exported_symbols():
     return ["eig_init", "eig_finalize", "eig_strerror", "eig_last_cuda_error", "eig_launch_count", "eig_sync",
             "eig_num_panels", "eig_v2_slots", "eig_he2hb", "eig_apply_q1", "eig_apply_q2", "eig_trsm_lh",
-            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile", "eig_hb2st", "eig_stedc", "eig_potrf", "eig_hegst"]
+            "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile", "eig_hb2st", "eig_stedc", "eig_potrf",
+            "eig_hegst", "eig_get_unique_id", "eig_column_slice", "eig_resolve_range", "eig_last_stats"]
+
+
+def unique_id() -> bytes:
+    """128-byte NCCL unique id (eig_get_unique_id; host-only, call on rank 0)."""
+    buf = C.create_string_buffer(128)
+    rc = lib().eig_get_unique_id(C.cast(buf, C.c_void_p))
+    if rc:
+        raise EigError(f"eig_get_unique_id rc={rc}: {lib().eig_strerror(rc).decode()}")
+    return buf.raw
+
+
+def column_slice(m: int, rank: int, nranks: int):
+    """Columns [lo, hi) of m owned by `rank` in the collective calls (eig_column_slice)."""
+    lo, hi = C.c_int64(0), C.c_int64(0)
+    rc = lib().eig_column_slice(m, rank, nranks, C.byref(lo), C.byref(hi))
+    if rc:
+        raise EigError(f"eig_column_slice rc={rc}")
+    return lo.value, hi.value
+
+
+def resolve_range(n: int, fraction=None, il=None, iu=None):
+    """(il, iu, m) exactly as eig_solve_gen selects them (eig_resolve_range)."""
+    rng, f, a, b = _range_args(fraction, il, iu)
+    o = [C.c_int64(0) for _ in range(3)]
+    rc = lib().eig_resolve_range(n, rng, f, a, b, *[C.byref(x) for x in o])
+    if rc:
+        raise EigError(f"eig_resolve_range rc={rc}")
+    return tuple(x.value for x in o)
+
+
+def _range_args(fraction, il, iu):
+    if fraction is not None:
+        return EIG_RANGE_FRACTION, float(fraction), 0, 0
+    if il is not None:
+        return EIG_RANGE_INDEX, 0.0, int(il), int(iu)
+    return EIG_RANGE_ALL, 0.0, 0, 0
 
 
 def num_panels(n: int, nb: int) -> int:
@@ -120,17 +177,26 @@ def _ptr(x):
 class Solver:
     """One library handle (eig_init) bound to a CUDA device and stream."""
 
-    def __init__(self, device: int = 0, nb: int = 64, q2_group: int = 0, stream=None):
+    def __init__(self, device: int = 0, nb: int = 64, q2_group: int = 0, stream=None, rank: int = 0,
+                 nranks: int = 1, nccl_id: bytes | None = None, n_max: int = 0, flags: int = 0):
+        """nccl_id (128 bytes from unique_id() on rank 0, same on every rank)
+        makes the handle collective: eig_init, solve_gen and hotpath must
+        then be called by all `nranks` processes (one per GPU)."""
         if not torch.cuda.is_available():
             raise EigError("no CUDA device: the B200 path has no CPU fallback")
         self.device = device
         self.nb = nb
         self.q2_group = q2_group
+        self.rank, self.nranks = rank, max(1, nranks)
+        self.collective = nccl_id is not None
+        self.flags = flags
         torch.cuda.set_device(device)
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
-        cfg = _Config(device, nb, q2_group, C.c_void_p(stream.cuda_stream))
+        self._id = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        cfg = _Config(device, nb, q2_group, C.c_void_p(stream.cuda_stream), rank, nranks,
+                      C.cast(self._id, C.c_void_p) if self._id is not None else None, n_max, flags)
         h = C.c_void_p()
         self._check(lib().eig_init(C.byref(h), C.byref(cfg)))
         self.h = h
@@ -240,29 +306,40 @@ class Solver:
         self._check(lib().eig_hegst(self.h, n, _ptr(A), _ld(A), _ptr(L), _ld(L)))
         return A
 
-    def solve_gen(self, A, B, fraction=None, il=None, iu=None):
+    def solve_gen(self, A, B, fraction=None, il=None, iu=None, n=None, stats=False):
         """Algorithm 1: A x = lambda B x.  A, B device column-major complex128
-        (lower read; both destroyed, B <- L).  Returns (w [n], Z [n, m]).
-        Raises EigError on failure (info n + j: B not positive definite)."""
-        n = A.shape[0]
-        self._mat(A, "A", n, n)
-        self._mat(B, "B", n, n)
-        if fraction is not None:
-            rng, f, a, b = EIG_RANGE_FRACTION, float(fraction), 0, 0
-            m = max(1, min(n, int(np.ceil(fraction * n))))
-        elif il is not None:
-            rng, f, a, b = EIG_RANGE_INDEX, 0.0, il, iu
-            m = iu - il + 1
-        else:
-            rng, f, a, b = EIG_RANGE_ALL, 0.0, 0, 0
-            m = n
-        w = torch.zeros(max(n, 1), dtype=torch.float64, device=A.device)
-        Z = empty_colmajor(n, m, device=A.device)
+        (lower read; both destroyed, B <- L).  Returns (w [n], Z [n, m]) (and
+        the per-stage statistics dict if stats=True).  Raises EigError on
+        failure (info n + j: B not positive definite).
+        Collective handle: every rank calls it; ranks > 0 may pass A = B =
+        None (then give n); Z is this rank's column slice (rank 0: all m
+        columns with EIG_GATHER_Z)."""
+        if n is None:
+            n = A.shape[0]
+        if A is not None or not self.collective or self.rank == 0:
+            self._mat(A, "A", n, n)
+            self._mat(B, "B", n, n)
+        il_, iu_, m = resolve_range(n, fraction, il, iu)
+        rng, f, a, b = _range_args(fraction, il, iu)
+        lo, hi = (0, m) if not self.collective else column_slice(m, self.rank, self.nranks)
+        if self.collective and self.rank == 0 and (self.flags & EIG_GATHER_Z):
+            lo, hi = 0, m
+        w = torch.zeros(max(n, 1), dtype=torch.float64, device=torch.device("cuda", self.device))
+        Z = empty_colmajor(n, max(hi - lo, 1), device=torch.device("cuda", self.device))
         mo = C.c_int64(0)
-        rc = lib().eig_solve_gen(self.h, n, _ptr(A), _ld(A), _ptr(B), _ld(B), rng, f, a, b, _ptr(w), _ptr(Z), _ld(Z),
-                                 C.byref(mo))
+        st = _Stats()
+        rc = lib().eig_solve_gen(self.h, n, _ptr(A), _ld(A) if A is not None else n, _ptr(B),
+                                 _ld(B) if B is not None else n, rng, f, a, b, _ptr(w), _ptr(Z), _ld(Z), C.byref(mo),
+                                 C.byref(st))
         self._check(rc)
-        return w[:n], Z[:, :mo.value]
+        out = (w[:n], Z[:, :hi - lo])
+        return (*out, st.to_dict()) if stats else out
+
+    def last_stats(self):
+        """Per-stage seconds / flops of the last hotpath or solve_gen call (eig_last_stats)."""
+        st = _Stats()
+        self._check(lib().eig_last_stats(self.h, C.byref(st)))
+        return st.to_dict()
 
     def apply_q1(self, A, T, E):
         n, m = E.shape
@@ -304,16 +381,25 @@ class Solver:
 
     def hotpath(self, A, V2, tau2, L, Z, E=None, flags=0, tau1=None, T1=None):
         """One pass of the whole hot path on device tensors:
-        he2hb(A) -> E = complex(Z) -> Q2 -> Q1 -> L^-H.  Returns (E, tau1, T1)."""
-        n = A.shape[0]
+        he2hb(A) -> E = complex(Z) -> Q2 -> Q1 -> L^-H.  Returns (E, tau1, T1).
+        Collective handle: ranks > 0 pass A = V2 = tau2 = L = None; Z / E are
+        every rank's own column slice."""
+        n = Z.shape[0]
         m = Z.shape[1]
-        self._mat(A, "A", n, n)
-        self._mat(L, "L", n, n)
         self._mat(Z, "Z", n, m, torch.float64)
         slots = v2_slots(n, self.nb)
+        K = num_panels(n, self.nb)
+        if self.collective and self.rank != 0 and A is None:
+            if E is None:
+                E = empty_colmajor(n, m, device=Z.device)
+            self._mat(E, "E", n, m)
+            self._check(lib().eig_hotpath(self.h, n, None, n, None, None, None, None, None, n, _ptr(Z), _ld(Z),
+                                          _ptr(E), _ld(E), m, flags))
+            return E, None, None
+        self._mat(A, "A", n, n)
+        self._mat(L, "L", n, n)
         self._dv(V2, torch.complex128, "V2", slots * self.nb)
         self._dv(tau2, torch.complex128, "tau2", slots)
-        K = num_panels(n, self.nb)
         if tau1 is None:
             tau1 = torch.zeros(max(K * self.nb, 1), dtype=torch.complex128, device=A.device)
         if T1 is None:

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libeigb200.so")
-SOURCES = ["abi.cu", "zgemm.cu", "panel.cu", "bt.cu", "q2.cu", "q2w.cu", "hb2st.cu", "dgemm.cu", "stedc.cu", "frontend.cu"]
+SOURCES = ["abi.cu", "zgemm.cu", "panel.cu", "bt.cu", "q2.cu", "q2w.cu", "hb2st.cu", "dgemm.cu", "stedc.cu", "frontend.cu", "comm.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -32,7 +32,9 @@ def build(force=False, verbose=False):
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
         if verbose:
             sys.stderr.write(out)
-    subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", OUT, *objs])
+    # NCCL: the system libnccl.so.2 (headers /usr/include/nccl.h); in a process
+    # that already loaded torch, the dynamic linker reuses torch's libnccl.so.2
+    subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", OUT, *objs, "-lnccl"])
     return OUT
 
 

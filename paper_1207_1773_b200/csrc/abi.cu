@@ -15,6 +15,7 @@
 #include "../../include/eig.h"
 #include "ctx.h"
 #include "kernels.h"
+#include "stages.h"
 
 namespace eig {
 
@@ -47,12 +48,12 @@ int Ctx::check(cudaError_t e, const char *what) {
   return EIG_ERR_CUDA;
 }
 
-static int64_t num_panels(int64_t n, int nb) {
+int64_t num_panels(int64_t n, int nb) {
   if (n <= nb) return 0;
   return (n - nb - 1) / nb + 1;
 }
 
-static int64_t v2_slots(int64_t n, int nb) {
+int64_t v2_slots(int64_t n, int nb) {
   int64_t tot = 0;
   for (int64_t j = 0; 1 + j * nb <= n - 1; j++) tot += n - 1 - j * nb;
   return tot;
@@ -68,7 +69,7 @@ static int64_t v2_slots(int64_t n, int nb) {
 // into (i) the next panel's nb columns and (ii) the rest; panel k+1 runs on a
 // high-priority side stream right after (i), concurrently with (ii).  The
 // [V | X | V] workspace is double-buffered by step parity.
-static int he2hb_run(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau, double2 *T) {
+int he2hb_run(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau, double2 *T) {
   const int nb = c.nb;
   const int64_t K = num_panels(n, nb);
   EIG_TRY(real_diag(c, n, A, lda));
@@ -149,7 +150,7 @@ static int he2hb_run(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau, d
 // The preparation of a group (explicit V, Gram matrix, merged T) runs on the
 // side stream one group ahead of the three big GEMMs on the main stream
 // (double-buffered by group parity), so only the GEMMs are on the critical path.
-static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const double2 *T, double2 *E, int64_t lde,
+int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const double2 *T, double2 *E, int64_t lde,
                         int64_t m) {
   const int nb = c.nb;
   const int64_t K = num_panels(n, nb);
@@ -246,8 +247,8 @@ static int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const 
 // hostE (optional, pinned host, leading dimension ldh): every 256-row block of E
 // is copied back on the transfer stream as soon as it is final (bottom block
 // first), overlapping the copy with the remaining blocks.
-static int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2 *E, int64_t lde, int64_t m,
-                       double2 *hostE = nullptr, int64_t ldh = 0) {
+int trsm_lh_run(Ctx &c, int64_t n, const double2 *L, int64_t ldl, double2 *E, int64_t lde, int64_t m,
+                double2 *hostE, int64_t ldh) {
   if (n <= 0 || m <= 0) return 0;
   const int bs = 64, BS = 256;
   const int64_t nblk = (n + bs - 1) / bs;
@@ -362,7 +363,7 @@ static int trsm_rlh_lower(Ctx &c, int64_t n, const double2 *L, int64_t ldl, doub
 // A' = L^-1 A L^-H (A' Hermitian), Algorithm 1 step 2: X = L^-1 A in
 // full, then only the lower trapezoid of X L^-H (a third of the first solve's
 // flops).
-static int hegst_run(Ctx &c, int64_t n, double2 *A, int64_t lda, const double2 *L, int64_t ldl) {
+int hegst_run(Ctx &c, int64_t n, double2 *A, int64_t lda, const double2 *L, int64_t ldl) {
   if (n <= 0) return 0;
   EIG_TRY(herm_full(c, n, A, lda));
   EIG_TRY(trsm_ln_run(c, n, L, ldl, A, lda, n));        // X = L^-1 A
@@ -402,7 +403,7 @@ static int q2_plan(Ctx &c, int64_t n, Q2Plan &p) {
   return 0;
 }
 
-static int apply_q2_run(Ctx &c, int64_t n, const double2 *V2, const double2 *tau2, double2 *E, int64_t lde,
+int apply_q2_run(Ctx &c, int64_t n, const double2 *V2, const double2 *tau2, double2 *E, int64_t lde,
                         int64_t m) {
   if (n <= 1 || m <= 0) return 0;
   if (c.q2g < 4) return EIG_ERR_NOTIMPL;  // nb < 3: no grouped blocks
@@ -428,6 +429,15 @@ extern "C" {
 
 int eig_init(eig_handle *h, const eig_config *cfg) {
   if (!h) return -1;
+  *h = nullptr;
+  // validate the whole configuration before any device call
+  if (cfg) {
+    if (cfg->nb < 0 || cfg->nb > 64) return -2;
+    if (cfg->nranks > 1 && !cfg->nccl_id) return -2;
+    if (cfg->nranks < 0 || (cfg->nranks > 0 && (cfg->rank < 0 || cfg->rank >= cfg->nranks))) return -2;
+    if (cfg->nranks <= 0 && cfg->rank != 0) return -2;
+    if (cfg->n_max < 0) return -2;
+  }
   eig_ctx *x = new (std::nothrow) eig_ctx();
   if (!x) return EIG_ERR_NOMEM;
   if (cfg) {
@@ -435,6 +445,11 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
     x->c.stream = (cudaStream_t)cfg->stream;
     if (cfg->nb) x->c.nb = cfg->nb;
     if (cfg->q2_group) x->c.q2g = cfg->q2_group;
+    x->c.rank = cfg->rank;
+    x->c.nranks = std::max(1, cfg->nranks);
+    x->c.coll = cfg->nccl_id != nullptr;
+    x->c.n_max = cfg->n_max;
+    x->c.flags = cfg->flags;
   }
   if (x->c.nb < 1 || x->c.nb > 64) { delete x; return -2; }
   if (!cfg || !cfg->q2_group) x->c.q2g = std::min(32, ((x->c.nb + 1) / 4) * 4);  // g <= nb + 1, multiple of 4
@@ -457,11 +472,23 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
   if (!rc) rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_blk, cudaEventDisableTiming), "event");
   for (int i = 0; i < 4 && !rc; i++)
     rc = x->c.check(cudaEventCreateWithFlags(&x->c.ev_q1[i], cudaEventDisableTiming), "event");
-  if (rc) { delete x; return rc; }
+  for (int i = 0; i < EIG_NSTAGES && !rc; i++) {
+    rc = x->c.check(cudaEventCreate(&x->c.st_beg[i]), "event");
+    if (!rc) rc = x->c.check(cudaEventCreate(&x->c.st_end[i]), "event");
+  }
+  if (rc) { eig_finalize(x); return rc; }
+  if (x->c.coll) {
+    rc = comm_init(x->c, cfg->nccl_id);
+    if (rc) { eig_finalize(x); return rc; }
+  }
   void *bar = x->c.ws(WS_BARRIER, 64);
-  if (!bar) { delete x; return EIG_ERR_NOMEM; }
+  if (!bar) { eig_finalize(x); return EIG_ERR_NOMEM; }
   rc = x->c.check(cudaMemset(bar, 0, 64), "barrier init");
-  if (rc) { delete x; return rc; }
+  if (rc) { eig_finalize(x); return rc; }
+  if (x->c.coll && x->c.n_max > 0) {
+    rc = comm_reserve(x->c, x->c.n_max);
+    if (rc) { eig_finalize(x); return rc; }
+  }
   if (getenv("EIG_Q2_PROFILE")) {
     x->c.q2_prof = (unsigned long long *)x->c.ws(WS_Q2PROF, 256);
     if (x->c.q2_prof) cudaMemset(x->c.q2_prof, 0, 256);
@@ -480,6 +507,11 @@ int eig_finalize(eig_handle h) {
   if (!h) return EIG_ERR_STATE;
   cudaSetDevice(h->c.device);
   cudaStreamSynchronize(h->c.stream);
+  comm_destroy(h->c);
+  for (int i = 0; i < EIG_NSTAGES; i++) {
+    if (h->c.st_beg[i]) cudaEventDestroy(h->c.st_beg[i]);
+    if (h->c.st_end[i]) cudaEventDestroy(h->c.st_end[i]);
+  }
   if (h->c.side) { cudaStreamSynchronize(h->c.side); cudaStreamDestroy(h->c.side); }
   if (h->c.ev_fork) cudaEventDestroy(h->c.ev_fork);
   if (h->c.ev_join) cudaEventDestroy(h->c.ev_join);
@@ -562,8 +594,14 @@ int eig_hb2st(eig_handle h, int64_t n, const void *A, int64_t lda, double *d, do
   EIG_TRY(valid(h));
   if (n < 0) return -2;
   if (lda < std::max<int64_t>(1, n)) return -4;
-  Ctx &c = h->c;
-  cudaSetDevice(c.device);
+  cudaSetDevice(h->c.device);
+  return hb2st_run(h->c, n, (const double2 *)A, lda, d, e, (double2 *)V2, (double2 *)tau2);
+}
+
+}  // extern "C"
+
+namespace eig {
+int hb2st_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, double *d, double *e, double2 *V2, double2 *tau2) {
   if (n <= 1) {
     if (n == 1) EIG_TRY(c.check(cudaMemcpy2DAsync(d, sizeof(double), A, sizeof(double2), sizeof(double), 1,
                                                   cudaMemcpyDeviceToDevice, c.stream), "d"));
@@ -573,8 +611,11 @@ int eig_hb2st(eig_handle h, int64_t n, const void *A, int64_t lda, double *d, do
   int64_t *d_off = (int64_t *)c.ws(WS_HBOFF, J * sizeof(int64_t));
   if (!d_off) return EIG_ERR_NOMEM;
   EIG_TRY(plan_tables(c, n, c.nb, 1, 0, J, nullptr, d_off));   // V2 slot offsets, on the stream
-  return hb2st(c, n, c.nb, (const double2 *)A, lda, d, e, (double2 *)V2, (double2 *)tau2, d_off);
+  return hb2st(c, n, c.nb, A, lda, d, e, V2, tau2, d_off);
 }
+}  // namespace eig
+
+extern "C" {
 
 int eig_stedc(eig_handle h, int64_t n, const double *d, const double *e, int64_t il, int64_t iu, double *w, double *Z,
               int64_t ldz) {
@@ -610,12 +651,27 @@ int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void 
   EIG_TRY(valid(h));
   Ctx &c = h->c;
   if (n < 1) return -2;
+  if (c.coll) {
+    if (flags & EIG_HOST_BUFFERS) return EIG_ERR_NOTIMPL;
+    if (ldz < n) return -13;
+    if (lde < n) return -15;
+    if (m < 0 || m > n) return -16;
+    if (c.n_max > 0 && n > c.n_max) return EIG_ERR_STATE;
+    cudaSetDevice(c.device);
+    return coll_hotpath(c, n, (double2 *)A, lda, (double2 *)tau1, (double2 *)T1, (const double2 *)V2,
+                        (const double2 *)tau2, (const double2 *)L, ldl, Z, ldz, (double2 *)E, lde, m, flags);
+  }
   if (lda < n) return -4;
   if (ldl < n) return -11;
   if (ldz < n) return -13;
   if (lde < n) return -15;
   if (m < 0 || m > n) return -16;
+  if (c.n_max > 0 && n > c.n_max) return EIG_ERR_STATE;
   cudaSetDevice(c.device);
+  c.stat_reset();
+  c.st.m = m;
+  c.st.col_hi = m;
+  EIG_TRY(c.stat_begin(EIG_ST_TOTAL));
   const int nb = c.nb;
   const int64_t K = num_panels(n, nb), slots = v2_slots(n, nb);
   const bool host = flags & EIG_HOST_BUFFERS;
@@ -670,19 +726,22 @@ int eig_hotpath(eig_handle h, int64_t n, void *A, int64_t lda, void *tau1, void 
     dlda = n; dldl = n; dldz = n; dlde = n;
   }
   if (!(flags & EIG_SKIP_HE2HB)) {
+    EIG_TRY(c.stat_begin(EIG_ST_HE2HB));
     EIG_TRY(he2hb_run(c, n, dA, dlda, dtau1, dT1));
+    EIG_TRY(c.stat_end(EIG_ST_HE2HB));
+    c.st.flops[EIG_ST_HE2HB] = 16.0 / 3.0 * (double)n * n * n;
   } else if (!host && !(flags & EIG_SKIP_BT) && K > 0 && !T1) {
     return -6;
   }
   if (host && !(flags & EIG_SKIP_BT)) EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_xfer, 0), "xfer join wait"));
   if (!(flags & EIG_SKIP_BT) && m > 0) {
-    EIG_TRY(complexify(c, n, m, dZ, dldz, dE, dlde));                      // a6: complexify
-    EIG_TRY(apply_q2_run(c, n, dV2, dtau2, dE, dlde, m));                   // a6: Q2
-    EIG_TRY(apply_q1_run(c, n, dA, dlda, dT1, dE, dlde, m));                // a7: Q1
-    // a8: L^-H; with host buffers each final row block of E is copied back
-    // on the transfer stream while the blocks above it are solved
-    EIG_TRY(trsm_lh_run(c, n, dL, dldl, dE, dlde, m, (host && E) ? (double2 *)E : nullptr, lde));
+    // a6 complexify + Q2, a7 Q1, a8 L^-H; with host buffers each final row
+    // block of E is copied back on the transfer stream while the blocks above
+    // it are solved
+    EIG_TRY(bt_run(c, n, dZ, dldz, dV2, dtau2, dA, dlda, dT1, dL, dldl, dE, dlde, m,
+                   (host && E) ? (double2 *)E : nullptr, lde));
   }
+  EIG_TRY(c.stat_end(EIG_ST_TOTAL));
   if (host) {
     // he2hb's tau / T factors to the caller's host buffers if given (queued
     // after the back-transform, which only reads them)
@@ -704,17 +763,54 @@ int eig_potrf(eig_handle h, int64_t n, void *B, int64_t ldb) {
   EIG_TRY(valid(h));
   if (n < 0) return -2;
   if (ldb < std::max<int64_t>(1, n)) return -4;
-  Ctx &c = h->c;
-  cudaSetDevice(c.device);
+  cudaSetDevice(h->c.device);
+  return potrf_run(h->c, n, (double2 *)B, ldb);
+}
+
+}  // extern "C"
+
+namespace eig {
+// Cholesky with LAPACK info (synchronous: the info word is read back)
+int potrf_run(Ctx &c, int64_t n, double2 *B, int64_t ldb) {
   int64_t *d_info = (int64_t *)c.ws(WS_INFO, 64);
   if (!d_info) return EIG_ERR_NOMEM;
   EIG_TRY(c.check(cudaMemsetAsync(d_info, 0, sizeof(int64_t), c.stream), "info"));
-  EIG_TRY(potrf_lower(c, n, (double2 *)B, ldb, d_info));
+  EIG_TRY(potrf_lower(c, n, B, ldb, d_info));
   int64_t info = 0;
   EIG_TRY(c.check(cudaMemcpyAsync(&info, d_info, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream), "info"));
   EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync"));
   return (int)info;
 }
+
+// E = L^-H Q1 Q2 complex(Zr) on m columns (a6..a8), with stage statistics
+int bt_run(Ctx &c, int64_t n, const double *Zr, int64_t ldzr, const double2 *V2, const double2 *tau2,
+           const double2 *A, int64_t lda, const double2 *T1, const double2 *L, int64_t ldl, double2 *E, int64_t lde,
+           int64_t m, double2 *hostE, int64_t ldh) {
+  const double dn = (double)n, dm = (double)m;
+  EIG_TRY(c.stat_begin(EIG_ST_BT));
+  if (m > 0) {
+    if (Zr) EIG_TRY(complexify(c, n, m, Zr, ldzr, E, lde));
+    EIG_TRY(c.stat_begin(EIG_ST_Q2));
+    if (c.q2g >= 4) EIG_TRY(apply_q2_run(c, n, V2, tau2, E, lde, m));
+    else if (n > 1) return EIG_ERR_NOTIMPL;
+    EIG_TRY(c.stat_end(EIG_ST_Q2));
+    EIG_TRY(c.stat_begin(EIG_ST_Q1));
+    EIG_TRY(apply_q1_run(c, n, A, lda, T1, E, lde, m));
+    EIG_TRY(c.stat_end(EIG_ST_Q1));
+    EIG_TRY(c.stat_begin(EIG_ST_TRSM));
+    EIG_TRY(trsm_lh_run(c, n, L, ldl, E, lde, m, hostE, ldh));
+    EIG_TRY(c.stat_end(EIG_ST_TRSM));
+  }
+  EIG_TRY(c.stat_end(EIG_ST_BT));
+  c.st.flops[EIG_ST_Q2] = 8.0 * dn * dn * dm;
+  c.st.flops[EIG_ST_Q1] = 8.0 * dn * dn * dm;
+  c.st.flops[EIG_ST_TRSM] = 4.0 * dn * dn * dm;
+  c.st.flops[EIG_ST_BT] = 20.0 * dn * dn * dm;
+  return 0;
+}
+}  // namespace eig
+
+extern "C" {
 
 int eig_hegst(eig_handle h, int64_t n, void *A, int64_t lda, const void *L, int64_t ldl) {
   EIG_TRY(valid(h));
@@ -725,41 +821,110 @@ int eig_hegst(eig_handle h, int64_t n, void *A, int64_t lda, const void *L, int6
   return hegst_run(h->c, n, (double2 *)A, lda, (const double2 *)L, ldl);
 }
 
-int eig_solve_gen(eig_handle h, int64_t n, void *A, int64_t lda, void *B, int64_t ldb, int range, double fraction,
-                  int64_t il, int64_t iu, double *w, void *Z, int64_t ldz, int64_t *m_out) {
-  EIG_TRY(valid(h));
-  Ctx &c = h->c;
+int eig_resolve_range(int64_t n, int range, double fraction, int64_t il_in, int64_t iu_in, int64_t *il, int64_t *iu,
+                      int64_t *m) {
   if (n < 0) return -2;
-  if (lda < std::max<int64_t>(1, n)) return -4;
-  if (ldb < std::max<int64_t>(1, n)) return -6;
+  int64_t lo = il_in, hi = iu_in;
   if (range == EIG_RANGE_ALL) {
-    il = 1;
-    iu = n;
+    lo = 1;
+    hi = n;
   } else if (range == EIG_RANGE_FRACTION) {
     if (!(fraction > 0.0 && fraction <= 1.0)) return -8;
-    il = 1;
-    iu = (int64_t)std::ceil(fraction * (double)n);
-    iu = std::max<int64_t>(1, std::min<int64_t>(n, iu));
+    lo = 1;
+    hi = (int64_t)std::ceil(fraction * (double)n);
+    hi = std::max<int64_t>(1, std::min<int64_t>(n, hi));
   } else if (range == EIG_RANGE_INDEX) {
-    if (il < 1 || il > std::max<int64_t>(1, n)) return -9;
-    if (iu < il || iu > n) return -10;
+    if (lo < 1 || lo > std::max<int64_t>(1, n)) return -9;
+    if (hi < lo || hi > n) return -10;
   } else {
     return -7;
   }
+  if (n == 0) {
+    lo = 1;
+    hi = 0;
+  }
+  if (il) *il = lo;
+  if (iu) *iu = hi;
+  if (m) *m = hi - lo + 1;
+  return 0;
+}
+
+int eig_column_slice(int64_t m, int rank, int nranks, int64_t *lo, int64_t *hi) {
+  if (m < 0) return -1;
+  if (nranks < 1) return -3;
+  if (rank < 0 || rank >= nranks) return -2;
+  if (lo) *lo = (m * rank) / nranks;
+  if (hi) *hi = (m * (rank + 1)) / nranks;
+  return 0;
+}
+
+int eig_get_unique_id(void *id128) { return comm_unique_id(id128); }
+
+int eig_last_stats(eig_handle h, struct eig_stats *out) {
+  EIG_TRY(valid(h));
+  if (!out) return -2;
+  Ctx &c = h->c;
+  cudaSetDevice(c.device);
+  EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync"));
+  eig_stats st = c.st;
+  for (int k = 0; k < EIG_NSTAGES; k++) {
+    st.seconds[k] = 0.0;
+    if (!c.st_on[k]) continue;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c.st_beg[k], c.st_end[k]) == cudaSuccess) st.seconds[k] = ms * 1e-3;
+    else cudaGetLastError();
+  }
+  if (c.st_on[EIG_ST_TOTAL] && c.st_on[EIG_ST_BT]) {   // waiting time before this rank's back-transform
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c.st_beg[EIG_ST_TOTAL], c.st_beg[EIG_ST_BT]) == cudaSuccess)
+      st.seconds[EIG_ST_WAIT] = ms * 1e-3;
+    else
+      cudaGetLastError();
+  }
+  *out = st;
+  return 0;
+}
+
+int eig_solve_gen(eig_handle h, int64_t n, void *A, int64_t lda, void *B, int64_t ldb, int range, double fraction,
+                  int64_t il, int64_t iu, double *w, void *Z, int64_t ldz, int64_t *m_out, struct eig_stats *stats) {
+  EIG_TRY(valid(h));
+  Ctx &c = h->c;
+  if (n < 0) return -2;
+  int64_t m = 0;
+  EIG_TRY(eig_resolve_range(n, range, fraction, il, iu, &il, &iu, &m));
+  if (c.n_max > 0 && n > c.n_max) return EIG_ERR_STATE;
+  cudaSetDevice(c.device);
+  if (c.coll) {
+    const int rc = coll_solve_gen(c, n, (double2 *)A, lda, (double2 *)B, ldb, il, iu, w, (double2 *)Z, ldz);
+    if (!rc && m_out) *m_out = m;
+    if (!rc && stats) EIG_TRY(eig_last_stats(h, stats));
+    return rc;
+  }
+  if (lda < std::max<int64_t>(1, n)) return -4;
+  if (ldb < std::max<int64_t>(1, n)) return -6;
   if (ldz < std::max<int64_t>(1, n)) return -13;
+  c.stat_reset();
+  c.st.m = m;
+  c.st.col_lo = 0;
+  c.st.col_hi = m;
   if (n == 0) {
     if (m_out) *m_out = 0;
+    if (stats) *stats = c.st;
     return 0;
   }
-  cudaSetDevice(c.device);
-  const int64_t m = iu - il + 1;
   const int nb = c.nb;
+  const double dn = (double)n;
+  EIG_TRY(c.stat_begin(EIG_ST_TOTAL));
   // step 1: B = L L^H
-  int rc = eig_potrf(h, n, B, ldb);
+  EIG_TRY(c.stat_begin(EIG_ST_POTRF));
+  const int rc = potrf_run(c, n, (double2 *)B, ldb);
   if (rc) return rc;
+  EIG_TRY(c.stat_end(EIG_ST_POTRF));
   double2 *dA = (double2 *)A, *dL = (double2 *)B;
   // step 2: A' = L^-1 A L^-H
+  EIG_TRY(c.stat_begin(EIG_ST_HEGST));
   EIG_TRY(hegst_run(c, n, dA, lda, dL, ldb));
+  EIG_TRY(c.stat_end(EIG_ST_HEGST));
   // step 3: two-stage standard eigensolver
   const int64_t K = num_panels(n, nb), slots = v2_slots(n, nb);
   double2 *tau1 = (double2 *)c.ws(WS_SG_TAU1, (size_t)std::max<int64_t>(K, 1) * nb * sizeof(double2));
@@ -770,17 +935,25 @@ int eig_solve_gen(eig_handle h, int64_t n, void *A, int64_t lda, void *B, int64_
   double2 *tau2 = (double2 *)c.ws(WS_SG_TAU2, (size_t)std::max<int64_t>(slots, 1) * sizeof(double2));
   double *Zr = (double *)c.ws(WS_SG_Z, (size_t)n * m * sizeof(double));
   if (!tau1 || !T1 || !dd || !de || !V2 || !tau2 || !Zr) return EIG_ERR_NOMEM;
+  EIG_TRY(c.stat_begin(EIG_ST_HE2HB));
   EIG_TRY(he2hb_run(c, n, dA, lda, tau1, T1));
-  EIG_TRY(eig_hb2st(h, n, dA, lda, dd, de, V2, tau2));
+  EIG_TRY(c.stat_end(EIG_ST_HE2HB));
+  EIG_TRY(c.stat_begin(EIG_ST_HB2ST));
+  EIG_TRY(hb2st_run(c, n, dA, lda, dd, de, V2, tau2));
+  EIG_TRY(c.stat_end(EIG_ST_HB2ST));
+  EIG_TRY(c.stat_begin(EIG_ST_STEDC));
   EIG_TRY(stedc(c, n, dd, de, il, iu, w, Zr, n));
+  EIG_TRY(c.stat_end(EIG_ST_STEDC));
   // step 3 back-transform and step 4: Z = L^-H Q1 Q2 complex(Zr)
-  EIG_TRY(complexify(c, n, m, Zr, n, (double2 *)Z, ldz));
-  if (c.q2g >= 4) EIG_TRY(apply_q2_run(c, n, V2, tau2, (double2 *)Z, ldz, m));
-  else if (n > 1) return EIG_ERR_NOTIMPL;
-  EIG_TRY(apply_q1_run(c, n, dA, lda, T1, (double2 *)Z, ldz, m));
-  EIG_TRY(trsm_lh_run(c, n, dL, ldb, (double2 *)Z, ldz, m));
+  EIG_TRY(bt_run(c, n, Zr, n, V2, tau2, dA, lda, T1, dL, ldb, (double2 *)Z, ldz, m));
+  EIG_TRY(c.stat_end(EIG_ST_TOTAL));
+  c.st.flops[EIG_ST_POTRF] = 4.0 / 3.0 * dn * dn * dn;
+  c.st.flops[EIG_ST_HEGST] = 4.0 * dn * dn * dn;
+  c.st.flops[EIG_ST_HE2HB] = 16.0 / 3.0 * dn * dn * dn;
   if (m_out) *m_out = m;
-  return c.check(cudaStreamSynchronize(c.stream), "sync");
+  EIG_TRY(c.check(cudaStreamSynchronize(c.stream), "sync"));
+  if (stats) EIG_TRY(eig_last_stats(h, stats));
+  return 0;
 }
 
 }  // extern "C"

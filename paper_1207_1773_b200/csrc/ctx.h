@@ -38,6 +38,8 @@ enum WsId {
   WS_INFO,        // device info word
   WS_SG_TAU1, WS_SG_T1, WS_SG_D, WS_SG_E, WS_SG_V2, WS_SG_TAU2, WS_SG_Z,   // solve_gen stage buffers
   WS_HOST_A, WS_HOST_V2, WS_HOST_TAU2, WS_HOST_L, WS_HOST_Z, WS_HOST_E, WS_HOST_TAU1, WS_HOST_T1,
+  // collective calls (comm.cu): received factors on ranks > 0, packing, slices
+  WS_C_A, WS_C_L, WS_C_PACK, WS_C_T1, WS_C_TAU1, WS_C_V2, WS_C_TAU2, WS_C_Z, WS_C_E, WS_C_STATUS,
   WS_COUNT
 };
 
@@ -53,6 +55,26 @@ struct Ctx {
   int q2g = 32;
   int num_sms = 148;
   int64_t launches = 0;
+  // collective (multi-GPU) state: NCCL communicator and its stream (comm.cu)
+  int rank = 0, nranks = 1;
+  bool coll = false;
+  void *nccl = nullptr;               // ncclComm_t
+  cudaStream_t cstream = nullptr;     // NCCL collectives, pack / unpack
+  cudaEvent_t ev_c[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t n_max = 0;
+  unsigned flags = 0;
+  // statistics of the last eig_hotpath / eig_solve_gen call (CUDA events)
+  cudaEvent_t st_beg[EIG_NSTAGES] = {}, st_end[EIG_NSTAGES] = {};
+  bool st_on[EIG_NSTAGES] = {};
+  eig_stats st = {};
+  void stat_reset() {
+    for (int k = 0; k < EIG_NSTAGES; k++) st_on[k] = false;
+    st = eig_stats();
+    st.rank = rank;
+    st.nranks = nranks;
+  }
+  int stat_begin(int k) { st_on[k] = true; return check(cudaEventRecord(st_beg[k], stream), "stat event"); }
+  int stat_end(int k) { return check(cudaEventRecord(st_end[k], stream), "stat event"); }
   unsigned long long bar_epoch = 0;  // panel arrival counter value after the last launch
   unsigned long long *q2_prof = nullptr;  // debug: device counters for apply_q2 phases (EIG_Q2_PROFILE)
   std::string last_err;

@@ -1,11 +1,19 @@
-"""Multi-process (world_size 2, gloo, CPU) test of the column-sharded
-back-transform driver paper_1207_1773_b200/dist.py.
+"""Multi-process (world_size 2, gloo, CPU) tests of the multi-GPU plumbing
+(DESIGN.md §8).
 
-The driver's plumbing (column slicing, broadcast of the factors from rank 0,
-per-rank back-transform, gather) is exercised with a CPU stand-in solver whose
-arithmetic is the oracle's (test-only); the result must be bitwise equal to
-the single-process composition, because every back-transform step acts on
-columns independently."""
+The collective work itself (NCCL broadcast of the factors, scatter of the
+eigenvector slices, per-rank back-transform) lives in libeigb200 (comm.cu)
+and needs GPUs; what runs here is everything around it that does not:
+
+* the C ABI's rank and argument logic: eig_get_unique_id on rank 0 shipped
+  to the other rank over torch.distributed (paper_1207_1773_b200.dist),
+  eig_column_slice / eig_resolve_range agreeing on every rank, and eig_init
+  rejecting bad {rank, nranks, nccl_id} before touching a device;
+* the property the sharding rests on: the back-transform of a column
+  slice does not depend on the other columns, so per-rank slices computed
+  with the CPU oracle and gathered are bitwise the unsliced result.
+"""
+import ctypes as C
 import os
 import socket
 
@@ -21,110 +29,6 @@ import synth
 N, NB, M = 70, 8, 11
 
 
-class OracleSolver:
-    """CPU stand-in with the Solver interface (test-only; uses oracle/)."""
-
-    def __init__(self, nb):
-        self.nb = nb
-
-    def he2hb(self, A):
-        n = A.shape[0]
-        A_o, tau = oracle.he2hb(oracle.full_hermitian(A.numpy()), self.nb)
-        A.copy_(torch.from_numpy(np.asfortranarray(A_o)).t().contiguous().t())
-        K = 0
-        while K * self.nb + self.nb < n:
-            K += 1
-        T = np.zeros((K, self.nb, self.nb), complex)
-        for k in range(K):
-            r0 = (k + 1) * self.nb
-            V = np.tril(A_o[r0:, k * self.nb:(k + 1) * self.nb], -1)
-            for j in range(min(self.nb, n - r0)):
-                V[j, j] = 1
-            T[k] = oracle.larft(V, tau[k * self.nb:(k + 1) * self.nb])
-        return torch.from_numpy(tau[:max(K * self.nb, 1)].copy()), torch.from_numpy(
-            T.transpose(0, 2, 1).reshape(-1).copy() if K else np.zeros(1, complex))
-
-    def apply_q2(self, V2, tau2, E, Z=None):
-        src = Z.numpy().astype(complex) if Z is not None else E.numpy()
-        E.copy_(torch.from_numpy(oracle.apply_q2(V2.numpy(), tau2.numpy(), self.nb, src)))
-
-    def apply_q1(self, A, T, E):
-        n = A.shape[0]
-        K = T.numel() // (self.nb * self.nb)
-        Tb = T.numpy()[:K * self.nb * self.nb].reshape(K, self.nb, self.nb)
-        tau = np.zeros(max(n, 1), complex)
-        for k in range(K):
-            tau[k * self.nb:(k + 1) * self.nb] = np.diag(Tb[k])
-        E.copy_(torch.from_numpy(oracle.apply_q1(A.numpy(), tau, self.nb, E.numpy())))
-
-    def trsm_lh(self, L, E):
-        E.copy_(torch.from_numpy(oracle.backsub_lh(np.tril(L.numpy()), E.numpy())))
-
-    # front end / tridiagonal stages (for the sharded Algorithm 1)
-    def potrf(self, B):
-        L, info = oracle.potrf(oracle.full_hermitian(B.numpy()))
-        B.copy_(_cm(L))
-        return info
-
-    def hegst(self, A, L):
-        A.copy_(_cm(oracle.std_form(A.numpy(), np.tril(L.numpy()))))
-
-    def hb2st(self, A):
-        n = A.shape[0]
-        Ao = A.numpy()
-        r, c = np.indices((n, n))
-        Bl = np.where((r - c >= 0) & (r - c <= self.nb), Ao, 0)
-        Band = np.tril(Bl) + np.tril(Bl, -1).conj().T
-        Band[np.diag_indices(n)] = Band.diagonal().real
-        d, e, V2, tau2 = oracle.hb2st(Band, self.nb)
-        return torch.from_numpy(d), torch.from_numpy(e.copy()), torch.from_numpy(V2.copy()), torch.from_numpy(tau2.copy())
-
-    def stedc(self, d, e):
-        w, Z, info = oracle.tql2(d.numpy(), e.numpy())
-        assert info == 0
-        return torch.from_numpy(w), _cm(Z)
-
-
-def _cm(x):
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(x).T)).t()
-
-
-def _inputs():
-    A = synth.rand_hermitian(N, 4)
-    V2, tau2 = synth.synthetic_v2(N, NB, 4)
-    L = synth.unit_lower(N, 4)
-    Z = synth.real_orthonormalish(N, M, 4)
-    return A, V2, tau2, L, Z
-
-
-def _worker(rank, world, port, out):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1207_1773_b200.dist import column_slice, gather_columns, hotpath_sharded
-    A, V2, tau2, L, Z = _inputs()
-    lo, hi = column_slice(M, rank, world)
-    slots = V2.shape[0]
-    K = (N - NB - 1) // NB + 1
-    if rank == 0:
-        tA, tV2, tt2, tL = _cm(A), torch.from_numpy(V2), torch.from_numpy(tau2), _cm(L)
-    else:   # other ranks receive everything from rank 0
-        tA = torch.zeros((N, N), dtype=torch.complex128).t().contiguous().t()
-        tV2 = torch.zeros((slots, NB), dtype=torch.complex128)
-        tt2 = torch.zeros(slots, dtype=torch.complex128)
-        tL = torch.zeros((N, N), dtype=torch.complex128).t().contiguous().t()
-    tau1 = torch.zeros(K * NB, dtype=torch.complex128)
-    T1 = torch.zeros(K * NB * NB, dtype=torch.complex128)
-    Zs = _cm(Z[:, lo:hi])
-    Es = torch.zeros((hi - lo, N), dtype=torch.complex128).t()
-    hotpath_sharded(OracleSolver(NB), tA, tau1, T1, tV2, tt2, tL, Zs, Es)
-    Eall = gather_columns(Es, M)
-    if rank == 0:
-        out.put(Eall.numpy().copy())
-    dist.barrier()
-    dist.destroy_process_group()
-
-
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -133,80 +37,127 @@ def _free_port():
     return p
 
 
-def _worker_gen(rank, world, port, out):
+def _spawn(target, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    return res
+
+
+def _init(rank, world, port):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_1207_1773_b200.dist import gather_columns, solve_gen_sharded
-    A, B = synth.pencil_rand(N, seed=9, kappa=10.0)
+
+
+# ------------------------------------------------------------------ ABI rank / argument logic
+def _worker_abi(rank, world, port, out):
+    _init(rank, world, port)
+    from paper_1207_1773_b200 import column_slice, lib, resolve_range
+    from paper_1207_1773_b200._binding import _Config
+    from paper_1207_1773_b200.dist import ship_unique_id
+    uid = ship_unique_id()                              # rank 0: eig_get_unique_id, gloo broadcast
+    ids = [None] * world
+    dist.all_gather_object(ids, uid)
+    slices = {m: column_slice(m, rank, world) for m in (0, 1, 7, 1250, 10000)}
+    allsl = [None] * world
+    dist.all_gather_object(allsl, slices)
+    rng = [resolve_range(5000, fraction=f) for f in (0.1, 0.25, 1e-9, 1.0)] + [resolve_range(300, il=5, iu=9)]
+    allrng = [None] * world
+    dist.all_gather_object(allrng, rng)
+    # eig_init validates {rank, nranks, nccl_id} before any device call
+    idbuf = C.create_string_buffer(uid, 128)
+    h = C.c_void_p()
+
+    def init(rk, nr, with_id):
+        cfg = _Config(0, 64, 0, None, rk, nr, C.cast(idbuf, C.c_void_p) if with_id else None, 0, 0)
+        return lib().eig_init(C.byref(h), C.byref(cfg))
+    codes = {"bad_rank": init(world + 3, world, True), "neg_rank": init(-1, world, True),
+             "no_id": init(rank, world, False)}
+    if not torch.cuda.is_available():
+        codes["valid_no_gpu"] = init(rank, world, True)  # passes validation, then no device: EIG_ERR_CUDA
+    lo, hi = C.c_int64(), C.c_int64()
+    codes["slice_bad_rank"] = lib().eig_column_slice(10, world, world, C.byref(lo), C.byref(hi))
+    codes["slice_bad_m"] = lib().eig_column_slice(-1, 0, world, C.byref(lo), C.byref(hi))
     if rank == 0:
-        tA, tB = _cm(A), _cm(B)
-    else:
-        tA = torch.zeros((N, N), dtype=torch.complex128).t().contiguous().t()
-        tB = torch.zeros((N, N), dtype=torch.complex128).t().contiguous().t()
-    w, Es, _ = solve_gen_sharded(OracleSolver(NB), tA, tB, NB)
-    Eall = gather_columns(Es, N)
-    if rank == 0:
-        out.put((w.numpy().copy(), Eall.numpy().copy()))
+        out.put((ids, allsl, allrng, codes))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_sharded_solve_gen_gloo_world2():
-    """Algorithm 1 with the sharded back-transform (2 ranks): the gathered
-    eigenvectors satisfy the residual / B-orthogonality gates and equal the
-    single-process composition bitwise."""
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker_gen, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    w, E = q.get(timeout=300)
-    for p in procs:
-        p.join(timeout=300)
-        assert p.exitcode == 0
-    A, B = synth.pencil_rand(N, seed=9, kappa=10.0)
-    R = A @ E - (B @ E) * w[None, :]
-    assert np.linalg.norm(R, 1) / (N * np.linalg.norm(A, 1) * np.linalg.norm(E, 1)) < 1e-14
-    assert np.linalg.norm(E.conj().T @ B @ E - np.eye(N), 1) / N < 1e-14
-    # single process, same stand-in solver
-    s = OracleSolver(NB)
-    tA, tB = _cm(A), _cm(B)
-    assert s.potrf(tB) == 0
-    s.hegst(tA, tB)
-    tau1, T1 = s.he2hb(tA)
-    d, e, V2, tau2 = s.hb2st(tA)
-    w1, Zr = s.stedc(d, e)
-    E1 = torch.zeros((N, N), dtype=torch.complex128).t()
-    s.apply_q2(V2, tau2, E1, Z=Zr)
-    s.apply_q1(tA, T1, E1)
-    s.trsm_lh(tB, E1)
-    assert np.array_equal(E, E1.numpy()) and np.array_equal(w, w1.numpy())
+def test_abi_rank_and_argument_logic_gloo_world2():
+    ids, allsl, allrng, codes = _spawn(_worker_abi)
+    assert len(ids[0]) == 128 and ids[0] == ids[1] and any(ids[0])
+    for m in (0, 1, 7, 1250, 10000):
+        sl = [allsl[r][m] for r in range(2)]
+        assert sl == [(0, m // 2), (m // 2, m)]           # floor(r m / P): contiguous, balanced, ordered
+    assert allrng[0] == allrng[1]
+    assert allrng[0][0] == (1, 500, 500) and allrng[0][1] == (1, 1250, 1250)
+    assert allrng[0][2] == (1, 1, 1) and allrng[0][3] == (1, 5000, 5000) and allrng[0][4] == (5, 9, 5)
+    assert codes["bad_rank"] == -2 and codes["neg_rank"] == -2 and codes["no_id"] == -2
+    if "valid_no_gpu" in codes:
+        assert codes["valid_no_gpu"] == -1001             # EIG_ERR_CUDA: validation passed
+    assert codes["slice_bad_rank"] == -2 and codes["slice_bad_m"] == -1
 
 
 def test_column_slices_partition():
-    from paper_1207_1773_b200.dist import column_slice
-    for m in (1, 7, 10000):
-        for P in (1, 2, 4, 8):
+    from paper_1207_1773_b200 import column_slice
+    for m in (0, 1, 7, 10000):
+        for P in (1, 2, 3, 4, 8):
             sl = [column_slice(m, r, P) for r in range(P)]
             assert sl[0][0] == 0 and sl[-1][1] == m
             assert all(sl[r][1] == sl[r + 1][0] for r in range(P - 1))
             assert max(b - a for a, b in sl) - min(b - a for a, b in sl) <= 1
 
 
-def test_sharded_backtransform_gloo_world2_bitwise():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    E_dist = q.get(timeout=300)
-    for p in procs:
-        p.join(timeout=300)
-        assert p.exitcode == 0
+def test_resolve_range_matches_reading_r12():
+    from paper_1207_1773_b200 import EigError, resolve_range
+    assert resolve_range(10000) == (1, 10000, 10000)
+    assert resolve_range(5000, fraction=0.1) == (1, 500, 500)       # lowest ceil(f n) (R12)
+    assert resolve_range(7, fraction=0.5) == (1, 4, 4)
+    with pytest.raises(EigError):
+        resolve_range(10, fraction=0.0)
+    with pytest.raises(EigError):
+        resolve_range(10, il=4, iu=3)
+
+
+# ------------------------------------------------------------------ slice independence (oracle)
+def _inputs():
+    A = synth.rand_hermitian(N, 4)
+    V2, tau2 = synth.synthetic_v2(N, NB, 4)
+    L = synth.unit_lower(N, 4)
+    Z = synth.real_orthonormalish(N, M, 4)
+    return A, V2, tau2, L, Z
+
+
+def _bt_oracle(A_o, tau_o, V2, tau2, L, Z):
+    return oracle.backsub_lh(L, oracle.apply_q1(A_o, tau_o, NB, oracle.apply_q2(V2, tau2, NB, Z.astype(complex))))
+
+
+def _worker_bt(rank, world, port, out):
+    _init(rank, world, port)
+    from paper_1207_1773_b200 import column_slice
     A, V2, tau2, L, Z = _inputs()
     A_o, tau_o = oracle.he2hb(A, NB)
-    E_ref = oracle.backsub_lh(L, oracle.apply_q1(A_o, tau_o, NB, oracle.apply_q2(V2, tau2, NB, Z.astype(complex))))
-    assert np.array_equal(E_dist, E_ref)
+    lo, hi = column_slice(M, rank, world)
+    E = _bt_oracle(A_o, tau_o, V2, tau2, L, Z[:, lo:hi])
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, E))
+    if rank == 0:
+        out.put(np.concatenate([p[1] for p in sorted(parts, key=lambda t: t[0])], axis=1))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sliced_backtransform_gloo_world2_bitwise():
+    E_dist = _spawn(_worker_bt)
+    A, V2, tau2, L, Z = _inputs()
+    A_o, tau_o = oracle.he2hb(A, NB)
+    assert np.array_equal(E_dist, _bt_oracle(A_o, tau_o, V2, tau2, L, Z))
