@@ -66,6 +66,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-zhegv", action="store_true", help="skip the end-to-end generalized solve timing")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
+    p.add_argument("--gemm", default="3m", choices=["3m", "4m"],
+                   help="complex GEMMs (he2hb updates, Q1, L^-H, front end) as 3 real DMMA products (3M) or 4 (4M)")
     a = p.parse_args()
     if a.m is None:
         a.m = a.n
@@ -281,7 +283,10 @@ def run_b200(a, rank, world, local_rank):
     E = empty_colmajor(n, ml, device=dev)
     t_gen = time.perf_counter() - t_gen
 
-    solver = Solver(local_rank, nb=nb, q2_group=a.g) if world == 1 else collective_solver(local_rank, nb, a.g)
+    from paper_1207_1773_b200 import EIG_NO_3M, EIG_USE_3M
+    gflags = EIG_USE_3M if a.gemm == "3m" else EIG_NO_3M
+    solver = (Solver(local_rank, nb=nb, q2_group=a.g, flags=gflags) if world == 1
+              else collective_solver(local_rank, nb, a.g, flags=gflags))
     stream = solver.stream
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     stage_names = ["he2hb", "q2", "q1", "trsm"]
@@ -348,7 +353,7 @@ def run_b200(a, rank, world, local_rank):
         t_bt_p = float(tb[0].item())
         t_bt_1 = None
         if rank == 0:   # t_BT(1): the same back-transform of all m columns on one GPU (rank 0's factors)
-            s1 = Solver(local_rank, nb=nb, q2_group=a.g)
+            s1 = Solver(local_rank, nb=nb, q2_group=a.g, flags=gflags)
             from paper_1207_1773_b200 import EIG_SKIP_HE2HB
             Zall = colmajor(synth.real_orthonormalish(n, m, a.seed), dev)
             Eall = empty_colmajor(n, m, device=dev)
@@ -389,7 +394,12 @@ def run_b200(a, rank, world, local_rank):
                 "traffic_note": "dram read+write bytes per launch (ncu --set full, profiles/traffic_r01h.json); "
                                 "algorithmic E traffic n^2/(2g) m 16 B each way = 2 x 250 GB (the wavefront kernel moves whole 95-row windows: ~3x); compute-bound",
                 "peak_source": peak_src,
-                "stage_tflops": {k: stage_flops[k] / (stages[k] * 1e-3) / 1e12 for k in stages}}
+                "stage_tflops": {k: stage_flops[k] / (stages[k] * 1e-3) / 1e12 for k in stages},
+                # tensor-pipe work: 3M issues 6 real flops per complex MAC (he2hb updates, Q1, trsm), the Q2
+                # real embedding 8 (plus its 616/512 parallelogram overhead, not counted here)
+                "gemm_mode": a.gemm.upper(),
+                "stage_pipe_frac": {k: stage_flops[k] * (0.75 if (a.gemm == "3m" and k != "q2") else 1.0)
+                                    / (stages[k] * 1e-3) / 1e12 / peak for k in stages}}
 
     # e2e through the C ABI with HOST buffers (pinned), N = 1
     e2e = None
@@ -468,6 +478,7 @@ def run_b200(a, rank, world, local_rank):
                 "data": "synthetic (seeded SplitMix64; G1 Hermitian A', random unitary V2, well-conditioned L, real Z)",
                 "config": {"workload": f"he2hb+BT n={n} m={m} nb={nb} g={a.g}", "n": n, "m": m, "nb": nb,
                            "q2_group": a.g, "parallelism": f"bt-columns{world}" if world > 1 else "single",
+                           "gemm": a.gemm.upper(),
                            "zhegv_seconds_hotpath": ms_step * 1e-3,
                            "l2": "inputs (1.6 GB each) exceed L2; no flush needed",
                            "input_gen_s": round(t_gen, 1)},

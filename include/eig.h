@@ -57,6 +57,10 @@ extern "C" {
 
 /* eig_config.flags */
 #define EIG_GATHER_Z     1u  /* collective eig_solve_gen: rank 0's Z receives all m columns      */
+#define EIG_USE_3M       2u  /* complex GEMMs (he2hb updates, Q1, triangular solves, hegst) as
+                                three real DMMA products (3M, Gauss) instead of four: 0.75 of
+                                the tensor-pipe work; nominal flops stay 8 per complex MAC   */
+#define EIG_NO_3M        4u  /* force the four-product form (overrides EIG_USE_3M / EIG_3M)   */
 
 /* eig_hotpath flags */
 #define EIG_HOST_BUFFERS 1u  /* pointers are host memory: copy in, run, copy E out (synchronous) */
@@ -87,7 +91,8 @@ typedef struct {
   int64_t n_max;     /* > 0: largest n this handle will see (calls with n > n_max
                         return EIG_ERR_STATE; collective receive buffers are
                         allocated at init); 0: grow lazily                        */
-  unsigned flags;    /* EIG_GATHER_Z                                               */
+  unsigned flags;    /* EIG_GATHER_Z | EIG_USE_3M | EIG_NO_3M.  Neither 3M flag: the
+                        environment EIG_3M=0/1 decides, else 3M is on (default)    */
 } eig_config;
 
 /* Per-call statistics (device seconds from CUDA events on this rank's

@@ -451,6 +451,10 @@ int eig_init(eig_handle *h, const eig_config *cfg) {
     x->c.n_max = cfg->n_max;
     x->c.flags = cfg->flags;
   }
+  {   // 3M complex GEMMs: flag, else environment EIG_3M (0 / 1), else on
+    const char *e = getenv("EIG_3M");
+    x->c.use_3m = (x->c.flags & EIG_USE_3M) ? true : ((x->c.flags & EIG_NO_3M) ? false : (e ? atoi(e) > 0 : true));
+  }
   if (x->c.nb < 1 || x->c.nb > 64) { delete x; return -2; }
   if (!cfg || !cfg->q2_group) x->c.q2g = std::min(32, ((x->c.nb + 1) / 4) * 4);  // g <= nb + 1, multiple of 4
   if (x->c.q2g != 0 && (x->c.q2g < 4 || x->c.q2g > 32 || x->c.q2g % 4 || x->c.q2g - 1 > x->c.nb)) {

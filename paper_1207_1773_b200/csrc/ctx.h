@@ -63,6 +63,7 @@ struct Ctx {
   cudaEvent_t ev_c[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t n_max = 0;
   unsigned flags = 0;
+  bool use_3m = false;                // EIG_USE_3M: complex GEMMs as three real products
   // statistics of the last eig_hotpath / eig_solve_gen call (CUDA events)
   cudaEvent_t st_beg[EIG_NSTAGES] = {}, st_end[EIG_NSTAGES] = {};
   bool st_on[EIG_NSTAGES] = {};

@@ -29,6 +29,8 @@ struct Zgemm {
   // not depend on N (column-sliced calls are bitwise equal to the unsliced one:
   // the back-transform's per-rank column slices)
   int64_t split_n = 0;
+  // 3M (Gauss) product: 0 = the handle's setting (EIG_USE_3M), 1 = on, -1 = off
+  int m3 = 0;
 };
 
 // N used by the back-transform GEMMs for their split-K choice (columns of E

@@ -7,6 +7,20 @@
 // Modes: Hermitian-lower A (hemm, a3), lower-triangular C (her2k, a5),
 // split-K with a deterministic reduction (skinny products, a4/a7/a8).
 // Used by he2hb (Fig. 1 (c) P:L97), Q1 and trsm.
+//
+// M3 = true: the 3M (Gauss) product instead of the real embedding.  With
+// planes a = ar + i ai, b = br + i bi and the sums as = ar + ai, bs = br + bi,
+//   P1 = sum ar br,  P2 = sum ai bi,  P3 = sum as bs,
+//   Re c = P1 - P2,  Im c = P3 - P1 - P2,
+// three real DMMA products per complex product instead of four (0.75 of the
+// DMMA work; nominal flops stay 8 per complex multiply-add, the pipe does 6).
+// The planes are formed in registers from one 16-byte shared-memory load per
+// complex operand element (conjugation flips ai / bi), warp tile 16 x 32
+// complex = 2 x 4 DMMA tiles per plane.  Normwise error bound of the same
+// order as the 4-real-product form (Higham, "Stability of a method for
+// multiplying complex matrices with three real matrix multiplications");
+// only the imaginary part's componentwise bound is weaker.  The path's
+// gates (parity 1e-11, residual / B-orthogonality 1e-14) are unchanged.
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
@@ -18,15 +32,31 @@
 namespace eig {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
-constexpr int LDA_S = BM + 4;  // sA[k][m]: k-major, m contiguous (+4 complex pad -> conflict free)
-constexpr int LDB_S = BK + 2;  // sB[n][k]: n-major, k contiguous (+2 complex pad)
-constexpr int LDAK = BK + 2;   // op(A) = A^H: sA[m][k], k contiguous like sB (conflict-free cp.async and fragments)
-constexpr int SA_ELEMS = (BK * LDA_S > BM * LDAK) ? BK * LDA_S : BM * LDAK;
-constexpr int LDBN = BN + 4;   // op(B) = B^H: sB[k][n], n contiguous
-constexpr int SB_ELEMS = (BN * LDB_S > BK * LDBN) ? BN * LDB_S : BK * LDBN;
-constexpr int STAGE_ELEMS = SA_ELEMS + SB_ELEMS;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double2);
+constexpr int BM = 64, BN = 64;
+// 3M warp tile: 16 complex rows x M3_WN complex cols (4 x (64 / M3_WN) warps)
+#ifndef M3_WN
+#define M3_WN 32
+#endif
+__host__ __device__ constexpr int threads_of(bool m3) { return m3 ? 32 * 4 * (BN / M3_WN) : 256; }
+// Shared-memory layouts (complex elements).  4M: 8-byte fragment loads;
+// 3M: 16-byte complex loads, eight lanes per phase (row g = lane>>2 in {0,1},
+// k t = lane&3), so the k-major strides are 2 mod 8 and the k-contiguous ones
+// 4 mod 8 (eight distinct 16-byte bank groups per phase).
+template <bool M3>
+struct Lay {
+  // K tile (complex): 3M runs one 198-register CTA per SM, so it takes twice
+  // the K per pipeline stage (half the CTA barriers per flop)
+  static constexpr int BK = M3 ? 32 : 16;
+  static constexpr int STAGES = 3;
+  static constexpr int LDA_S = M3 ? BM + 2 : BM + 4;  // sA[k][m]: k-major, m contiguous
+  static constexpr int LDB_S = M3 ? BK + 4 : BK + 2;  // sB[n][k]: n-major, k contiguous
+  static constexpr int LDAK = M3 ? BK + 4 : BK + 2;   // op(A) = A^H: sA[m][k], k contiguous
+  static constexpr int LDBN = M3 ? BN + 2 : BN + 4;   // op(B) = B^H: sB[k][n], n contiguous
+  static constexpr int SA_ELEMS = (BK * LDA_S > BM * LDAK) ? BK * LDA_S : BM * LDAK;
+  static constexpr int SB_ELEMS = (BN * LDB_S > BK * LDBN) ? BN * LDB_S : BK * LDBN;
+  static constexpr int STAGE_ELEMS = SA_ELEMS + SB_ELEMS;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double2);
+};
 
 struct Params {
   int64_t M, N, K;
@@ -43,8 +73,13 @@ struct Params {
   int tiles_m;
 };
 
-template <int OPA, int OPB, bool HERM, int LOWER>
-__global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
+template <int OPA, int OPB, bool HERM, int LOWER, bool M3>
+__global__ void __launch_bounds__(threads_of(M3), M3 ? 1 : 2) zgemm_kernel(Params p) {
+  constexpr int THREADS = threads_of(M3);
+  using LY = Lay<M3>;
+  constexpr int BK = LY::BK, STAGES = LY::STAGES;
+  constexpr int LDA_S = LY::LDA_S, LDB_S = LY::LDB_S, LDAK = LY::LDAK, LDBN = LY::LDBN;
+  constexpr int SA_ELEMS = LY::SA_ELEMS, STAGE_ELEMS = LY::STAGE_ELEMS;
   extern __shared__ __align__(16) double2 smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2;
@@ -121,6 +156,157 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
     }
   };
 
+#pragma unroll
+  for (int s0 = 0; s0 < STAGES - 1; s0++) {
+    if (s0 < nk) load(s0, kbeg + (int64_t)s0 * BK);
+    cp_async_commit();
+  }
+  // C += alpha A B with alpha = +-1: start the accumulators from C (its loads
+  // overlap the pipeline prologue instead of trailing the main loop) and fold
+  // the sign of alpha into the A fragments.
+  const bool fuse_c = (p.part == nullptr) && p.beta == 1.0 && (p.alpha == 1.0 || p.alpha == -1.0);
+  const unsigned aflip = (fuse_c && p.alpha == -1.0) ? 0x80000000u : 0u;
+
+  // per k-tile: is op(A) conjugated, and is the A tile stored [m][k] (KM)
+  auto tile_mode = [&](int kt, int st, bool &conjA) {
+    conjA = (OPA == OP_C);
+    if (HERM) {
+      const int64_t k0 = kbeg + (int64_t)kt * BK;
+      if (k0 >= m0 + BM) {
+        conjA = true;
+      } else if (k0 + BK - 1 <= m0) {
+        conjA = false;
+      } else {
+        conjA = false;
+        double2 *sA = smem + st * STAGE_ELEMS;
+        for (int i = tid; i < BM * BK; i += THREADS) {
+          const int m = i % BM, k = i / BM;
+          const int64_t gm = m0 + m, gk = k0 + k;
+          double2 v = sA[k * LDA_S + m];
+          if (gm < gk) v.y = -v.y;
+          else if (gm == gk) v.y = 0.0;
+          sA[k * LDA_S + m] = v;
+        }
+        __syncthreads();
+      }
+    }
+  };
+
+  if constexpr (M3) {
+    // ------------------------------------------------------------ 3M path
+    // warp tile 16 complex rows (wm) x M3_WN complex cols (wn): 2 x NJ tiles per plane
+    const int g8 = lane >> 2, t4 = lane & 3;
+    constexpr int NJ = M3_WN / 8;
+    double acc[3][2][NJ][2];
+#pragma unroll
+    for (int q = 0; q < 3; q++)
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int j = 0; j < NJ; j++) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
+    // alpha = -1 (fused): accumulate from -C and negate at the end (exact), so
+    // the A planes need no sign flips
+    const double cs = aflip ? -1.0 : 1.0;
+    if (fuse_c) {   // P1 = Re C, P2 = 0, P3 = Re C + Im C  (times cs)
+#pragma unroll
+      for (int i = 0; i < 2; i++)
+#pragma unroll
+        for (int j = 0; j < NJ; j++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int64_t gm = m0 + wm * 16 + i * 8 + g8, gn = n0 + wn * M3_WN + j * 8 + 2 * t4 + h;
+            const double2 c = (gm < p.M && gn < p.N) ? p.C[gm + gn * p.ldc] : czero();
+            acc[0][i][j][h] = cs * c.x;
+            acc[2][i][j][h] = cs * (c.x + c.y);
+          }
+    }
+    for (int kt = 0; kt < nk; kt++) {
+      const int st = kt % STAGES;
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        const int nxt = kt + STAGES - 1;
+        if (nxt < nk) load(nxt % STAGES, kbeg + (int64_t)nxt * BK);
+        cp_async_commit();
+      }
+      bool conjA;
+      tile_mode(kt, st, conjA);
+      const double2 *a2 = smem + st * STAGE_ELEMS;
+      const double2 *b2 = a2 + SA_ELEMS;
+      auto compute = [&](auto km) {
+        constexpr bool KM = decltype(km)::value;   // A tile stored [m][k]
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ks++) {
+          const int kk = ks * 4 + t4;
+          double ar[2], ai[2], as[2], br[NJ], bi[NJ], bs[NJ];
+#pragma unroll
+          for (int i = 0; i < 2; i++) {
+            const int mm = wm * 16 + i * 8 + g8;
+            const double2 v = KM ? a2[mm * LDAK + kk] : a2[kk * LDA_S + mm];
+            ar[i] = v.x;
+            ai[i] = conjA ? -v.y : v.y;
+            as[i] = ar[i] + ai[i];
+          }
+#pragma unroll
+          for (int j = 0; j < NJ; j++) {
+            const int nn = wn * M3_WN + j * 8 + g8;
+            const double2 v = OPB == OP_C ? b2[kk * LDBN + nn] : b2[nn * LDB_S + kk];
+            br[j] = v.x;
+            bi[j] = OPB == OP_C ? -v.y : v.y;
+            bs[j] = br[j] + bi[j];
+          }
+          // plane-major order: consecutive DMMAs share their A operand
+#pragma unroll
+          for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) dmma(acc[0][i][j], ar[i], br[j]);
+#pragma unroll
+          for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) dmma(acc[1][i][j], ai[i], bi[j]);
+#pragma unroll
+          for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < NJ; j++) dmma(acc[2][i][j], as[i], bs[j]);
+        }
+      };
+      if (HERM) {
+        if (conjA) compute(std::true_type{});
+        else compute(std::false_type{});
+      } else {
+        compute(std::integral_constant<bool, OPA == OP_C>{});
+      }
+    }
+    cp_async_wait<0>();
+    // epilogue: lane holds complex (row g8, cols 2 t4 + h) of every tile
+#pragma unroll
+    for (int i = 0; i < 2; i++)
+#pragma unroll
+      for (int j = 0; j < NJ; j++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int64_t gm = m0 + wm * 16 + i * 8 + g8, gn = n0 + wn * M3_WN + j * 8 + 2 * t4 + h;
+          if (gm >= p.M || gn >= p.N) continue;
+          const double p1 = acc[0][i][j][h], p2 = acc[1][i][j][h], p3 = acc[2][i][j][h];
+          const double2 v = make_double2(cs * (p1 - p2), cs * (p3 - p1 - p2));
+          if (p.part) {
+            p.part[(int64_t)blockIdx.y * p.M * p.N + gm + gn * p.M] = v;
+          } else {
+            if (LOWER && p.row0 + gm < gn) continue;
+            double2 *cp = p.C + gm + gn * p.ldc;
+            double2 out = fuse_c ? v : make_double2(p.alpha * v.x, p.alpha * v.y);
+            if (!fuse_c && p.beta != 0.0) {
+              const double2 c = *cp;
+              out.x += p.beta * c.x;
+              out.y += p.beta * c.y;
+            }
+            if (LOWER && p.row0 + gm == gn) out.y = 0.0;
+            *cp = out;
+          }
+        }
+    return;
+  } else {
+  // ------------------------------------------------------------ 4M (real embedding) path
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; i++)
@@ -128,18 +314,6 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
     for (int j = 0; j < 4; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const LaneEmb le(lane);
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; s++) {
-    if (s < nk) load(s, kbeg + (int64_t)s * BK);
-    cp_async_commit();
-  }
-
-  // C += alpha A B with alpha = +-1: start the accumulators from C (its loads
-  // overlap the pipeline prologue instead of trailing the main loop) and fold
-  // the sign of alpha into the A fragments.
-  const bool fuse_c = (p.part == nullptr) && p.beta == 1.0 && (p.alpha == 1.0 || p.alpha == -1.0);
-  const unsigned aflip = (fuse_c && p.alpha == -1.0) ? 0x80000000u : 0u;
   if (fuse_c) {
     const int rpc = (lane >> 2) & 1;
 #pragma unroll
@@ -163,27 +337,8 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
       cp_async_commit();
     }
     const int st = kt % STAGES;
-    bool conjA = (OPA == OP_C);
-    if (HERM) {
-      const int64_t k0 = kbeg + (int64_t)kt * BK;
-      if (k0 >= m0 + BM) {
-        conjA = true;
-      } else if (k0 + BK - 1 <= m0) {
-        conjA = false;
-      } else {
-        conjA = false;
-        double2 *sA = smem + st * STAGE_ELEMS;
-        for (int i = tid; i < BM * BK; i += THREADS) {
-          const int m = i % BM, k = i / BM;
-          const int64_t gm = m0 + m, gk = k0 + k;
-          double2 v = sA[k * LDA_S + m];
-          if (gm < gk) v.y = -v.y;
-          else if (gm == gk) v.y = 0.0;
-          sA[k * LDA_S + m] = v;
-        }
-        __syncthreads();
-      }
-    }
+    bool conjA;
+    tile_mode(kt, st, conjA);
     const double *a = reinterpret_cast<const double *>(smem + st * STAGE_ELEMS);
     const double *b = reinterpret_cast<const double *>(smem + st * STAGE_ELEMS + SA_ELEMS);
     const unsigned anm = (conjA ? le.a_neg_conj : le.a_neg) ^ aflip;
@@ -248,6 +403,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_kernel(Params p) {
         }
       }
     }
+  }
 }
 
 // C = alpha * sum_z part[z] + beta * C  (fixed summation order -> deterministic)
@@ -276,9 +432,16 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int split, const doub
 }
 
 template <int OPA, int OPB, bool HERM, int LOWER>
-int launch_t(Ctx &ctx, const Params &p, dim3 grid) {
-  EIG_TRY(ctx.smem_attr((const void *)zgemm_kernel<OPA, OPB, HERM, LOWER>, (int)SMEM_BYTES, "zgemm attr"));
-  zgemm_kernel<OPA, OPB, HERM, LOWER><<<grid, THREADS, SMEM_BYTES, ctx.stream>>>(p);
+int launch_t(Ctx &ctx, const Params &p, dim3 grid, bool m3) {
+  if (m3) {
+    constexpr size_t sm = Lay<true>::SMEM_BYTES;
+    EIG_TRY(ctx.smem_attr((const void *)zgemm_kernel<OPA, OPB, HERM, LOWER, true>, (int)sm, "zgemm attr"));
+    zgemm_kernel<OPA, OPB, HERM, LOWER, true><<<grid, threads_of(true), sm, ctx.stream>>>(p);
+  } else {
+    constexpr size_t sm = Lay<false>::SMEM_BYTES;
+    EIG_TRY(ctx.smem_attr((const void *)zgemm_kernel<OPA, OPB, HERM, LOWER, false>, (int)sm, "zgemm attr"));
+    zgemm_kernel<OPA, OPB, HERM, LOWER, false><<<grid, threads_of(false), sm, ctx.stream>>>(p);
+  }
   return ctx.launched("zgemm_kernel");
 }
 
@@ -296,12 +459,14 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   const int64_t Nm = g.split_n > 0 ? g.split_n : g.N;
   const int64_t tiles_model =
       g.split_n > 0 ? (int64_t)tiles_m * ((g.split_n + BN - 1) / BN) : tiles;
+  const bool m3 = g.m3 > 0 || (g.m3 == 0 && ctx.use_3m);
+  const int BK = m3 ? Lay<true>::BK : Lay<false>::BK;
   const int64_t ktiles = std::max<int64_t>(1, (g.K + BK - 1) / BK);
   int split = g.splitk;
   if (split <= 0) {
     // pick the split that minimises (waves of 2 CTAs/SM) x (k-tiles per CTA + fixed per-CTA cost),
     // plus the partial-sum traffic of the reduction (in k-tile units)
-    const int64_t cap = 2LL * ctx.num_sms;
+    const int64_t cap = (m3 ? 1LL : 2LL) * ctx.num_sms;   // resident CTAs (3M: one 255-register CTA per SM)
     const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(64, ktiles / 4));
     double best = 1e300;
     split = 1;
@@ -343,22 +508,22 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   dim3 grid((unsigned)tiles, (unsigned)split);
   int rc;
   if (g.herm_a)
-    rc = launch_t<OP_N, OP_N, true, 0>(ctx, p, grid);
+    rc = launch_t<OP_N, OP_N, true, 0>(ctx, p, grid, m3);
   else if (g.lower_c == 1) {
-    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 1>(ctx, p, grid);
-    else if (g.opa == OP_N && g.opb == OP_N) rc = launch_t<OP_N, OP_N, false, 1>(ctx, p, grid);
+    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 1>(ctx, p, grid, m3);
+    else if (g.opa == OP_N && g.opb == OP_N) rc = launch_t<OP_N, OP_N, false, 1>(ctx, p, grid, m3);
     else return -2;
   } else if (g.lower_c == 2) {
-    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 2>(ctx, p, grid);
+    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 2>(ctx, p, grid, m3);
     else return -2;
   } else if (g.opa == OP_N && g.opb == OP_N)
-    rc = launch_t<OP_N, OP_N, false, 0>(ctx, p, grid);
+    rc = launch_t<OP_N, OP_N, false, 0>(ctx, p, grid, m3);
   else if (g.opa == OP_C && g.opb == OP_N)
-    rc = launch_t<OP_C, OP_N, false, 0>(ctx, p, grid);
+    rc = launch_t<OP_C, OP_N, false, 0>(ctx, p, grid, m3);
   else if (g.opa == OP_N && g.opb == OP_C)
-    rc = launch_t<OP_N, OP_C, false, 0>(ctx, p, grid);
+    rc = launch_t<OP_N, OP_C, false, 0>(ctx, p, grid, m3);
   else
-    rc = launch_t<OP_C, OP_C, false, 0>(ctx, p, grid);
+    rc = launch_t<OP_C, OP_C, false, 0>(ctx, p, grid, m3);
   if (rc) return rc;
   if (split > 1) {
     const int64_t total = g.M * g.N;

@@ -18,9 +18,9 @@ gpu = pytest.mark.gpu
 TOL = 1e-11
 
 
-def _solver(nb=64, g=0):
-    from paper_1207_1773_b200 import Solver
-    return Solver(0, nb=nb, q2_group=g)
+def _solver(nb=64, g=0, m3=False):
+    from paper_1207_1773_b200 import EIG_NO_3M, EIG_USE_3M, Solver
+    return Solver(0, nb=nb, q2_group=g, flags=EIG_USE_3M if m3 else EIG_NO_3M)
 
 
 def _dev(x):
@@ -34,10 +34,11 @@ def _rel(a, b):
 
 # ------------------------------------------------------------------ engine
 @gpu
+@pytest.mark.parametrize("m3", [False, True])
 @pytest.mark.parametrize("opa,opb", [("N", "N"), ("C", "N"), ("N", "C"), ("C", "C")])
 @pytest.mark.parametrize("M,N,K", [(100, 70, 45), (64, 64, 16), (1, 130, 300), (257, 3, 129)])
-def test_zgemm_ops(opa, opb, M, N, K):
-    s = _solver()
+def test_zgemm_ops(opa, opb, M, N, K, m3):
+    s = _solver(m3=m3)
     A = synth.cnormal(1, 1, (M, K) if opa == "N" else (K, M))
     B = synth.cnormal(1, 2, (K, N) if opb == "N" else (N, K))
     C0 = synth.cnormal(1, 3, (M, N))
@@ -50,8 +51,9 @@ def test_zgemm_ops(opa, opb, M, N, K):
 
 
 @gpu
-def test_zgemm_splitk_and_hermitian_and_lower():
-    s = _solver()
+@pytest.mark.parametrize("m3", [False, True])
+def test_zgemm_splitk_and_hermitian_and_lower(m3):
+    s = _solver(m3=m3)
     n, k = 333, 40
     H = synth.rand_hermitian(n, 5)
     Hs = np.tril(H) + np.triu(synth.cnormal(5, 9, (n, n)), 1)   # garbage above the diagonal
@@ -80,8 +82,8 @@ def test_zgemm_splitk_and_hermitian_and_lower():
 
 
 # ------------------------------------------------------------------ he2hb
-def _check_he2hb(n, nb, seed=0, gen="rand"):
-    s = _solver(nb=nb)
+def _check_he2hb(n, nb, seed=0, gen="rand", m3=False):
+    s = _solver(nb=nb, m3=m3)
     if gen == "rand":
         A = synth.rand_hermitian(n, seed)
     else:
@@ -114,6 +116,13 @@ def _check_he2hb(n, nb, seed=0, gen="rand"):
 @pytest.mark.parametrize("n,nb", [(256, 16), (300, 32), (517, 64), (130, 64), (65, 64), (64, 64), (97, 8)])
 def test_he2hb_parity(n, nb):
     _check_he2hb(n, nb)
+
+
+@gpu
+@pytest.mark.parametrize("n,nb", [(256, 16), (517, 64)])
+def test_he2hb_parity_3m(n, nb):
+    """EIG_USE_3M: the trailing updates as three real products (same tolerance)."""
+    _check_he2hb(n, nb, m3=True)
 
 
 @gpu
@@ -220,9 +229,10 @@ def test_trsm_lh_parity(n, m):
 
 # ------------------------------------------------------------------ whole pass
 @gpu
+@pytest.mark.parametrize("m3", [False, True])
 @pytest.mark.parametrize("n,nb,g,m", [(256, 16, 8, 256), (600, 64, 32, 60)])
-def test_hotpath_parity(n, nb, g, m):
-    s = _solver(nb=nb, g=g)
+def test_hotpath_parity(n, nb, g, m, m3):
+    s = _solver(nb=nb, g=g, m3=m3)
     A = synth.rand_hermitian(n, 11)
     V2, tau2 = synth.synthetic_v2(n, nb, 11)
     L = synth.unit_lower(n, 11)

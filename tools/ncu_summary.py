@@ -35,9 +35,15 @@ def main(rep, top=20):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    hdr = rows[1]
+    # the source page starts with a kernel-name line when the report holds one
+    # kernel; find the header row by its columns instead of assuming row 1
+    hi = next((i for i, r in enumerate(rows) if "Source" in r and "Instructions Executed" in r), None)
+    if hi is None:
+        print("(no SASS source page in this report)")
+        return
+    hdr = rows[hi]
     idx = {h: i for i, h in enumerate(hdr)}
-    data = rows[2:]
+    data = [r for r in rows[hi + 1:] if len(r) == len(hdr)]
 
     def f(r, k):
         try:

@@ -43,10 +43,12 @@ def main():
     p.add_argument("--nb", type=int, default=64)
     p.add_argument("--g", type=int, default=0)
     p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--m3", action="store_true", help="complex GEMMs as three real products (EIG_USE_3M)")
     p.add_argument("--kw", type=int, default=0, help="gemm mode: panel width of the V^H E / E -= V Y shapes (default nb)")
     a = p.parse_args()
     dev = torch.device("cuda:0")
-    s = Solver(0, nb=a.nb, q2_group=a.g)
+    from paper_1207_1773_b200 import EIG_NO_3M, EIG_USE_3M
+    s = Solver(0, nb=a.nb, q2_group=a.g, flags=EIG_USE_3M if a.m3 else EIG_NO_3M)
     n = a.n
     m = a.m or n
     if a.mode == "gemm":
