@@ -161,6 +161,18 @@ int64_t eig_v2_slots(int64_t n, int nb);
  * Uses nb from the handle's config. */
 int eig_he2hb(eig_handle h, int64_t n, void *A, int64_t lda, void *tau, void *T);
 
+/* ------------------------------------------------------------------ NEXT-4
+ * The same reduction computed by the 1D block-cyclic DISTRIBUTED algorithm
+ * (§6; csrc/he2hb_dist.cu) with `nranks` virtual ranks on this GPU:
+ * rank r owns the full columns of the nb-wide blocks b = r mod nranks, the
+ * panel runs on its owner, V / T / tau are broadcast, W = A22 V is the sum of
+ * the ranks' partial products (allreduce), each rank updates its own columns.
+ * The collectives are device copies and a fixed-order sum here; over NCCL in
+ * the collective path.  Arguments and output layout as eig_he2hb (A
+ * Hermitian, lower read; overwritten with band + V1).  Synchronous.
+ * Library-internal scratch: nranks * n * (n / nranks + 6 nb) + n^2 complex128. */
+int eig_he2hb_sim(eig_handle h, int64_t n, int nranks, void *A, int64_t lda, void *tau, void *T);
+
 /* ------------------------------------------------------------------ a7
  * E <- Q1 E: E is n x m (lde >= n), A/T as produced by eig_he2hb. */
 int eig_apply_q1(eig_handle h, int64_t n, const void *A, int64_t lda, const void *T, void *E, int64_t lde,

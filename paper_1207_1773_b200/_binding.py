@@ -80,6 +80,7 @@ def lib():
             "eig_zgemm": (C.c_int, [h, C.c_char, C.c_char, I, I, I, D, P, I, P, I, D, P, I, C.c_int, C.c_int]),
             "eig_solve_gen": (C.c_int, [h, I, P, I, P, I, C.c_int, D, I, I, P, P, I, P, P]),
             "eig_get_unique_id": (C.c_int, [P]),
+            "eig_he2hb_sim": (C.c_int, [h, I, C.c_int, P, I, P, P]),
             "eig_column_slice": (C.c_int, [I, C.c_int, C.c_int, C.POINTER(I), C.POINTER(I)]),
             "eig_resolve_range": (C.c_int, [I, C.c_int, D, I, I, C.POINTER(I), C.POINTER(I), C.POINTER(I)]),
             "eig_last_stats": (C.c_int, [h, P]),
@@ -101,7 +102,8 @@ def exported_symbols():
     return ["eig_init", "eig_finalize", "eig_strerror", "eig_last_cuda_error", "eig_launch_count", "eig_sync",
             "eig_num_panels", "eig_v2_slots", "eig_he2hb", "eig_apply_q1", "eig_apply_q2", "eig_trsm_lh",
             "eig_hotpath", "eig_zgemm", "eig_solve_gen", "eig_debug_q2_profile", "eig_hb2st", "eig_stedc", "eig_potrf",
-            "eig_hegst", "eig_get_unique_id", "eig_column_slice", "eig_resolve_range", "eig_last_stats"]
+            "eig_hegst", "eig_get_unique_id", "eig_column_slice", "eig_resolve_range", "eig_last_stats",
+            "eig_he2hb_sim"]
 
 
 def unique_id() -> bytes:
@@ -265,6 +267,17 @@ class Solver:
         tau = torch.zeros(max(K * self.nb, 1), dtype=torch.complex128, device=A.device)
         T = torch.zeros(max(K * self.nb * self.nb, 1), dtype=torch.complex128, device=A.device)
         self._check(lib().eig_he2hb(self.h, n, _ptr(A), _ld(A), _ptr(tau), _ptr(T)))
+        return tau, T
+
+    def he2hb_sim(self, A: torch.Tensor, nranks: int):
+        """NEXT-4: he2hb by the 1D block-cyclic distributed algorithm with
+        `nranks` virtual ranks on this GPU (same outputs as he2hb)."""
+        n = A.shape[0]
+        self._mat(A, "A", n, n)
+        K = num_panels(n, self.nb)
+        tau = torch.zeros(max(K * self.nb, 1), dtype=torch.complex128, device=A.device)
+        T = torch.zeros(max(K * self.nb * self.nb, 1), dtype=torch.complex128, device=A.device)
+        self._check(lib().eig_he2hb_sim(self.h, n, nranks, _ptr(A), _ld(A), _ptr(tau), _ptr(T)))
         return tau, T
 
     def hb2st(self, A):

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libeigb200.so")
-SOURCES = ["abi.cu", "zgemm.cu", "panel.cu", "bt.cu", "q2.cu", "q2w.cu", "hb2st.cu", "dgemm.cu", "stedc.cu", "frontend.cu", "comm.cu"]
+SOURCES = ["abi.cu", "zgemm.cu", "panel.cu", "bt.cu", "q2.cu", "q2w.cu", "hb2st.cu", "dgemm.cu", "stedc.cu", "frontend.cu", "comm.cu", "he2hb_dist.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

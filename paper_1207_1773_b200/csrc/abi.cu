@@ -562,6 +562,17 @@ int eig_he2hb(eig_handle h, int64_t n, void *A, int64_t lda, void *tau, void *T)
   return he2hb_run(h->c, n, (double2 *)A, lda, (double2 *)tau, (double2 *)T);
 }
 
+int eig_he2hb_sim(eig_handle h, int64_t n, int nranks, void *A, int64_t lda, void *tau, void *T) {
+  EIG_TRY(valid(h));
+  if (n < 0) return -2;
+  if (nranks < 1) return -3;
+  if (!A && n > 0) return -4;
+  if (lda < std::max<int64_t>(1, n)) return -5;
+  if (num_panels(n, h->c.nb) > 0 && (!tau || !T)) return !tau ? -6 : -7;
+  cudaSetDevice(h->c.device);
+  return he2hb_sim(h->c, n, nranks, (double2 *)A, lda, (double2 *)tau, (double2 *)T);
+}
+
 int eig_apply_q1(eig_handle h, int64_t n, const void *A, int64_t lda, const void *T, void *E, int64_t lde, int64_t m) {
   EIG_TRY(valid(h));
   if (n < 0) return -2;

@@ -1,0 +1,333 @@
+// he2hb_dist.cu — NEXT-4: reduction to band form with the columns of the
+// Hermitian matrix distributed 1D block-cyclically over P ranks (§6:
+// "The data on the GPUs is distributed in a 1D block cyclic way"; the
+// trigger and the projection are in DESIGN.md §8).
+//
+// Rank r owns the FULL columns (both triangles) of the nb-wide column blocks
+// b with b mod P == r, stored in order in a local n x nloc array (ld n).
+// Step k (panel = block k, owner o = k mod P, trailing rows/cols r0 = (k+1) nb):
+//   owner:  panel QR + T of A[r0:, block k]                (panel_qr_kernel, a1-a2)
+//   bcast:  V_k (s x nb), T_k, tau_k from o                (every rank keeps them: V1, T1 for the BT)
+//   all:    W_r = A[r0:, J_r] V_k[J_r]                     (J_r = r's trailing columns, one zgemm)
+//   allreduce W = sum_r W_r                                 (a3: W = A22 V)
+//   all:    W <- W T, M = T^H V^H W, X = W - 1/2 V M        (a4, replicated)
+//   all:    A[r0:, J_r] -= V X[J_r]^H + X V[J_r]^H          (a5 on the owned full columns)
+// Every rank therefore does 24 s^2 nb / P flops per step instead of the
+// single-GPU 16 s^2 nb (full columns instead of the lower triangle).
+//
+// The collectives go through `DistOps`: NCCL on the handle's communicator
+// for real ranks, or, for P "virtual" ranks on ONE GPU (eig_he2hb_sim, the
+// arithmetic check), device copies and a fixed-order sum over the ranks'
+// buffers.  Both run the same per-rank local code below.
+#include <nccl.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "kernels.h"
+#include "stages.h"
+
+namespace eig {
+namespace {
+
+// global column of local column lc of rank r (1D block-cyclic, block nb)
+__host__ __device__ __forceinline__ int64_t gcol_of(int64_t lc, int r, int P, int nb) {
+  return ((lc / nb) * P + r) * nb + lc % nb;
+}
+// local columns of rank r
+int64_t ncols_of(int64_t n, int r, int P, int nb) {
+  const int64_t NB = (n + nb - 1) / nb;
+  int64_t c = 0;
+  for (int64_t b = r; b < NB; b += P) c += std::min<int64_t>(nb, n - b * nb);
+  return c;
+}
+// first local column of rank r whose global column is >= g0 (g0 a block start)
+int64_t first_local_ge(int64_t g0, int r, int P, int nb) {
+  const int64_t b0 = g0 / nb;
+  int64_t b = b0 + ((r - b0 % P) % P + P) % P;   // smallest owned block >= b0
+  return (b / P) * nb;
+}
+
+// Mg[lr, :] = M[gcol(lc0 + lr) - r0, :]  (rows of an s x w matrix, ld ldm,
+// for the trailing local columns of rank r), Mg ld ldg
+__global__ void gather_rows_kernel(int64_t nl, int64_t lc0, int r, int P, int nb, int64_t r0, int w,
+                                   const double2 *M, int64_t ldm, double2 *Mg, int64_t ldg) {
+  const int64_t total = nl * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lr = e % nl;
+    const int col = (int)(e / nl);
+    Mg[lr + col * ldg] = M[(gcol_of(lc0 + lr, r, P, nb) - r0) + col * ldm];
+  }
+}
+
+// local <-> global full columns (block-cyclic), for the virtual-rank check
+__global__ void cyclic_copy_kernel(int64_t n, int r, int P, int nb, int64_t nl, double2 *G, int64_t ldg,
+                                   double2 *Lc, bool to_local) {
+  const int64_t total = n * nl;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e % n, lc = e / n;
+    double2 *g = G + row + gcol_of(lc, r, P, nb) * ldg;
+    if (to_local) Lc[e] = *g;
+    else *g = Lc[e];
+  }
+}
+
+// V_k tails into the he2hb layout of the (n x n, ld) V1 holder: column k nb + j,
+// rows (k+1) nb + j + 1 .. n-1  <-  V[j+1.., j]
+__global__ void place_v_kernel(int64_t s, int nb, const double2 *V, int64_t ldv, double2 *A, int64_t lda) {
+  const int64_t total = s * nb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % s;
+    const int j = (int)(e / s);
+    if (i > j) A[i + j * lda] = V[i + j * ldv];
+  }
+}
+
+// out = sum_q in[q] (fixed order q = 0..P-1)
+__global__ void sum_ranks_kernel(int64_t count, int P, double2 *const *in, double2 *out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = in[0][e];
+    for (int q = 1; q < P; q++) acc = cadd(acc, in[q][e]);
+    out[e] = acc;
+  }
+}
+
+int grid_for(Ctx &c, int64_t total) { return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 8LL * c.num_sms)); }
+
+}  // namespace
+
+// Per-rank state of the distributed reduction.
+struct DistRank {
+  int r;                 // global rank id
+  double2 *Aloc;         // n x nloc, ld n (full columns of the owned blocks)
+  int64_t nloc;
+  double2 *V1;           // n x n, ld n: V1 tails in the he2hb layout (receives every panel's V)
+  double2 *tau, *T;      // K nb, K nb nb
+  double2 *Vb, *Wb, *Xb, *Gb, *Sm;   // work: V (s x nb), W / X (s x nb), gathered rows, small
+  double2 *Wpart;        // this rank's partial W
+};
+
+// The collectives of the distributed reduction.  For real ranks `ranks` has
+// one entry (this process); for virtual ranks all P live on this GPU.
+struct DistOps {
+  Ctx *c;
+  bool virt;
+  int P;
+  std::vector<DistRank> *ranks;
+  double2 **d_ptrs;      // virtual: device array of P pointers (sum_ranks_kernel)
+  // every rank's buf <- owner's buf (count complex)
+  int bcast(std::vector<double2 *> bufs, size_t count, int owner) {
+    if (count == 0) return 0;
+    if (virt) {
+      for (int q = 0; q < P; q++)
+        if (q != owner)
+          EIG_TRY(c->check(cudaMemcpyAsync(bufs[q], bufs[owner], count * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                           c->stream), "virtual bcast"));
+      return 0;
+    }
+    c->st.bytes_comm += (int64_t)(count * sizeof(double2));
+    if (ncclBroadcast(bufs[0], bufs[0], count * 2, ncclDouble, owner, (ncclComm_t)c->nccl, c->stream) != ncclSuccess) {
+      c->last_err = "ncclBroadcast (he2hb_dist)";
+      return EIG_ERR_NCCL;
+    }
+    return 0;
+  }
+  // every rank's out <- sum of every rank's in
+  int allreduce(std::vector<double2 *> in, std::vector<double2 *> out, size_t count) {
+    if (count == 0) return 0;
+    if (virt) {
+      EIG_TRY(c->check(cudaMemcpyAsync(d_ptrs, in.data(), P * sizeof(double2 *), cudaMemcpyHostToDevice, c->stream),
+                       "virtual allreduce ptrs"));
+      sum_ranks_kernel<<<grid_for(*c, (int64_t)count), 256, 0, c->stream>>>((int64_t)count, P, d_ptrs, out[0]);
+      EIG_TRY(c->launched("sum_ranks_kernel"));
+      for (int q = 1; q < P; q++)
+        EIG_TRY(c->check(cudaMemcpyAsync(out[q], out[0], count * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream),
+                         "virtual allreduce copy"));
+      return 0;
+    }
+    c->st.bytes_comm += (int64_t)(count * sizeof(double2));
+    if (ncclAllReduce(in[0], out[0], count * 2, ncclDouble, ncclSum, (ncclComm_t)c->nccl, c->stream) != ncclSuccess) {
+      c->last_err = "ncclAllReduce (he2hb_dist)";
+      return EIG_ERR_NCCL;
+    }
+    return 0;
+  }
+};
+
+// The distributed reduction over the ranks in `ops.ranks` (see the header).
+int he2hb_dist_run(Ctx &c, int64_t n, DistOps &ops) {
+  const int nb = c.nb, P = ops.P;
+  const int64_t K = num_panels(n, nb);
+  std::vector<DistRank> &R = *ops.ranks;
+  const int nv = (int)R.size();
+  auto bufs = [&](auto f) {
+    std::vector<double2 *> v(nv);
+    for (int q = 0; q < nv; q++) v[q] = f(R[q]);
+    return v;
+  };
+  auto local_of = [&](int owner) -> int {   // index in R of global rank `owner`, or -1
+    for (int q = 0; q < nv; q++)
+      if (R[q].r == owner) return q;
+    return -1;
+  };
+  for (int64_t k = 0; k < K; k++) {
+    const int64_t r0 = (k + 1) * nb, s = n - r0;
+    const int owner = (int)(k % P);
+    const int qo = local_of(owner);
+    const int nref = (int)std::min<int64_t>(nb, s);
+    // a1-a2: panel on its owner (explicit V into Vb, ld s)
+    if (qo >= 0) {
+      DistRank &o = R[qo];
+      const int64_t lc = (k / P) * nb;   // local column of block k
+      EIG_TRY(panel_qr(c, o.Aloc + r0 + lc * n, n, s, nb, o.tau + k * nb, o.T + k * nb * nb, o.Vb, nullptr, s,
+                       c.stream));
+    }
+    // V_k, T_k, tau_k to every rank (the BT needs them all: V1 and T1 stay replicated)
+    EIG_TRY(ops.bcast(bufs([](DistRank &d) { return d.Vb; }), (size_t)s * nb, owner));
+    EIG_TRY(ops.bcast(bufs([&](DistRank &d) { return d.T + k * nb * nb; }), (size_t)nb * nb, owner));
+    EIG_TRY(ops.bcast(bufs([&](DistRank &d) { return d.tau + k * nb; }), (size_t)nb, owner));
+    for (auto &d : R) {
+      place_v_kernel<<<grid_for(c, s * nref), 256, 0, c.stream>>>(s, nref, d.Vb, s, d.V1 + r0 + k * nb * n, n);
+      EIG_TRY(c.launched("place_v_kernel"));
+    }
+    // a3: W_r = A[r0:, J_r] V[J_r]
+    std::vector<int64_t> lc0(nv), nl(nv);
+    for (int q = 0; q < nv; q++) {
+      DistRank &d = R[q];
+      lc0[q] = std::min<int64_t>(d.nloc, first_local_ge(r0, d.r, P, nb));
+      nl[q] = d.nloc - lc0[q];
+      if (nl[q] > 0) {
+        gather_rows_kernel<<<grid_for(c, nl[q] * nb), 256, 0, c.stream>>>(nl[q], lc0[q], d.r, P, nb, r0, nb, d.Vb, s,
+                                                                           d.Gb, nl[q]);
+        EIG_TRY(c.launched("gather_rows_kernel"));
+        Zgemm g;
+        g.M = s; g.N = nb; g.K = nl[q]; g.A = d.Aloc + r0 + lc0[q] * n; g.lda = n; g.B = d.Gb; g.ldb = nl[q];
+        g.C = d.Wpart; g.ldc = s;
+        EIG_TRY(zgemm(c, g));
+      } else {
+        EIG_TRY(c.check(cudaMemsetAsync(d.Wpart, 0, (size_t)s * nb * sizeof(double2), c.stream), "W = 0"));
+      }
+    }
+    EIG_TRY(ops.allreduce(bufs([](DistRank &d) { return d.Wpart; }), bufs([](DistRank &d) { return d.Wb; }),
+                          (size_t)s * nb));
+    // a4 (replicated): X = W T - 1/2 V (T^H V^H W T)
+    for (auto &d : R) {
+      const double2 *Tk = d.T + k * nb * nb;
+      Zgemm g;
+      g.M = s; g.N = nb; g.K = nb; g.A = d.Wb; g.lda = s; g.B = Tk; g.ldb = nb; g.C = d.Xb; g.ldc = s;
+      EIG_TRY(zgemm(c, g));   // X = W T
+      g = Zgemm();
+      g.opa = OP_C; g.M = nb; g.N = nb; g.K = s; g.A = d.Vb; g.lda = s; g.B = d.Xb; g.ldb = s; g.C = d.Sm; g.ldc = nb;
+      EIG_TRY(zgemm(c, g));   // V^H (W T)
+      g = Zgemm();
+      g.opa = OP_C; g.M = nb; g.N = nb; g.K = nb; g.A = Tk; g.lda = nb; g.B = d.Sm; g.ldb = nb; g.C = d.Sm + nb * nb;
+      g.ldc = nb;
+      EIG_TRY(zgemm(c, g));   // M = T^H V^H W T
+      g = Zgemm();
+      g.M = s; g.N = nb; g.K = nb; g.A = d.Vb; g.lda = s; g.B = d.Sm + nb * nb; g.ldb = nb; g.C = d.Xb; g.ldc = s;
+      g.alpha = -0.5; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));   // X = W T - 1/2 V M
+    }
+    // a5: owned full columns  A[r0:, J_r] -= [V X] [X_g V_g]^H
+    for (int q = 0; q < nv; q++) {
+      DistRank &d = R[q];
+      if (nl[q] <= 0) continue;
+      double2 *XV = d.Gb;   // [X_g | V_g]  (nl x 2nb)
+      gather_rows_kernel<<<grid_for(c, nl[q] * nb), 256, 0, c.stream>>>(nl[q], lc0[q], d.r, P, nb, r0, nb, d.Xb, s,
+                                                                         XV, nl[q]);
+      EIG_TRY(c.launched("gather_rows_kernel"));
+      gather_rows_kernel<<<grid_for(c, nl[q] * nb), 256, 0, c.stream>>>(nl[q], lc0[q], d.r, P, nb, r0, nb, d.Vb, s,
+                                                                         XV + nl[q] * nb, nl[q]);
+      EIG_TRY(c.launched("gather_rows_kernel"));
+      // [V | X] side by side: V in Vb, X in Xb (both ld s) -> two K = nb products
+      Zgemm g;
+      g.opb = OP_C; g.M = s; g.N = nl[q]; g.K = nb; g.A = d.Vb; g.lda = s; g.B = XV; g.ldb = nl[q];
+      g.C = d.Aloc + r0 + lc0[q] * n; g.ldc = n; g.alpha = -1.0; g.beta = 1.0;
+      EIG_TRY(zgemm(c, g));   // -= V X_g^H
+      g.A = d.Xb; g.B = XV + nl[q] * nb;
+      EIG_TRY(zgemm(c, g));   // -= X V_g^H
+    }
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ virtual ranks (one GPU)
+// he2hb of the Hermitian A (n x n, lda, lower read) computed by the
+// distributed algorithm with P virtual ranks on this GPU; the result is
+// assembled into A in the single-GPU he2hb layout (band + V1), plus tau, T.
+int he2hb_sim(Ctx &c, int64_t n, int P, double2 *A, int64_t lda, double2 *tau, double2 *T) {
+  const int nb = c.nb;
+  const int64_t K = num_panels(n, nb);
+  EIG_TRY(real_diag(c, n, A, lda));
+  if (K == 0) return 0;
+  EIG_TRY(herm_full(c, n, A, lda));
+  std::vector<double2 *> allocs;
+  auto dalloc = [&](size_t elems) -> double2 * {
+    double2 *p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(elems, 1) * sizeof(double2)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    allocs.push_back(p);
+    return p;
+  };
+  std::vector<DistRank> R(P);
+  double2 **d_ptrs = nullptr;
+  int rc = c.check(cudaMalloc(&d_ptrs, P * sizeof(double2 *)), "ptrs");
+  const int64_t s0 = n - nb;
+  for (int q = 0; q < P && !rc; q++) {
+    DistRank &d = R[q];
+    d.r = q;
+    d.nloc = ncols_of(n, q, P, nb);
+    d.Aloc = dalloc((size_t)n * d.nloc);
+    d.V1 = (q == 0) ? A : nullptr;   // rank 0 writes V1 straight into A; the others into scratch
+    if (q != 0) d.V1 = dalloc((size_t)n * n);
+    d.tau = (q == 0) ? tau : dalloc((size_t)K * nb);
+    d.T = (q == 0) ? T : dalloc((size_t)K * nb * nb);
+    d.Vb = dalloc((size_t)s0 * nb);
+    d.Wb = dalloc((size_t)s0 * nb);
+    d.Xb = dalloc((size_t)s0 * nb);
+    d.Wpart = dalloc((size_t)s0 * nb);
+    d.Gb = dalloc((size_t)n * 2 * nb);
+    d.Sm = dalloc((size_t)2 * nb * nb);
+    if (!d.Aloc || !d.V1 || !d.tau || !d.T || !d.Vb || !d.Wb || !d.Xb || !d.Wpart || !d.Gb || !d.Sm) rc = EIG_ERR_NOMEM;
+    if (!rc && d.nloc > 0) {
+      cyclic_copy_kernel<<<grid_for(c, n * d.nloc), 256, 0, c.stream>>>(n, q, P, nb, d.nloc, A, lda, d.Aloc, true);
+      rc = c.launched("cyclic_copy_kernel");
+    }
+  }
+  if (!rc) {
+    DistOps ops{&c, true, P, &R, d_ptrs};
+    rc = he2hb_dist_run(c, n, ops);
+  }
+  // assemble: band (rows c..c+nb of column c) from the owners' columns; V1 already in A
+  for (int q = 0; q < P && !rc; q++) {
+    DistRank &d = R[q];
+    if (d.nloc <= 0) continue;
+    // copy whole owned columns into a scratch n x n, then take the band rows into A
+    double2 *full = dalloc((size_t)n * n);
+    if (!full) { rc = EIG_ERR_NOMEM; break; }
+    cyclic_copy_kernel<<<grid_for(c, n * d.nloc), 256, 0, c.stream>>>(n, q, P, nb, d.nloc, full, n, d.Aloc, false);
+    rc = c.launched("cyclic_copy_kernel");
+    if (rc) break;
+    for (int64_t lc = 0; lc < d.nloc && !rc; lc += nb) {
+      const int64_t g0 = gcol_of(lc, q, P, nb);
+      const int64_t w = std::min<int64_t>(nb, n - g0);
+      // rows g0 .. min(n, g0 + w + nb) of the block's columns (covers the band 0 <= r - c <= nb)
+      const int64_t rows = std::min<int64_t>(n, g0 + w + nb) - g0;
+      rc = c.check(cudaMemcpy2DAsync(A + g0 + g0 * lda, lda * sizeof(double2), full + g0 + g0 * n, n * sizeof(double2),
+                                     rows * sizeof(double2), w, cudaMemcpyDeviceToDevice, c.stream), "band");
+    }
+  }
+  // the band rows below the diagonal block of each column hold R (in the
+  // panel columns) and nothing else; rows beyond c + nb are V1 (placed above)
+  if (!rc) rc = c.check(cudaStreamSynchronize(c.stream), "sync");
+  for (double2 *p : allocs) cudaFree(p);
+  if (d_ptrs) cudaFree(d_ptrs);
+  if (!rc) rc = real_diag(c, n, A, lda);
+  return rc;
+}
+
+}  // namespace eig

@@ -337,7 +337,7 @@ __device__ __forceinline__ void pmark(unsigned long long *pp, long long &tl, int
 // WAVE: the window's three 32-row chunks arrive as three cp.async groups
 // followed by one more (the next item's chunk 0); phase A waits for each chunk
 // just before its first k-step, and nothing is refilled here.
-template <bool WAVE = false>
+template <bool WAVE = false, int WPEND = 3>
 __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const double *vc, const double *tt,
                                            unsigned long long *pp, long long &tl) {
   // ---------------- phase A: Y = V^H E   (M-fragment mf nonzero on k-steps 2mf .. 2mf+33)
@@ -350,16 +350,18 @@ __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const d
       cp_async_wait<0>();
       __syncwarp();
     }
+    // WAVE: groups pending at entry = [chunk 0, chunk 1, chunk 2] plus WPEND - 2
+    // younger ones (the next item's chunk 0 with a spare slot)
     if (WAVE && ks == 0) {
-      cp_async_wait<3>();
+      cp_async_wait<WPEND>();
       __syncwarp();
     }
     if (WAVE && ks == 16) {
-      cp_async_wait<2>();
+      cp_async_wait<WPEND - 1>();
       __syncwarp();
     }
     if (WAVE && ks == 32) {
-      cp_async_wait<1>();
+      cp_async_wait<WPEND - 2>();
       __syncwarp();
     }
     const int ch = ks < 16 ? F.ch0 : (ks < 32 ? F.ch1 : F.ch2);
@@ -853,8 +855,14 @@ __device__ __forceinline__ int64_t wave_J(const Q2wArgs &a, int64_t g) { return 
 // item being computed uses three, and the fourth receives the next item's
 // first chunk as soon as the item starts; the next item's other two chunks go
 // into the slots of the finished item, so the window loads overlap compute.
-constexpr int LDWV = 129;   // 4 chunks of 32 rows + 1 (odd: conflict-free)
-constexpr int WAVE_WARPS = 10;                       // 2-3 per SM sub-partition; items are claimed dynamically
+#ifndef Q2_WAVE_SLOTS
+#define Q2_WAVE_SLOTS 4
+#endif
+// 4 slots: 10 warps, the next item's first chunk prefetched into the spare slot;
+// 3 slots: 12 warps (3 per SM sub-partition), no spare (more warps hide the loads)
+constexpr int WSLOTS = Q2_WAVE_SLOTS;
+constexpr int LDWV = 32 * WSLOTS + 1;   // chunks of 32 rows + 1 (odd: conflict-free)
+constexpr int WAVE_WARPS = WSLOTS == 4 ? 10 : 12;   // items are claimed dynamically
 constexpr int OFF_WAVE_T = VC_STAGE;                 // layout: V | T | windows
 constexpr int OFF_WAVE_WIN = OFF_WAVE_T + T_STAGE;
 static_assert(OFF_WAVE_WIN + WAVE_WARPS * 8 * LDWV <= OFF_BAR, "wave windows must fit the q2w shared-memory size");
@@ -966,20 +974,30 @@ __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArg
             nrs = item_rs(nxt);
             nc0 = nf * 8;
             nnc = (int)imin64(8, a.m - nc0);
-            load_chunk(nrs, nc0, nnc, 0, sd);
+            if (WSLOTS == 4) load_chunk(nrs, nc0, nnc, 0, sd);
           }
-          cp_async_commit();   // (possibly empty) keeps the group count uniform
           long long tl = 0;
-          full_block<true>(Fr, L, vcd, ttd, nullptr, tl);
+          if (WSLOTS == 4) {
+            cp_async_commit();   // (possibly empty) keeps the group count uniform
+            full_block<true, 3>(Fr, L, vcd, ttd, nullptr, tl);
+          } else {
+            full_block<true, 2>(Fr, L, vcd, ttd, nullptr, tl);
+          }
           __syncwarp();        // every lane is done reading this item's chunks
           if (nxt >= 0) {
+            if (WSLOTS != 4) {
+              load_chunk(nrs, nc0, nnc, 0, sa);
+              cp_async_commit();
+            }
             load_chunk(nrs, nc0, nnc, 1, sb);
             cp_async_commit();
             load_chunk(nrs, nc0, nnc, 2, sc);
             cp_async_commit();
-            const int s_old = sa;
-            sa = sd;
-            sd = s_old;
+            if (WSLOTS == 4) {
+              const int s_old = sa;
+              sa = sd;
+              sd = s_old;
+            }
           }
           cur = nxt;
         }

@@ -36,6 +36,10 @@ int bt_run(Ctx &c, int64_t n, const double *Zr, int64_t ldzr, const double2 *V2,
            const double2 *A, int64_t lda, const double2 *T1, const double2 *L, int64_t ldl, double2 *E, int64_t lde,
            int64_t m, double2 *hostE = nullptr, int64_t ldh = 0);
 
+// NEXT-4 (he2hb_dist.cu): the 1D block-cyclic distributed reduction computed by
+// P virtual ranks on this GPU (arithmetic check), result in the he2hb layout
+int he2hb_sim(Ctx &c, int64_t n, int P, double2 *A, int64_t lda, double2 *tau, double2 *T);
+
 // ------------------------------------------------------------- collective (comm.cu)
 int comm_unique_id(void *id128);
 int comm_init(Ctx &c, const void *id128);   // ncclCommInitRank (collective over the ranks)
