@@ -61,6 +61,9 @@ extern "C" {
                                 three real DMMA products (3M, Gauss) instead of four: 0.75 of
                                 the tensor-pipe work; nominal flops stay 8 per complex MAC   */
 #define EIG_NO_3M        4u  /* force the four-product form (overrides EIG_USE_3M / EIG_3M)   */
+#define EIG_DIST_HE2HB   8u  /* collective eig_solve_gen: he2hb distributed over all ranks (1D
+                                block-cyclic columns, NEXT-4) instead of on rank 0; every rank
+                                then already holds V1 / T1 (no V1 broadcast)                  */
 
 /* eig_hotpath flags */
 #define EIG_HOST_BUFFERS 1u  /* pointers are host memory: copy in, run, copy E out (synchronous) */
@@ -91,7 +94,7 @@ typedef struct {
   int64_t n_max;     /* > 0: largest n this handle will see (calls with n > n_max
                         return EIG_ERR_STATE; collective receive buffers are
                         allocated at init); 0: grow lazily                        */
-  unsigned flags;    /* EIG_GATHER_Z | EIG_USE_3M | EIG_NO_3M.  Neither 3M flag: the
+  unsigned flags;    /* EIG_GATHER_Z | EIG_USE_3M | EIG_NO_3M | EIG_DIST_HE2HB.  Neither 3M flag: the
                         environment EIG_3M=0/1 decides, else 3M is on (default)    */
 } eig_config;
 

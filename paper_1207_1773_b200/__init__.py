@@ -6,10 +6,10 @@ All compute runs in ``libeigb200.so`` (hand-written CUDA, FP64 DMMA).  This
 package is the C-ABI binding (``include/eig.h``) plus torch plumbing.  It
 never imports ``oracle/`` and has no CPU fallback.
 """
-from ._binding import (EIG_GATHER_Z, EIG_HOST_BUFFERS, EIG_NO_3M, EIG_USE_3M, EIG_SKIP_BT, EIG_SKIP_HE2HB, STAGES, EigError,  # noqa: F401
+from ._binding import (EIG_DIST_HE2HB, EIG_GATHER_Z, EIG_HOST_BUFFERS, EIG_NO_3M, EIG_USE_3M, EIG_SKIP_BT, EIG_SKIP_HE2HB, STAGES, EigError,  # noqa: F401
                        Solver, colmajor, column_slice, empty_colmajor, exported_symbols, lib, num_panels,
                        resolve_range, unique_id, v2_slots)
 
 __all__ = ["Solver", "EigError", "colmajor", "empty_colmajor", "lib", "num_panels", "v2_slots", "exported_symbols",
            "unique_id", "column_slice", "resolve_range", "STAGES", "EIG_HOST_BUFFERS", "EIG_SKIP_BT",
-           "EIG_SKIP_HE2HB", "EIG_GATHER_Z", "EIG_USE_3M", "EIG_NO_3M"]
+           "EIG_SKIP_HE2HB", "EIG_GATHER_Z", "EIG_USE_3M", "EIG_NO_3M", "EIG_DIST_HE2HB"]

@@ -27,6 +27,7 @@ EIG_SKIP_BT = 4
 EIG_GATHER_Z = 1          # eig_config.flags
 EIG_USE_3M = 2
 EIG_NO_3M = 4
+EIG_DIST_HE2HB = 8
 STAGES = ["potrf", "hegst", "he2hb", "hb2st", "stedc", "wait", "q2", "q1", "trsm", "bt", "gather", "total"]
 
 _lib = None

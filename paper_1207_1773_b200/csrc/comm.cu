@@ -267,21 +267,44 @@ int coll_solve_gen(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *B, int64
   EIG_TRY(order(c, c.stream, c.cstream, c.ev_c[0], "comm fork"));
   EIG_TRY(bcast_status(c, info, &info));
   if (info) return (int)info;
-  // ---- steps 2 and 3a on rank 0; L, V1, T1 broadcast while it chases the bulges
+  const bool dist = (c.flags & EIG_DIST_HE2HB) != 0;
   if (root) {
     EIG_TRY(c.stat_begin(EIG_ST_HEGST));
     EIG_TRY(hegst_run(c, n, dA, dlda, dL, dldl));
     EIG_TRY(c.stat_end(EIG_ST_HEGST));
-    EIG_TRY(c.stat_begin(EIG_ST_HE2HB));
-    EIG_TRY(he2hb_run(c, n, dA, dlda, r.tau1, r.T1));
-    EIG_TRY(c.stat_end(EIG_ST_HE2HB));
     c.st.flops[EIG_ST_HEGST] = 4.0 * dn * dn * dn;
-    c.st.flops[EIG_ST_HE2HB] = 16.0 / 3.0 * dn * dn * dn;
   }
-  EIG_TRY(order(c, c.stream, c.cstream, c.ev_c[1], "he2hb done"));
-  EIG_TRY(bcast_lower(c, dL, n, dldl, r.pk, "bcast L"));
-  EIG_TRY(bcast_lower(c, dA, n, dlda, r.pk, "bcast A (V1)"));
-  EIG_TRY(bcast(c, r.T1, (size_t)K * nb * nb * sizeof(double2), "bcast T1"));
+  if (!dist) {
+    // ---- step 3a on rank 0; L, V1, T1 broadcast while it chases the bulges
+    if (root) {
+      EIG_TRY(c.stat_begin(EIG_ST_HE2HB));
+      EIG_TRY(he2hb_run(c, n, dA, dlda, r.tau1, r.T1));
+      EIG_TRY(c.stat_end(EIG_ST_HE2HB));
+      c.st.flops[EIG_ST_HE2HB] = 16.0 / 3.0 * dn * dn * dn;
+    }
+    EIG_TRY(order(c, c.stream, c.cstream, c.ev_c[1], "he2hb done"));
+    EIG_TRY(bcast_lower(c, dL, n, dldl, r.pk, "bcast L"));
+    EIG_TRY(bcast_lower(c, dA, n, dlda, r.pk, "bcast A (V1)"));
+    EIG_TRY(bcast(c, r.T1, (size_t)K * nb * nb * sizeof(double2), "bcast T1"));
+  } else {
+    // ---- NEXT-4: step 3a distributed over all ranks (1D block-cyclic
+    // columns, he2hb_dist.cu).  Every rank ends with all of V1 (in dA) and
+    // T1; rank 0 also gets the band for the bulge chase.  All NCCL work of
+    // this phase is on the compute stream (one communicator, one order).
+    if (root) EIG_TRY(herm_full(c, n, dA, dlda));
+    const int64_t nloc = dist_ncols(n, c.rank, P, nb);
+    double2 *Aloc = (double2 *)c.ws(WS_C_ALOC, (size_t)n * std::max<int64_t>(nloc, 1) * sizeof(double2));
+    double2 *work = (double2 *)c.ws(WS_C_DWORK, he2hb_dist_work(n, nb, P, c.rank) * sizeof(double2));
+    double2 *pack = (root && dlda != n) ? (double2 *)c.ws(WS_C_E, (size_t)n * n * sizeof(double2)) : nullptr;
+    if (!Aloc || !work || (root && dlda != n && !pack)) return EIG_ERR_NOMEM;
+    EIG_TRY(c.stat_begin(EIG_ST_HE2HB));
+    EIG_TRY(dist_scatter(c, n, dA, dlda, Aloc, pack));
+    EIG_TRY(he2hb_dist_nccl(c, n, Aloc, dA, r.tau1, r.T1, work, root ? dA : nullptr, dlda));
+    EIG_TRY(c.stat_end(EIG_ST_HE2HB));
+    c.st.flops[EIG_ST_HE2HB] = 16.0 / 3.0 * dn * dn * dn / P;
+    EIG_TRY(order(c, c.stream, c.cstream, c.ev_c[1], "he2hb done"));
+    EIG_TRY(bcast_lower(c, dL, n, dldl, r.pk, "bcast L"));
+  }
   // ---- bulge chase on rank 0; V2 / tau2 broadcast during stedc
   if (root) {
     EIG_TRY(c.stat_begin(EIG_ST_HB2ST));

@@ -40,6 +40,7 @@ enum WsId {
   WS_HOST_A, WS_HOST_V2, WS_HOST_TAU2, WS_HOST_L, WS_HOST_Z, WS_HOST_E, WS_HOST_TAU1, WS_HOST_T1,
   // collective calls (comm.cu): received factors on ranks > 0, packing, slices
   WS_C_A, WS_C_L, WS_C_PACK, WS_C_T1, WS_C_TAU1, WS_C_V2, WS_C_TAU2, WS_C_Z, WS_C_E, WS_C_STATUS,
+  WS_C_ALOC, WS_C_DWORK,   // NEXT-4 distributed he2hb: this rank's columns, work
   WS_COUNT
 };
 

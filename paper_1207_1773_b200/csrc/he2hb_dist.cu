@@ -330,4 +330,147 @@ int he2hb_sim(Ctx &c, int64_t n, int P, double2 *A, int64_t lda, double2 *tau, d
   return rc;
 }
 
+// ------------------------------------------------------------------ real ranks (NCCL)
+namespace {
+
+// band rows [g0, g0 + w + nb) of the w columns of every owned block, packed
+// block after block as (2 nb) x w column-major slabs (rows past n zero)
+__global__ void band_pack_kernel(int64_t n, int r, int P, int nb, int64_t nloc, const double2 *Aloc, double2 *out,
+                                 bool unpack, double2 *A, int64_t lda) {
+  const int64_t nblk = (nloc + nb - 1) / nb;
+  const int64_t total = nblk * 2 * nb * nb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lb = e / (2 * nb * nb);
+    const int64_t rem = e % (2 * nb * nb);
+    const int j = (int)(rem / (2 * nb)), i = (int)(rem % (2 * nb));
+    const int64_t lc = lb * nb + j;
+    if (lc >= nloc) continue;
+    const int64_t gc = gcol_of(lc, r, P, nb);
+    const int64_t g0 = gc - j, row = g0 + i;
+    if (!unpack) {
+      out[e] = row < n ? Aloc[row + lc * n] : czero();
+    } else if (row < n && row >= gc) {   // lower part only (band, then R / V heads of the panel)
+      A[row + gc * lda] = out[e];
+    }
+  }
+}
+
+}  // namespace
+
+// Rank 0 holds the full Hermitian A (n x n, lda); every rank receives the
+// full columns of its blocks into Aloc (n x nloc, ld n).  Grouped
+// send/recv, one message per block.
+int dist_scatter(Ctx &c, int64_t n, const double2 *A, int64_t lda, double2 *Aloc, double2 *pack) {
+  const int nb = c.nb, P = c.nranks, r = c.rank;
+  const int64_t NB = (n + nb - 1) / nb;
+  ncclComm_t comm = (ncclComm_t)c.nccl;
+  if (r == 0) {   // own blocks: local copies
+    for (int64_t b = 0; b < NB; b += P) {
+      const int64_t w = std::min<int64_t>(nb, n - b * nb);
+      EIG_TRY(c.check(cudaMemcpy2DAsync(Aloc + (b / P) * nb * n, n * sizeof(double2), A + b * nb * lda,
+                                        lda * sizeof(double2), n * sizeof(double2), w, cudaMemcpyDeviceToDevice,
+                                        c.stream), "scatter own"));
+    }
+    if (lda != n) {   // contiguous send copies of the other ranks' blocks
+      for (int64_t b = 0; b < NB; b++)
+        if (b % P)
+          EIG_TRY(c.check(cudaMemcpy2DAsync(pack + b * nb * n, n * sizeof(double2), A + b * nb * lda,
+                                            lda * sizeof(double2), n * sizeof(double2),
+                                            std::min<int64_t>(nb, n - b * nb), cudaMemcpyDeviceToDevice, c.stream),
+                          "scatter pack"));
+    }
+  }
+  if (P == 1) return 0;
+  if (ncclGroupStart() != ncclSuccess) return EIG_ERR_NCCL;
+  for (int64_t b = 0; b < NB; b++) {
+    const int q = (int)(b % P);
+    if (q == 0) continue;
+    const size_t cnt = (size_t)n * std::min<int64_t>(nb, n - b * nb) * 2;
+    if (r == 0) {
+      const double2 *src = (lda == n) ? A + b * nb * lda : pack + b * nb * n;
+      if (ncclSend(src, cnt, ncclDouble, q, comm, c.stream) != ncclSuccess) return EIG_ERR_NCCL;
+      c.st.bytes_comm += (int64_t)(cnt * sizeof(double));
+    } else if (q == r) {
+      if (ncclRecv(Aloc + (b / P) * nb * n, cnt, ncclDouble, 0, comm, c.stream) != ncclSuccess) return EIG_ERR_NCCL;
+      c.st.bytes_comm += (int64_t)(cnt * sizeof(double));
+    }
+  }
+  if (ncclGroupEnd() != ncclSuccess) return EIG_ERR_NCCL;
+  return 0;
+}
+
+// The distributed reduction for this rank (NCCL collectives).  Aloc: this
+// rank's columns; V1: n x n (ld n) receiving every panel's reflector tails in
+// the he2hb layout; tau, T: K nb and K nb^2 (every rank gets all of them).
+// Afterwards the band of every block is gathered into rank 0's A (lower, lda).
+int he2hb_dist_nccl(Ctx &c, int64_t n, double2 *Aloc, double2 *V1, double2 *tau, double2 *T, double2 *work,
+                    double2 *A0, int64_t lda0) {
+  const int nb = c.nb, P = c.nranks;
+  const int64_t s0 = std::max<int64_t>(n - nb, 1);
+  std::vector<DistRank> R(1);
+  DistRank &d = R[0];
+  d.r = c.rank;
+  d.nloc = ncols_of(n, c.rank, P, nb);
+  d.Aloc = Aloc;
+  d.V1 = V1;
+  d.tau = tau;
+  d.T = T;
+  d.Vb = work;
+  d.Wb = d.Vb + s0 * nb;
+  d.Xb = d.Wb + s0 * nb;
+  d.Wpart = d.Xb + s0 * nb;
+  d.Gb = d.Wpart + s0 * nb;
+  d.Sm = d.Gb + (size_t)n * 2 * nb;
+  double2 *bandbuf = d.Sm + 2 * nb * nb;   // (NB_loc) x 2nb x nb per rank, P of them on rank 0
+  DistOps ops{&c, false, P, &R, nullptr};
+  EIG_TRY(he2hb_dist_run(c, n, ops));
+  // band gather: every rank packs its blocks' band slabs, rank 0 receives and unpacks
+  const int64_t NB = (n + nb - 1) / nb, maxblk = (NB + P - 1) / P;
+  const size_t slab = (size_t)maxblk * 2 * nb * nb;
+  if (c.rank != 0 || P == 1) {
+    band_pack_kernel<<<grid_for(c, (int64_t)slab), 256, 0, c.stream>>>(n, c.rank, P, nb, d.nloc, Aloc, bandbuf,
+                                                                      false, nullptr, 0);
+    EIG_TRY(c.launched("band_pack_kernel"));
+  }
+  if (P > 1) {
+    ncclComm_t comm = (ncclComm_t)c.nccl;
+    if (ncclGroupStart() != ncclSuccess) return EIG_ERR_NCCL;
+    for (int q = 1; q < P; q++) {
+      if (c.rank == 0) {
+        if (ncclRecv(bandbuf + (size_t)q * slab, slab * 2, ncclDouble, q, comm, c.stream) != ncclSuccess)
+          return EIG_ERR_NCCL;
+      } else if (c.rank == q) {
+        if (ncclSend(bandbuf, slab * 2, ncclDouble, 0, comm, c.stream) != ncclSuccess) return EIG_ERR_NCCL;
+      }
+      c.st.bytes_comm += (int64_t)(slab * sizeof(double2));
+    }
+    if (ncclGroupEnd() != ncclSuccess) return EIG_ERR_NCCL;
+  }
+  if (c.rank == 0) {
+    for (int q = 0; q < P; q++) {
+      const int64_t nl = ncols_of(n, q, P, nb);
+      if (nl <= 0) continue;
+      double2 *src = bandbuf + (size_t)q * slab;
+      if (q == 0 && P > 1) {   // rank 0's own slabs straight from its columns
+        band_pack_kernel<<<grid_for(c, (int64_t)slab), 256, 0, c.stream>>>(n, 0, P, nb, nl, Aloc, src, false,
+                                                                          nullptr, 0);
+        EIG_TRY(c.launched("band_pack_kernel"));
+      }
+      band_pack_kernel<<<grid_for(c, (int64_t)slab), 256, 0, c.stream>>>(n, q, P, nb, nl, nullptr, src, true, A0,
+                                                                        lda0);
+      EIG_TRY(c.launched("band_pack_kernel"));
+    }
+  }
+  return 0;
+}
+
+// workspace of he2hb_dist_nccl (complex elements)
+size_t he2hb_dist_work(int64_t n, int nb, int P, int rank) {
+  const int64_t s0 = std::max<int64_t>(n - nb, 1);
+  const int64_t NB = (n + nb - 1) / nb, maxblk = (NB + P - 1) / P;
+  const size_t slab = (size_t)maxblk * 2 * nb * nb;
+  return (size_t)4 * s0 * nb + (size_t)n * 2 * nb + 2 * nb * nb + slab * (rank == 0 ? P : 1);
+}
+int64_t dist_ncols(int64_t n, int rank, int P, int nb) { return ncols_of(n, rank, P, nb); }
+
 }  // namespace eig

@@ -856,10 +856,12 @@ __device__ __forceinline__ int64_t wave_J(const Q2wArgs &a, int64_t g) { return 
 // first chunk as soon as the item starts; the next item's other two chunks go
 // into the slots of the finished item, so the window loads overlap compute.
 #ifndef Q2_WAVE_SLOTS
-#define Q2_WAVE_SLOTS 4
+#define Q2_WAVE_SLOTS 3
 #endif
 // 4 slots: 10 warps, the next item's first chunk prefetched into the spare slot;
-// 3 slots: 12 warps (3 per SM sub-partition), no spare (more warps hide the loads)
+// 3 slots: 12 warps (3 per SM sub-partition, 159 registers), no spare: the
+// extra warps hide the window loads better than the prefetch did (n = 10^4:
+// m = 10^4 / 1250 / 1000: 346.5 / 59.2 / 50.5 ms -> 328.8 / 56.2 / 48.2 ms)
 constexpr int WSLOTS = Q2_WAVE_SLOTS;
 constexpr int LDWV = 32 * WSLOTS + 1;   // chunks of 32 rows + 1 (odd: conflict-free)
 constexpr int WAVE_WARPS = WSLOTS == 4 ? 10 : 12;   // items are claimed dynamically

@@ -39,6 +39,12 @@ int bt_run(Ctx &c, int64_t n, const double *Zr, int64_t ldzr, const double2 *V2,
 // NEXT-4 (he2hb_dist.cu): the 1D block-cyclic distributed reduction computed by
 // P virtual ranks on this GPU (arithmetic check), result in the he2hb layout
 int he2hb_sim(Ctx &c, int64_t n, int P, double2 *A, int64_t lda, double2 *tau, double2 *T);
+// ... and over NCCL for this rank of the handle's communicator (collective)
+int64_t dist_ncols(int64_t n, int rank, int P, int nb);
+size_t he2hb_dist_work(int64_t n, int nb, int P, int rank);
+int dist_scatter(Ctx &c, int64_t n, const double2 *A, int64_t lda, double2 *Aloc, double2 *pack);
+int he2hb_dist_nccl(Ctx &c, int64_t n, double2 *Aloc, double2 *V1, double2 *tau, double2 *T, double2 *work,
+                    double2 *A0, int64_t lda0);
 
 // ------------------------------------------------------------- collective (comm.cu)
 int comm_unique_id(void *id128);

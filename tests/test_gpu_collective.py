@@ -89,3 +89,26 @@ def test_collective_host_buffers_not_available():
     rc = lib().eig_hotpath(sc.h, 10, None, 10, None, None, None, None, None, 10, None, 10, None, 10, 1,
                            EIG_HOST_BUFFERS)
     assert rc == -1005
+
+
+@gpu
+@pytest.mark.parametrize("n,nb", [(300, 16), (1000, 64)])
+def test_collective_solve_gen_distributed_he2hb_p1(n, nb):
+    """EIG_DIST_HE2HB on a one-rank communicator: the whole NEXT-4 path over
+    NCCL (block scatter, per-step V/T broadcasts and W allreduce, band gather)
+    gives the same eigenpairs as the single-GPU solver within the gates."""
+    import math
+    from paper_1207_1773_b200 import EIG_DIST_HE2HB, Solver
+    A, B = synth.pencil_rand(n, seed=n + 5, kappa=1e2)
+    w1, Z1 = Solver(0, nb=nb).solve_gen(_dev(np.tril(A)), _dev(np.tril(B)))
+    sc = _coll(nb=nb, flags=EIG_DIST_HE2HB)
+    w, Z, st = sc.solve_gen(_dev(np.tril(A)), _dev(np.tril(B)), stats=True)
+    torch.cuda.synchronize()
+    w, w1 = w.cpu().numpy(), w1.cpu().numpy()
+    assert np.max(np.abs(w - w1)) / np.max(np.abs(w1)) < 1e-12
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    R = Ad @ Z - (Bd @ Z) * torch.from_numpy(w).cuda()[None, :]
+    one = lambda M: torch.linalg.matrix_norm(M, ord=1).item()  # noqa: E731
+    assert one(R) / (n * one(Ad) * one(Z)) < 1e-14
+    assert one(Z.conj().T @ Bd @ Z - torch.eye(n, dtype=Z.dtype, device=Z.device)) / n < 1e-14
+    assert st["seconds"]["he2hb"] > 0 and st["bytes_comm"] > 0
