@@ -65,6 +65,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-zhegv", action="store_true", help="skip the end-to-end generalized solve timing")
+    p.add_argument("--no-dist-he2hb", action="store_true", help="N > 1: skip the EIG_DIST_HE2HB zhegv timing")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
     p.add_argument("--gemm", default="3m", choices=["3m", "4m"],
                    help="complex GEMMs (he2hb updates, Q1, L^-H, front end) as 3 real DMMA products (3M) or 4 (4M)")
@@ -159,7 +160,32 @@ def cpu_sample(n, nb, seed, budget, pre=None):
     value = (fl_he + fl_bt) / (t_he + t_bt) / 1e12
     desc = (f"oracle on n={n}: first {r} he2hb reflectors ({t_he:.1f} s) + {c} eigenvector columns through "
             f"Q2,Q1,L^-H ({t_bt:.1f} s); nominal flops of the sample / time")
+    cpu_sample.parts = {"he2hb_tflops": fl_he / t_he / 1e12, "bt_tflops": fl_bt / t_bt / 1e12,
+                        "he2hb_s": t_he, "bt_s": t_bt, "reflectors": r, "columns": c}
     return value, cores, desc, t_he + t_bt
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_sample_threads(n, nb, threads):
+    """The same oracle sample at order n in a child process with OMP_NUM_THREADS = threads."""
+    code = ("import sys, json; sys.path.insert(0, %r); import bench; "
+            "v, c, d, t = bench.cpu_sample(%d, %d, 0, 0.0); "
+            "print(json.dumps({'value': v, 'desc': d, 'parts': bench.cpu_sample.parts}))" % (ROOT, n, nb))
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+    try:
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:   # reported, not fatal
+        return {"error": str(e)[:200]}
 
 
 def run_reference(a, rank, world):
@@ -455,6 +481,26 @@ def run_b200(a, rank, world, local_rank):
                  "note": "collective eig_solve_gen: rank 0 potrf, hegst, he2hb, hb2st, stedc; NCCL broadcast of "
                          "L / V1 / T1 (during hb2st) and V2 (during stedc), scatter of the eigenvector slices; "
                          "back-transform sharded by eigenvector columns; max over ranks"}
+        if not a.no_dist_he2hb:   # NEXT-4: the same solve with he2hb distributed over the ranks (EIG_DIST_HE2HB)
+            from paper_1207_1773_b200 import EIG_DIST_HE2HB
+            sd = collective_solver(local_rank, nb, a.g, flags=gflags | EIG_DIST_HE2HB)
+            if rank == 0:
+                Aw.copy_(A0)
+                Bw.copy_(B0)
+            sd.solve_gen(Aw, Bw, n=n)                   # warm-up
+            if rank == 0:
+                Aw.copy_(A0)
+                Bw.copy_(B0)
+            torch.cuda.synchronize()
+            dist.barrier()
+            w_, Z_, dst = sd.solve_gen(Aw, Bw, n=n, stats=True)
+            torch.cuda.synchronize()
+            dist.barrier()
+            td = torch.tensor([dst["seconds"]["total"], dst["seconds"]["he2hb"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(td, op=dist.ReduceOp.MAX)
+            zhegv["dist_he2hb"] = {"seconds": float(td[0].item()), "he2hb_s_max": float(td[1].item()),
+                                   "note": "EIG_DIST_HE2HB: he2hb 1D block-cyclic over the ranks (NEXT-4)"}
+            sd.close()
         del Aw, Bw, B0, w_, Z_
     if rank == 0 and world == 1 and not a.no_zhegv:
         del E
@@ -469,7 +515,11 @@ def run_b200(a, rank, world, local_rank):
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         v, cores, desc, secs = cpu_sample(n, nb, a.seed, a.cpu_budget, pre=(A_h, V2_h, tau2_h, L_h))
-        cpu = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc}
+        cpu = {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": desc, "cpu": cpu_model(),
+               "parts": cpu_sample.parts,
+               "one_thread_n2000": cpu_sample_threads(2000, nb, 1),
+               "note": "per-part TFLOP/s beside the GPU stage_tflops (he2hb vs q2+q1+trsm); the oracle's "
+                       "reflector updates and column loops are OpenMP-parallel over `cores` threads"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,

@@ -155,7 +155,12 @@ int apply_q1_run(Ctx &c, int64_t n, const double2 *A, int64_t lda, const double2
   const int nb = c.nb;
   const int64_t K = num_panels(n, nb);
   if (K == 0 || m <= 0) return 0;
-  const int ga_max = std::max(1, 256 / nb);
+  // panels aggregated per pass over E (K of the two big GEMMs); EIG_Q1_KW tunes it
+  static const int kw_env = [] {
+    const char *e = getenv("EIG_Q1_KW");
+    return e ? atoi(e) : 256;
+  }();
+  const int ga_max = std::max(1, kw_env / nb);
   const int kw = ga_max * nb;                       // aggregated width
   const int64_t ldv = n - nb;
   double2 *Vb0 = (double2 *)c.ws(WS_V, (size_t)4 * ldv * kw * sizeof(double2));   // V and V T, per parity
