@@ -864,7 +864,10 @@ __device__ __forceinline__ int64_t wave_J(const Q2wArgs &a, int64_t g) { return 
 // m = 10^4 / 1250 / 1000: 346.5 / 59.2 / 50.5 ms -> 328.8 / 56.2 / 48.2 ms)
 constexpr int WSLOTS = Q2_WAVE_SLOTS;
 constexpr int LDWV = 32 * WSLOTS + 1;   // chunks of 32 rows + 1 (odd: conflict-free)
-constexpr int WAVE_WARPS = WSLOTS == 4 ? 10 : 12;   // items are claimed dynamically
+#ifndef Q2_WAVE_WARPS
+#define Q2_WAVE_WARPS (WSLOTS == 4 ? 10 : 12)
+#endif
+constexpr int WAVE_WARPS = Q2_WAVE_WARPS;   // items are claimed dynamically
 constexpr int OFF_WAVE_T = VC_STAGE;                 // layout: V | T | windows
 constexpr int OFF_WAVE_WIN = OFF_WAVE_T + T_STAGE;
 static_assert(OFF_WAVE_WIN + WAVE_WARPS * 8 * LDWV <= OFF_BAR, "wave windows must fit the q2w shared-memory size");
