@@ -148,10 +148,11 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
           scale = czero();
         } else {
           beta = -copysign(sqrt(al.x * al.x + al.y * al.y + nrm), al.x);
-          tau = make_double2((beta - al.x) / beta, -al.y / beta);
+          const double ib = 1.0 / beta;   // two divisions instead of four (critical path)
+          tau = make_double2((beta - al.x) * ib, -al.y * ib);
           const double2 d = make_double2(al.x - beta, al.y);
-          const double dd = d.x * d.x + d.y * d.y;
-          scale = make_double2(d.x / dd, -d.y / dd);
+          const double idd = 1.0 / (d.x * d.x + d.y * d.y);
+          scale = make_double2(d.x * idd, -d.y * idd);
         }
         sv[lane] = (lane == 0) ? make_double2(1.0, 0.0) : (lane < len ? cmul(x0, scale) : czero());
         sv[lane + 32] = (lane + 32 < len) ? cmul(x1, scale) : czero();
@@ -170,10 +171,7 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
         for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta : czero();
       }
       __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        st_release_i32(a.progressA + i, (int)(j + 1));
-      }
+      if (tid == 0) st_release_i32(a.progressA + i, (int)(j + 1));
       // ---- (a) on the previous bulge (shared memory only): f, then store
       if (na > 0) {
         if (upd) {   // one warp per column: lanes over the rows (conflict-free), shuffle reduction
@@ -259,7 +257,9 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
         }
       }
       mark(3);
-      __threadfence();
+      // the barrier orders every thread's D / Ablk stores before thread 0's
+      // gpu-scope release store, which is cumulative over them (PTX memory
+      // model): no separate fence
       __syncthreads();
       if (tid == 0) st_release_i32(a.progress + i, (int)(j + 1));
       mark(5);
