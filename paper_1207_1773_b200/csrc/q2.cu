@@ -410,12 +410,8 @@ __global__ void __launch_bounds__(QT, 1) apply_q2_kernel(Q2Args a, int nslab) {
 
 int q2_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, double2 *E, int64_t lde, int64_t m) {
   if (p.nblocks <= 0 || m <= 0) return 0;
-  // column-owning-warp kernel (q2w.cu) for its shape unless EIG_Q2_KERNEL=row
-  static const int use_w = [] {
-    const char *e = getenv("EIG_Q2_KERNEL");
-    return (e && e[0] == 'r') ? 0 : 1;
-  }();
-  if (use_w) {
+  // the wavefront kernel (q2w.cu) for its shape (nb = 64, g = 32) unless EIG_Q2_WAVE=0
+  {
     const int rc = q2w_apply(ctx, p, V2, T2, E, lde, m);
     if (rc <= 0) return rc;
   }

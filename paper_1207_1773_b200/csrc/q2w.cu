@@ -1,29 +1,26 @@
-// q2w.cu — E <- Q2 E (a6) with column-owning warps, for nb = 64, g = 32.
+// q2w.cu — E <- Q2 E (a6) for nb = 64, g = 32: the wavefront kernel.
 //
-// Same block structure as q2.cu (R7: block (i0, j) of g sweeps is
-// I - V T V^H, V the W x g parallelogram, W = nb + g - 1 = 95; groups applied
-// last to first, steps ascending), different work split:
+// Block structure of DESIGN.md R7 (block (i0, j) of g sweeps is I - V T V^H,
+// V the W x g parallelogram, W = nb + g - 1 = 95), executed in the wavefront
+// order of reading R17: all blocks with equal t = j + (G-1-g) are disjoint,
+// so one cooperative kernel walks the steps t and, within a step, every
+// (block, 8-column fragment) item is an independent task:
 //
-//  * a CTA owns up to 9 eight-column fragments of E per slab; 8 "full" warps
-//    own one fragment each and its 96-row window (a ring of three 32-row
-//    chunks in shared memory) and run all three contractions for it alone —
-//    Y = V^H E (phase A), Y = T Y (phase B), E -= V Y (phase C) — with Y in
-//    registers, moved between the accumulator and operand layouts by warp
-//    shuffles, so they never wait for each other;
-//  * the 9th fragment is shared by a quad of warps (one per SM sub-partition,
-//    each doing a quarter of every phase, Y exchanged through shared memory
-//    under a 128-thread named barrier), so all four DMMA pipes get the same
-//    work (2.25 fragments each instead of 3 on one of them);
-//  * V (compact: Vc[t][4 + s] = v_t[s], zero pads on both sides) and T are
-//    double-buffered and loaded with bulk async copies that complete on an
-//    mbarrier; the last warp to release a buffer issues the copies of the
-//    block two ahead into it (no producer warp, no block-wide barrier);
+//  * a warp runs all three contractions of an item alone — Y = V^H E
+//    (phase A), Y = T Y (phase B), E -= V Y (phase C) — with Y in registers,
+//    moved between the DMMA accumulator and operand layouts by shuffles;
+//  * V (compact: Vc[t][4 + s] = v_t[s], zero pads on both sides,
+//    bank-conflict-free row placement) and T of a block are staged once per
+//    CTA for all its warps;
 //  * every loop over k-steps and row groups is fully unrolled against the
 //    compile-time parallelogram shape: all shared-memory addresses are a lane
 //    base plus an immediate, and only the nonzero DMMA tiles are issued;
-//  * rows that leave the window are stored straight from the accumulators and
-//    their ring slots are refilled with the next block's rows (cp.async)
-//    while the remaining row groups are computed.
+//  * twelve warps per CTA claim items from a shared counter; each keeps its
+//    item's 95-row window in three 32-row chunk slots (cp.async groups waited
+//    for chunk by chunk inside phase A) and stores the rows straight from the
+//    phase-C accumulators.
+// The r01 per-fragment kernels (a warp per fragment walking the block chain)
+// were removed in r02; other (nb, g) shapes use the generic kernel of q2.cu.
 #include <algorithm>
 #include <cstdlib>
 
@@ -52,13 +49,6 @@ __host__ __device__ constexpr int vrow(int t) { return LDVC * t + dv(t & 3); }
 // T columns: cb(k) = 68 (k >> 1) + 36 (k & 1): consecutive columns 4 apart mod 8
 constexpr int T_STAGE = 68 * (G / 2);
 __host__ __device__ constexpr int tcol(int k) { return 68 * (k >> 1) + 36 * (k & 1); }
-constexpr int LDY = 34;                          // quad Y exchange: Y[col][refl]
-constexpr int NFW = 8, NQW = 4, NW = NFW + NQW;  // full warps, quad warps
-constexpr int NFS = NFW + 1;                     // fragments per slab
-constexpr int WT = NW * 32;
-#ifndef Q2W_QUAD
-#define Q2W_QUAD 1   // 0: the 9th fragment goes to warp 8 as a full warp (measured 20% slower)
-#endif
 
 struct Q2wArgs {
   int64_t n, m, lde;
@@ -73,42 +63,11 @@ struct Q2wArgs {
 };
 
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(cnt));
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t *b, unsigned tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra W_%=;\n}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-// L2 policies: the E stream (read and written once per group) is evict-first,
-// the V / T blocks (read by every CTA) evict-last.
+// L2 policy of the E stream (read and written once per item): evict-first.
 __device__ __forceinline__ uint64_t pol_evict_first() {
   uint64_t p;
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
-}
-__device__ __forceinline__ uint64_t pol_evict_last() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          su32(dst)),
-      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol_evict_last())
-      : "memory");
-}
-__device__ __forceinline__ void st_stream(double *p, double v) {
-  asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol_evict_first())
-               : "memory");
 }
 // non-volatile DMMA: lets the scheduler interleave the unrolled tiles freely
 __device__ __forceinline__ void dmma_nv(double (&c)[2], double a, double b) {
@@ -121,7 +80,6 @@ __device__ __forceinline__ void cp_async16m(void *smem, const void *gmem, bool v
                "r"(valid ? 16 : 0), "l"(pol_evict_first())
                : "memory");
 }
-__device__ __forceinline__ void quad_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __host__ __device__ constexpr int imin_c(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int imax_c(int a, int b) { return a > b ? a : b; }
@@ -142,75 +100,13 @@ __device__ __forceinline__ void acc_to_b(const double (&acc)[NM][2], double (&bl
   }
 }
 
-// shared memory: Vc[2] | T[2] | E windows (NFS) | Y, Y2 (quad) | full[2] mbarriers, done[2] counters
+// dynamic shared memory of the wavefront kernel (layout defined there)
 extern __shared__ __align__(128) double2 q2w_sm[];
-constexpr int OFF_T = 2 * VC_STAGE, OFF_E = OFF_T + 2 * T_STAGE, OFF_Y = OFF_E + NFS * 8 * LDE,
-              OFF_Y2 = OFF_Y + 8 * LDY, OFF_BAR = OFF_Y2 + 8 * LDY;
-__device__ __forceinline__ double2 *vc_buf(int bi) { return q2w_sm + bi * VC_STAGE; }
-__device__ __forceinline__ double2 *t_buf(int bi) { return q2w_sm + OFF_T + bi * T_STAGE; }
-__device__ __forceinline__ uint64_t *full_bar(int bi) { return reinterpret_cast<uint64_t *>(q2w_sm + OFF_BAR) + bi; }
-__device__ __forceinline__ int *done_cnt(int bi) { return reinterpret_cast<int *>(q2w_sm + OFF_BAR + 1) + bi; }
 
 // ---------------------------------------------------------------- block sequence
-// (slab, group gi from last to first, step j ascending), identical in every warp.
-struct BlkIt {
-  int sl;
-  int64_t gi, j, J;
-  bool valid;
-};
 __device__ __forceinline__ int64_t steps_of(const Q2wArgs &a, int64_t gi) {
   const int64_t i0 = gi * G;
   return (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
-}
-__device__ __forceinline__ void it_settle(const Q2wArgs &a, BlkIt &it) {
-  while (it.valid && it.j >= it.J) {
-    if (--it.gi < 0) {
-      if (++it.sl >= a.nslab) {
-        it.valid = false;
-        return;
-      }
-      it.gi = a.ngroups - 1;
-    }
-    it.J = steps_of(a, it.gi);
-    it.j = 0;
-  }
-}
-__device__ __forceinline__ void it_begin(const Q2wArgs &a, BlkIt &it) {
-  it.sl = 0;
-  it.gi = a.ngroups - 1;
-  it.j = 0;
-  it.valid = a.ngroups > 0 && a.nslab > 0;
-  it.J = it.valid ? steps_of(a, it.gi) : 0;
-  it_settle(a, it);
-}
-__device__ __forceinline__ void it_next(const Q2wArgs &a, BlkIt &it) {
-  if (!it.valid) return;
-  it.j++;
-  it_settle(a, it);
-}
-
-// Warp-wide: bulk copies of block `it`'s V (live slots) and T into buffer bi.
-// The global offsets of a block (off[j], first[gi]) are read when the
-// iterator reaches it, two blocks before its copies are issued.
-struct BlkSrc {
-  int64_t offj, firstg;   // raw off[j], first[gi] (used only when the copies are issued)
-  int64_t gi, j;
-};
-__device__ __forceinline__ BlkSrc blk_src(const Q2wArgs &a, const BlkIt &it) {
-  BlkSrc b;
-  b.gi = it.gi;
-  b.j = it.j;
-  b.offj = it.valid ? a.off[it.j] : 0;
-  b.firstg = it.valid ? a.first[it.gi] : 0;
-  return b;
-}
-__device__ __forceinline__ void issue_block(const Q2wArgs &a, const BlkSrc &b, int bi, int lane) {
-  const int64_t i0 = b.gi * G;
-  const int nvalid = (int)imax64(0, imin64(G, a.n - 2 - b.j * NB - i0 + 1));
-  if (lane == 0) mbar_arrive_tx(full_bar(bi), (unsigned)(nvalid * NB * 16 + G * G * 16));
-  __syncwarp();
-  if (lane < nvalid) bulk_g2s(vc_buf(bi) + vrow(lane) + PADL, a.V2 + (b.offj + i0 + lane) * NB, NB * 16, full_bar(bi));
-  bulk_g2s(t_buf(bi) + tcol(lane), a.T2 + (b.firstg + b.j) * G * G + lane * G, G * 16, full_bar(bi));
 }
 
 // ---------------------------------------------------------------- per-lane constants
@@ -425,419 +321,6 @@ __device__ __forceinline__ void full_block(const Frag &F, const Lane &L, const d
   pmark(pp, tl, 3);
 }
 
-// Quad warp I: a quarter of every phase of the shared fragment.
-template <int I>
-__device__ __forceinline__ void quad_block(const Frag &F, const Lane &L, const double *vc, const double *tt) {
-  double *yq = reinterpret_cast<double *>(q2w_sm + OFF_Y);
-  double *y2q = reinterpret_cast<double *>(q2w_sm + OFF_Y2);
-  const int lane = L.lane;
-  // ---------------- phase A: M-fragments 2I, 2I+1
-  double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-  for (int ks = 4 * I; ks < imin_c(48, 4 * I + 36); ks++) {
-    const int ch = ks < 16 ? F.ch0 : (ks < 32 ? F.ch1 : F.ch2);
-    const double e = F.ew[ch + L.offEB + 4 * (ks & 15)];
-#pragma unroll
-    for (int u = 0; u < 2; u++) {
-      const int mf = 2 * I + u;
-      if (ks >= 2 * mf && ks <= 2 * mf + 33) dmma_nv(y[u], xsign(vc[L.offA + 568 * mf + 4 * ks], L.negConj), e);
-    }
-  }
-  // Y[col][refl] (accumulator layout: refl 4mf + rr>>1, comp rr&1, cols 2(lane&3), +1)
-#pragma unroll
-  for (int u = 0; u < 2; u++) {
-    const int refl = 4 * (2 * I + u) + (L.rr >> 1);
-#pragma unroll
-    for (int c = 0; c < 2; c++) yq[2 * ((2 * (lane & 3) + c) * LDY + refl) + (L.rr & 1)] = y[u][c];
-  }
-  quad_sync();
-  // ---------------- phase B: M-fragments I, 7-I (k-steps 2mf .. 15)
-  const int offYB = 2 * ((lane >> 2) * LDY + L.kq) + (lane & 1);
-#pragma unroll
-  for (int u = 0; u < 2; u++) {
-    const int mf = u == 0 ? I : 7 - I;
-    y[u][0] = y[u][1] = 0.0;
-#pragma unroll
-    for (int ks = 2 * mf; ks < 16; ks++) dmma_nv(y[u], xsign(tt[L.offT + 136 * ks + 8 * mf], L.negT), yq[offYB + 4 * ks]);
-  }
-#pragma unroll
-  for (int u = 0; u < 2; u++) {
-    const int refl = 4 * (u == 0 ? I : 7 - I) + (L.rr >> 1);
-#pragma unroll
-    for (int c = 0; c < 2; c++) y2q[2 * ((2 * (lane & 3) + c) * LDY + refl) + (L.rr & 1)] = y[u][c];
-  }
-  quad_sync();
-  // ---------------- phase C: row groups {I, 7-I, 8+I, 15-I} then {16+I, 23-I}
-  double yb[16];
-#pragma unroll
-  for (int ks = 0; ks < 16; ks++) yb[ks] = y2q[offYB + 4 * ks];
-  if (I == 0 && F.more) {
-    // the padding slot (current row 95) receives the next block's row 31
-    const int c = lane >> 2;
-    const int64_t row = F.rs + W;
-    const bool ok = (lane & 3) == 0 && row < F.n && c < F.ncols;
-    if ((lane & 3) == 0) cp_async16m(&F.Ew[c * LDE + ring_slot(F.base - 1)], ok ? F.E + row + (F.c0 + c) * F.lde : F.E, ok);
-  }
-  phase_c_rows<4, QuadLow<I>, true>(F, L, vc, yb);
-  cp_async_commit();
-  phase_c_rows<2, QuadHigh<I>, false>(F, L, vc, yb);
-}
-
-// ---------------------------------------------------------------- kernel
-__global__ void __launch_bounds__(WT, 1) apply_q2w_kernel(Q2wArgs a) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // zero the compact V buffers once (their pads are never written again) and the E windows
-  for (int e = threadIdx.x; e < OFF_T; e += WT) q2w_sm[e] = czero();
-  for (int e = threadIdx.x; e < NFS * 8 * LDE; e += WT) q2w_sm[OFF_E + e] = czero();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; i++) {
-      mbar_init(full_bar(i), 1);
-      *done_cnt(i) = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  BlkIt cur, ahead;
-  it_begin(a, cur);
-  ahead = cur;
-  if (w == 0) {   // prologue: blocks 0 and 1
-    if (ahead.valid) issue_block(a, blk_src(a, ahead), 0, lane);
-    it_next(a, ahead);
-    if (ahead.valid) issue_block(a, blk_src(a, ahead), 1, lane);
-    it_next(a, ahead);
-  } else {
-    it_next(a, ahead);
-    it_next(a, ahead);
-  }
-  const int F = a.nfr_total, Gd = gridDim.x;
-  const int f0 = (int)((int64_t)F * blockIdx.x / Gd), f1 = (int)((int64_t)F * (blockIdx.x + 1) / Gd);
-  const bool quad = Q2W_QUAD && w >= NFW;
-  const int qi = w - NFW;
-  const Lane L(lane);
-  Frag Fr;
-  Fr.Ew = q2w_sm + OFF_E + (quad ? NFW : imin_c(w, NFW)) * 8 * LDE;
-  Fr.ew = reinterpret_cast<double *>(Fr.Ew);
-  Fr.E = a.E;
-  Fr.lde = a.lde;
-  Fr.lde2 = 2 * a.lde;
-  Fr.n = a.n;
-  // fragments of slab sl in this CTA, and how many warps work on them
-  auto slab_k = [&](int sl) { return imax_c(0, imin_c(NFS, f1 - (f0 + sl * NFS))); };
-  auto n_active = [](int k) { return (Q2W_QUAD && (k & 3) == 1) ? k - 1 + NQW : k; };
-  BlkSrc asrc;
-  bool active = false;
-  int cur_sl = -1, nact = 0;
-  int64_t cnt = 0;
-  while (cur.valid) {
-    if (cur.sl != cur_sl) {
-      cur_sl = cur.sl;
-      const int s0 = f0 + cur_sl * NFS;
-      const int k = slab_k(cur_sl);
-      const bool quad_on = Q2W_QUAD && (k & 3) == 1;
-      const int nfull = quad_on ? k - 1 : k;
-      nact = n_active(k);
-      active = quad ? quad_on : (w < nfull);
-      if (active) asrc = blk_src(a, ahead);
-      const int fr = quad ? s0 + nfull : s0 + w;
-      Fr.c0 = (int64_t)fr * 8;
-      Fr.ncols = active ? (int)imin64(8, a.m - Fr.c0) : 0;
-      const int cA = 2 * (lane & 3);
-      Fr.ok0 = cA < Fr.ncols;
-      Fr.ok1 = cA + 1 < Fr.ncols;
-    }
-    const int64_t i0 = cur.gi * G;
-    if (cur.j == 0) {
-      Fr.base = 0;
-      if (active) {
-        // group start: the whole window, rows rs .. rs + 95 (row 95 is padding)
-        const int64_t rs = i0 + 1;
-        const int e0 = quad ? lane + 32 * qi : lane, es = quad ? 32 * NQW : 32;
-        for (int e = e0; e < RING * 8; e += es) {
-          const int q = e % RING, c = e / RING;
-          const int64_t row = rs + q;
-          const bool ok = q < W && row < a.n && c < Fr.ncols;
-          cp_async16m(&Fr.Ew[c * LDE + q], ok ? a.E + row + (Fr.c0 + c) * a.lde : a.E, ok);
-        }
-        cp_async_commit();
-        cp_async_commit();   // empty group: the full warps' wait<1> then covers the window
-      }
-    }
-    const int bi = (int)(cnt & 1);
-    if (!active) {   // idle in this slab: keep the block count, touch nothing
-      it_next(a, cur);
-      it_next(a, ahead);
-      cnt++;
-      continue;
-    }
-    Fr.rs = i0 + 1 + cur.j * NB;
-    Fr.more = cur.j + 1 < cur.J;
-    const bool prof = a.prof != nullptr && blockIdx.x == 0 && lane == 0 && w == 0;
-    unsigned long long *pp = prof ? a.prof + 24 : nullptr;
-    long long tl = prof ? clock64() : 0;
-    mbar_wait(full_bar(bi), (unsigned)((cnt >> 1) & 1));
-    pmark(pp, tl, 0);
-    {
-      if (quad) {
-        cp_async_wait<0>();
-        __syncwarp();
-        quad_sync();   // the quad's refills and row-group stores of the previous block
-      } else {
-        cp_async_wait<1>();   // group X (rows 64..94 of this block's window); Y is awaited in phase A
-        __syncwarp();
-      }   // the quad's refills and row-group stores of the previous block
-      Fr.ch0 = 2 * 32 * ((0 + Fr.base / 32) % 3);
-      Fr.ch1 = 2 * 32 * ((1 + Fr.base / 32) % 3);
-      Fr.ch2 = 2 * 32 * ((2 + Fr.base / 32) % 3);
-      Fr.gE = reinterpret_cast<double *>(a.E + Fr.rs + (L.rr >> 1) + (Fr.c0 + 2 * (lane & 3)) * a.lde) + (L.rr & 1);
-      const double *vc = reinterpret_cast<const double *>(vc_buf(bi));
-      const double *tt = reinterpret_cast<const double *>(t_buf(bi));
-      if (!quad) full_block(Fr, L, vc, tt, pp, tl);
-      else if (qi == 0) quad_block<0>(Fr, L, vc, tt);
-      else if (qi == 1) quad_block<1>(Fr, L, vc, tt);
-      else if (qi == 2) quad_block<2>(Fr, L, vc, tt);
-      else quad_block<3>(Fr, L, vc, tt);
-      if (!Fr.more) __threadfence_block();   // the next group re-reads these rows
-      Fr.base = Fr.base + NB >= RING ? Fr.base + NB - RING : Fr.base + NB;
-    }
-    // release buffer bi; the last warp refills it with the block two ahead
-    // (every value this warp loaded from it has been consumed by now)
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      last = atomicAdd(done_cnt(bi), 1) == nact - 1;
-      if (last) *done_cnt(bi) = 0;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && ahead.valid && slab_k(ahead.sl) > 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_block(a, asrc, bi, lane);
-    }
-    pmark(pp, tl, 4);
-    it_next(a, cur);
-    it_next(a, ahead);
-    asrc = blk_src(a, ahead);
-    cnt++;
-  }
-}
-
-// ---------------------------------------------------------------- split kernel (small m)
-// One fragment shared by NQ warps (NQ = 4: like the quad above; NQ = 8: one
-// M-fragment / three row groups per warp), NG fragments per CTA.  For small m
-// (few fragments per SM) this keeps 8-16 warps per SM busy on the sequential
-// block chain instead of one or two.
-template <int NQ, int I>
-struct SplitSets {
-  static constexpr int NMA = 8 / NQ;   // phase A / B M-fragments per warp
-  __device__ static constexpr int ma(int u) { return NQ == 4 ? 2 * I + u : I; }
-  __device__ static constexpr int mb(int u) { return NQ == 4 ? (u == 0 ? I : 7 - I) : I; }
-  static constexpr int NLO = NQ == 4 ? 4 : 2, NHI = NQ == 4 ? 2 : 1;
-};
-template <int NQ, int I>
-struct SplitLow {
-  __device__ static constexpr int f(int u) {
-    return NQ == 4 ? (u == 0 ? I : u == 1 ? 7 - I : u == 2 ? 8 + I : 15 - I) : (u == 0 ? I : 15 - I);
-  }
-};
-template <int NQ, int I>
-struct SplitHigh {
-  __device__ static constexpr int f(int u) { return NQ == 4 ? (u == 0 ? 16 + I : 23 - I) : 16 + I; }
-};
-
-template <int NQ, int I>
-__device__ __forceinline__ void split_block(const Frag &F, const Lane &L, const double *vc, const double *tt,
-                                            double *yq, double *y2q, int barid) {
-  using S = SplitSets<NQ, I>;
-  constexpr int NMA = S::NMA;
-  const int lane = L.lane;
-  // ---------------- phase A
-  double y[NMA][2];
-#pragma unroll
-  for (int u = 0; u < NMA; u++) y[u][0] = y[u][1] = 0.0;
-  constexpr int KS0 = 2 * S::ma(0), KS1 = imin_c(48, 2 * S::ma(NMA - 1) + 34);
-#pragma unroll
-  for (int ks = KS0; ks < KS1; ks++) {
-    const int ch = ks < 16 ? F.ch0 : (ks < 32 ? F.ch1 : F.ch2);
-    const double e = F.ew[ch + L.offEB + 4 * (ks & 15)];
-#pragma unroll
-    for (int u = 0; u < NMA; u++) {
-      const int mf = S::ma(u);
-      if (ks >= 2 * mf && ks <= 2 * mf + 33) dmma_nv(y[u], xsign(vc[L.offA + 568 * mf + 4 * ks], L.negConj), e);
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < NMA; u++) {
-    const int refl = 4 * S::ma(u) + (L.rr >> 1);
-#pragma unroll
-    for (int c = 0; c < 2; c++) yq[2 * ((2 * (lane & 3) + c) * LDY + refl) + (L.rr & 1)] = y[u][c];
-  }
-  asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(32 * NQ) : "memory");
-  // ---------------- phase B
-  const int offYB = 2 * ((lane >> 2) * LDY + L.kq) + (lane & 1);
-#pragma unroll
-  for (int u = 0; u < NMA; u++) {
-    const int mf = S::mb(u);
-    y[u][0] = y[u][1] = 0.0;
-#pragma unroll
-    for (int ks = 2 * mf; ks < 16; ks++) dmma_nv(y[u], xsign(tt[L.offT + 136 * ks + 8 * mf], L.negT), yq[offYB + 4 * ks]);
-  }
-#pragma unroll
-  for (int u = 0; u < NMA; u++) {
-    const int refl = 4 * S::mb(u) + (L.rr >> 1);
-#pragma unroll
-    for (int c = 0; c < 2; c++) y2q[2 * ((2 * (lane & 3) + c) * LDY + refl) + (L.rr & 1)] = y[u][c];
-  }
-  asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(32 * NQ) : "memory");
-  // ---------------- phase C
-  double yb[16];
-#pragma unroll
-  for (int ks = 0; ks < 16; ks++) yb[ks] = y2q[offYB + 4 * ks];
-  if (I == 0 && F.more) {
-    // the padding slot (current row 95) receives the next block's row 31
-    const int c = lane >> 2;
-    const int64_t row = F.rs + W;
-    const bool ok = (lane & 3) == 0 && row < F.n && c < F.ncols;
-    if ((lane & 3) == 0) cp_async16m(&F.Ew[c * LDE + ring_slot(F.base - 1)], ok ? F.E + row + (F.c0 + c) * F.lde : F.E, ok);
-  }
-  phase_c_rows<S::NLO, SplitLow<NQ, I>, true>(F, L, vc, yb);
-  cp_async_commit();
-  phase_c_rows<S::NHI, SplitHigh<NQ, I>, false>(F, L, vc, yb);
-}
-
-template <int NQ>
-__device__ __forceinline__ void split_dispatch(int I, const Frag &F, const Lane &L, const double *vc,
-                                               const double *tt, double *yq, double *y2q, int barid) {
-  switch (I) {
-    case 0: split_block<NQ, 0>(F, L, vc, tt, yq, y2q, barid); break;
-    case 1: split_block<NQ, 1>(F, L, vc, tt, yq, y2q, barid); break;
-    case 2: split_block<NQ, 2>(F, L, vc, tt, yq, y2q, barid); break;
-    case 3: split_block<NQ, 3>(F, L, vc, tt, yq, y2q, barid); break;
-    case 4: if constexpr (NQ > 4) split_block<NQ, 4 % NQ>(F, L, vc, tt, yq, y2q, barid); break;
-    case 5: if constexpr (NQ > 5) split_block<NQ, 5 % NQ>(F, L, vc, tt, yq, y2q, barid); break;
-    case 6: if constexpr (NQ > 6) split_block<NQ, 6 % NQ>(F, L, vc, tt, yq, y2q, barid); break;
-    default: if constexpr (NQ > 7) split_block<NQ, 7 % NQ>(F, L, vc, tt, yq, y2q, barid); break;
-  }
-}
-
-template <int NQ, int NG>
-__global__ void __launch_bounds__(32 * NQ * NG, 1) apply_q2s_kernel(Q2wArgs a) {
-  constexpr int TH = 32 * NQ * NG;
-  static_assert(NG * 8 * LDE + NG * 2 * 8 * LDY <= NFS * 8 * LDE, "split layout must fit the q2w window area");
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int g = w / NQ, I = w % NQ;
-  for (int e = threadIdx.x; e < OFF_T; e += TH) q2w_sm[e] = czero();
-  for (int e = threadIdx.x; e < NFS * 8 * LDE; e += TH) q2w_sm[OFF_E + e] = czero();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; i++) {
-      mbar_init(full_bar(i), 1);
-      *done_cnt(i) = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  BlkIt cur, ahead;
-  it_begin(a, cur);
-  ahead = cur;
-  if (w == 0) {
-    if (ahead.valid) issue_block(a, blk_src(a, ahead), 0, lane);
-    it_next(a, ahead);
-    if (ahead.valid) issue_block(a, blk_src(a, ahead), 1, lane);
-    it_next(a, ahead);
-  } else {
-    it_next(a, ahead);
-    it_next(a, ahead);
-  }
-  const int F = a.nfr_total, Gd = gridDim.x;
-  const int f0 = (int)((int64_t)F * blockIdx.x / Gd), f1 = (int)((int64_t)F * (blockIdx.x + 1) / Gd);
-  const Lane L(lane);
-  double *yq = reinterpret_cast<double *>(q2w_sm + OFF_E + NG * 8 * LDE + g * 2 * 8 * LDY);
-  double *y2q = yq + 2 * 8 * LDY;
-  const int barid = 1 + g;
-  Frag Fr;
-  Fr.Ew = q2w_sm + OFF_E + g * 8 * LDE;
-  Fr.ew = reinterpret_cast<double *>(Fr.Ew);
-  Fr.E = a.E;
-  Fr.lde = a.lde;
-  Fr.lde2 = 2 * a.lde;
-  Fr.n = a.n;
-  auto slab_k = [&](int sl) { return imax_c(0, imin_c(NG, f1 - (f0 + sl * NG))); };
-  BlkSrc asrc;
-  bool active = false;
-  int cur_sl = -1, nact = 0;
-  int64_t cnt = 0;
-  while (cur.valid) {
-    if (cur.sl != cur_sl) {
-      cur_sl = cur.sl;
-      const int k = slab_k(cur_sl);
-      nact = NQ * k;
-      active = g < k;
-      if (active) asrc = blk_src(a, ahead);
-      Fr.c0 = (int64_t)(f0 + cur_sl * NG + g) * 8;
-      Fr.ncols = active ? (int)imin64(8, a.m - Fr.c0) : 0;
-      const int cA = 2 * (lane & 3);
-      Fr.ok0 = cA < Fr.ncols;
-      Fr.ok1 = cA + 1 < Fr.ncols;
-    }
-    const int64_t i0 = cur.gi * G;
-    if (cur.j == 0) {
-      Fr.base = 0;
-      if (active) {
-        const int64_t rs = i0 + 1;
-        for (int e = lane + 32 * I; e < RING * 8; e += 32 * NQ) {
-          const int q = e % RING, c = e / RING;
-          const int64_t row = rs + q;
-          const bool ok = q < W && row < a.n && c < Fr.ncols;
-          cp_async16m(&Fr.Ew[c * LDE + q], ok ? a.E + row + (Fr.c0 + c) * a.lde : a.E, ok);
-        }
-        cp_async_commit();
-      }
-    }
-    const int bi = (int)(cnt & 1);
-    if (!active) {
-      it_next(a, cur);
-      it_next(a, ahead);
-      cnt++;
-      continue;
-    }
-    Fr.rs = i0 + 1 + cur.j * NB;
-    Fr.more = cur.j + 1 < cur.J;
-    const bool prof = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long *pp = prof ? a.prof + 24 : nullptr;
-    long long tl = prof ? clock64() : 0;
-    mbar_wait(full_bar(bi), (unsigned)((cnt >> 1) & 1));
-    pmark(pp, tl, 0);
-    cp_async_wait<0>();
-    __syncwarp();
-    pmark(pp, tl, 1);
-    asm volatile("bar.sync %0, %1;" ::"r"(barid), "r"(32 * NQ) : "memory");   // the group's refills / stores
-    pmark(pp, tl, 2);
-    Fr.ch0 = 2 * 32 * ((0 + Fr.base / 32) % 3);
-    Fr.ch1 = 2 * 32 * ((1 + Fr.base / 32) % 3);
-    Fr.ch2 = 2 * 32 * ((2 + Fr.base / 32) % 3);
-    Fr.gE = reinterpret_cast<double *>(a.E + Fr.rs + (L.rr >> 1) + (Fr.c0 + 2 * (lane & 3)) * a.lde) + (L.rr & 1);
-    split_dispatch<NQ>(I, Fr, L, reinterpret_cast<const double *>(vc_buf(bi)),
-                       reinterpret_cast<const double *>(t_buf(bi)), yq, y2q, barid);
-    pmark(pp, tl, 3);
-    if (!Fr.more) __threadfence_block();
-    Fr.base = Fr.base + NB >= RING ? Fr.base + NB - RING : Fr.base + NB;
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      last = atomicAdd(done_cnt(bi), 1) == nact - 1;
-      if (last) *done_cnt(bi) = 0;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last && ahead.valid && slab_k(ahead.sl) > 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_block(a, asrc, bi, lane);
-    }
-    pmark(pp, tl, 4);
-    it_next(a, cur);
-    it_next(a, ahead);
-    asrc = blk_src(a, ahead);
-    cnt++;
-  }
-}
-
 // ---------------------------------------------------------------- wavefront kernel (small m)
 // Block (g, j) of group g (sweeps 32g..32g+31, rows 32g+1+64j .. +94)
 // overlaps only blocks (g+1, j-1) and (g+1, j) of the group applied before it
@@ -870,7 +353,8 @@ constexpr int LDWV = 32 * WSLOTS + 1;   // chunks of 32 rows + 1 (odd: conflict-
 constexpr int WAVE_WARPS = Q2_WAVE_WARPS;   // items are claimed dynamically
 constexpr int OFF_WAVE_T = VC_STAGE;                 // layout: V | T | windows
 constexpr int OFF_WAVE_WIN = OFF_WAVE_T + T_STAGE;
-static_assert(OFF_WAVE_WIN + WAVE_WARPS * 8 * LDWV <= OFF_BAR, "wave windows must fit the q2w shared-memory size");
+constexpr int OFF_WAVE_END = OFF_WAVE_WIN + WAVE_WARPS * 8 * LDWV;
+static_assert(OFF_WAVE_END * 16 + 32 <= 227 * 1024, "wave kernel shared memory");
 
 __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArgs a, int64_t T) {
   namespace cg = cooperative_groups;
@@ -1016,11 +500,17 @@ __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArg
 
 }  // namespace
 
-size_t q2w_smem_bytes() { return (size_t)OFF_BAR * sizeof(double2) + 32; }
+size_t q2w_smem_bytes() { return (size_t)OFF_WAVE_END * sizeof(double2) + 32; }
 
-// Returns 1 if the shape is not handled here (caller falls back to q2.cu).
+// Returns 1 if the shape is not handled here (caller falls back to the
+// generic grouped kernel of q2.cu, which EIG_Q2_WAVE=0 also selects).
 int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, double2 *E, int64_t lde, int64_t m) {
   if (p.nb != NB || p.g != G) return 1;
+  static const int wave_env = [] {
+    const char *e = getenv("EIG_Q2_WAVE");
+    return e ? atoi(e) : 1;
+  }();
+  if (!wave_env) return 1;
   Q2wArgs a;
   a.n = p.n;
   a.m = m;
@@ -1033,46 +523,19 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
   a.E = E;
   a.nfr_total = (int)((m + 7) / 8);
   a.prof = ctx.q2_prof;
-  const int grid = std::min(ctx.num_sms, a.nfr_total);
-  const int per = (a.nfr_total + grid - 1) / grid;
-  a.nslab = (per + NFS - 1) / NFS;
+  a.nslab = 1;
   const size_t smem = q2w_smem_bytes();
-  // the wavefront kernel (measured faster at every m: n = 10^4, m = 1000 / 2500 /
-  // 5000 / 10000: 54 / 110 / 206 / 392 ms vs 135 / 274 / 306 / 404 ms for the
-  // per-fragment kernels below, which EIG_Q2_WAVE=0 selects)
-  static const int wave_env = [] {
-    const char *e = getenv("EIG_Q2_WAVE");
-    return e ? atoi(e) : 1;
-  }();
-  if (wave_env) {
-    int64_t T = 0;
-    for (int64_t g = 0; g < a.ngroups; g++) {
-      const int64_t i0 = g * G;
-      const int64_t J = (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
-      if (J > 0) T = std::max<int64_t>(T, J - 1 + (a.ngroups - 1 - g) + 1);
-    }
-    EIG_TRY(ctx.smem_attr((const void *)apply_q2wave_kernel, (int)smem, "q2wave attr"));
-    const int gridw = ctx.num_sms;
-    void *args[] = {&a, &T};
-    EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)apply_q2wave_kernel, dim3(gridw), dim3(32 * WAVE_WARPS), args, smem,
-                                                  ctx.stream), "q2wave launch"));
-    return ctx.launched("apply_q2wave_kernel");
+  int64_t T = 0;   // wavefront steps
+  for (int64_t g = 0; g < a.ngroups; g++) {
+    const int64_t i0 = g * G;
+    const int64_t J = (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
+    if (J > 0) T = std::max<int64_t>(T, J - 1 + (a.ngroups - 1 - g) + 1);
   }
-  // few fragments per SM: share each fragment over 8 warps (EIG_Q2W_SPLIT=0 disables)
-  static const int split_env = [] {
-    const char *e = getenv("EIG_Q2W_SPLIT");
-    return e ? atoi(e) : 1;
-  }();
-  if (split_env && per <= 2) {
-    a.nslab = (per + 1) / 2;
-    EIG_TRY(ctx.smem_attr((const void *)apply_q2s_kernel<8, 2>, (int)smem, "q2s attr"));
-    apply_q2s_kernel<8, 2><<<grid, 32 * 8 * 2, smem, ctx.stream>>>(a);
-    return ctx.launched("apply_q2s_kernel");
-  }
-  EIG_TRY(ctx.smem_attr((const void *)apply_q2w_kernel, (int)smem, "q2w attr"));
-  apply_q2w_kernel<<<grid, WT, smem, ctx.stream>>>(a);
-  EIG_TRY(ctx.launched("apply_q2w_kernel"));
-  return 0;
+  EIG_TRY(ctx.smem_attr((const void *)apply_q2wave_kernel, (int)smem, "q2wave attr"));
+  void *args[] = {&a, &T};
+  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)apply_q2wave_kernel, dim3(ctx.num_sms), dim3(32 * WAVE_WARPS),
+                                                args, smem, ctx.stream), "q2wave launch"));
+  return ctx.launched("apply_q2wave_kernel");
 }
 
 }  // namespace eig

@@ -249,10 +249,10 @@ def test_hotpath_parity(n, nb, g, m, m3):
 
 
 @gpu
-def test_apply_q2_per_fragment_kernels_subprocess():
-    """EIG_Q2_WAVE=0 selects the per-fragment Q2 kernels (apply_q2w_kernel for
-    >= 3 fragments per SM, apply_q2s_kernel below); the switch is read once per
-    process, so the check runs in a child process (same oracle comparison)."""
+def test_apply_q2_generic_kernel_subprocess():
+    """EIG_Q2_WAVE=0 routes nb = 64, g = 32 to the generic grouped kernel
+    (apply_q2_kernel, q2.cu) instead of the wavefront; the switch is read once
+    per process, so the check runs in a child process (same oracle comparison)."""
     import os
     import subprocess
     import sys
