@@ -61,12 +61,12 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
   double2 *sD = hsm;                  // [64][LDD] diagonal block (lower)
   double2 *sP0 = sD + 64 * LDD;       // two [64 cols][64 rows] bulge buffers (column-major, row index fast)
   double2 *sxg = sP0 + 2 * 64 * 64;   // [64] x of the first task of a sweep
-  __shared__ double2 sv[64];          // reflector
+  __shared__ double2 sv2[2][64];      // reflector of this task / of the next (computed early)
   __shared__ double2 sp[64];          // p, then w
   __shared__ double2 sg[64];          // g = tau (C v)
   __shared__ double2 sf[64];          // f = conj(tau) v^H Ablk
   __shared__ double2 spart[8][64];    // partial dot products
-  __shared__ double2 s_tau, s_beta;
+  __shared__ double2 s_tau2[2], s_beta2[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n = a.n;
   const int nb = a.nb, ldab = a.ldab;
@@ -105,8 +105,40 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
   // stored by task j (task j+1 stores the final values of that region), and
   // x / Ablk need no load; the reflector and the (a) update run before the
   // wait on sweep i-1, which only D_j and Cblk_j depend on.
+  // zlarfg (reading R1) of x = (x0 at lane, x1 at lane + 32), length len, by
+  // one warp, into reflector buffer b (entries in the band's scaled units,
+  // <= 1, see hb2st())
+  auto reflector = [&](double2 x0, double2 x1, double2 al, int len, int b) {
+    double nrm = (lane >= 1 ? x0.x * x0.x + x0.y * x0.y : 0.0) + x1.x * x1.x + x1.y * x1.y;
+    nrm = warp_sum(nrm);
+    double2 tau, scale;
+    double beta;
+    if (nrm == 0.0 && al.y == 0.0) {
+      tau = czero();
+      beta = al.x;
+      scale = czero();
+    } else {
+      beta = -copysign(sqrt(al.x * al.x + al.y * al.y + nrm), al.x);
+      const double ib = 1.0 / beta;   // two divisions instead of four (critical path)
+      tau = make_double2((beta - al.x) * ib, -al.y * ib);
+      const double2 d = make_double2(al.x - beta, al.y);
+      const double idd = 1.0 / (d.x * d.x + d.y * d.y);
+      scale = make_double2(d.x * idd, -d.y * idd);
+    }
+    sv2[b][lane] = (lane == 0) ? make_double2(1.0, 0.0) : (lane < len ? cmul(x0, scale) : czero());
+    sv2[b][lane + 32] = (lane + 32 < len) ? cmul(x1, scale) : czero();
+    if (lane == 0) {
+      s_tau2[b] = tau;
+      s_beta2[b] = make_double2(beta, 0.0);
+    }
+  };
+
+  // Pipelining across the tasks of a sweep: the target column of task j+1 is
+  // column 0 of task j's updated Cblk, so warp 0 updates that column first and
+  // builds task j+1's reflector while the other warps finish the (b) / (c)
+  // updates of task j; task j+1 then starts with its reflector in hand.
   for (int64_t i = blockIdx.x; i + 1 < n; i += gridDim.x) {
-    int cur = 0;
+    int cur = 0, rb = 0;
     int64_t off_next = a.off[0];   // V2 slot offsets, read one task ahead
     for (int64_t j = 0;; j++) {
       const int64_t off_j = off_next;
@@ -120,8 +152,8 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       const int nc = (int)(kend - r1);                        // rows below R
       double2 *sC = sP0 + cur * 4096;                         // this task's Cblk
       const double2 *sPrev = sP0 + (cur ^ 1) * 4096;          // previous task's Cblk = [x | Ablk]
-      const double2 *sx = (j == 0) ? sxg : sPrev;
       const double2 *sA = sPrev + 64;                         // Ablk column k at sA + k*64
+      const double2 *sv = sv2[rb];
       if (r1 < n - 1) off_next = a.off[j + 1];
       mark(-1);
       if (j == 0) {
@@ -132,43 +164,20 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
         __syncthreads();
       }
       mark(0);
-      // ---- reflector (x in shared memory)
-      if (warp == 0) {
-        const double2 x0 = lane < len ? sx[lane] : czero();
-        const double2 x1 = lane + 32 < len ? sx[lane + 32] : czero();
-        // zlarfg (reading R1) in the band's scaled units (entries <= 1, see hb2st())
-        double nrm = (lane >= 1 ? x0.x * x0.x + x0.y * x0.y : 0.0) + x1.x * x1.x + x1.y * x1.y;
-        nrm = warp_sum(nrm);
-        const double2 al = sx[0];
-        double2 tau, scale;
-        double beta;
-        if (nrm == 0.0 && al.y == 0.0) {
-          tau = czero();
-          beta = al.x;
-          scale = czero();
-        } else {
-          beta = -copysign(sqrt(al.x * al.x + al.y * al.y + nrm), al.x);
-          const double ib = 1.0 / beta;   // two divisions instead of four (critical path)
-          tau = make_double2((beta - al.x) * ib, -al.y * ib);
-          const double2 d = make_double2(al.x - beta, al.y);
-          const double idd = 1.0 / (d.x * d.x + d.y * d.y);
-          scale = make_double2(d.x * idd, -d.y * idd);
-        }
-        sv[lane] = (lane == 0) ? make_double2(1.0, 0.0) : (lane < len ? cmul(x0, scale) : czero());
-        sv[lane + 32] = (lane + 32 < len) ? cmul(x1, scale) : czero();
-        if (lane == 0) {
-          s_tau = tau;
-          s_beta = make_double2(beta, 0.0);
-        }
+      // ---- reflector: the first task of a sweep builds it here, the others
+      // got it from the previous task's update phase
+      if (j == 0) {
+        if (warp == 0)
+          reflector(lane < len ? sxg[lane] : czero(), lane + 32 < len ? sxg[lane + 32] : czero(), sxg[0], len, rb);
+        __syncthreads();
       }
-      __syncthreads();
-      const double2 tau = s_tau, ctau = cconj(tau);
+      const double2 tau = s_tau2[rb], ctau = cconj(tau);
       const bool upd = tau.x != 0.0 || tau.y != 0.0;
       {
         const int64_t slot = off_j + i;
         for (int t = tid; t < nb; t += HT) a.V2[slot * nb + t] = (t < len) ? sv[t] : czero();
         if (tid == 0) a.tau2[slot] = tau;
-        for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta : czero();
+        for (int t = tid; t < len; t += HT) *M(r0 + t, c) = (t == 0) ? s_beta2[rb] : czero();
       }
       __syncthreads();
       if (tid == 0) st_release_i32(a.progressA + i, (int)(j + 1));
@@ -242,19 +251,28 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
           for (int t = lane; t < len; t += 32) sp[t] = cadd(sp[t], cmul(al, sv[t]));
         }
         __syncthreads();
-        for (int e = tid; e < 64 * 64; e += HT) {          // (b) D - v w^H - w v^H  (lower), to global
-          const int rr = e & 63, cc = e >> 6;
-          if (rr < len && cc <= rr) {
-            double2 d = sD[rr + cc * LDD];
-            d = csub(d, cadd(cmul(sv[rr], cconj(sp[cc])), cmul(sp[rr], cconj(sv[cc]))));
-            if (rr == cc) d.y = 0.0;
-            *M(r0 + rr, r0 + cc) = d;
+        if (warp > 0) {
+          for (int e = tid - 32; e < 64 * 64; e += HT - 32) {   // (b) D - v w^H - w v^H (lower), to global
+            const int rr = e & 63, cc = e >> 6;
+            if (rr < len && cc <= rr) {
+              double2 d = sD[rr + cc * LDD];
+              d = csub(d, cadd(cmul(sv[rr], cconj(sp[cc])), cmul(sp[rr], cconj(sv[cc]))));
+              if (rr == cc) d.y = 0.0;
+              *M(r0 + rr, r0 + cc) = d;
+            }
           }
+          for (int e = tid - 32; e < 64 * 63; e += HT - 32) {   // (c) y - g v^H, columns 1.. (smem)
+            const int rr = e & 63, t = 1 + (e >> 6);
+            if (rr < nc && t < len) sC[rr + t * 64] = csub(sC[rr + t * 64], cmul(sg[rr], cconj(sv[t])));
+          }
+        } else {   // warp 0: column 0 of (c), which is the next task's target column
+          for (int rr = lane; rr < nc; rr += 32) sC[rr] = csub(sC[rr], cmul(sg[rr], cconj(sv[0])));
         }
-        for (int e = tid; e < 64 * 64; e += HT) {          // (c) y - g v^H, kept in shared memory
-          const int rr = e & 63, t = e >> 6;
-          if (rr < nc && t < len) sC[rr + t * 64] = csub(sC[rr + t * 64], cmul(sg[rr], cconj(sv[t])));
-        }
+      }
+      // warp 0: the next task's reflector from that column (its length is nc)
+      if (warp == 0 && r1 < n - 1) {
+        __syncwarp();
+        reflector(lane < nc ? sC[lane] : czero(), lane + 32 < nc ? sC[lane + 32] : czero(), sC[0], nc, rb ^ 1);
       }
       mark(3);
       // the barrier orders every thread's D / Ablk stores before thread 0's
@@ -264,6 +282,7 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
       if (tid == 0) st_release_i32(a.progress + i, (int)(j + 1));
       mark(5);
       cur ^= 1;
+      rb ^= 1;
     }
   }
   if (prof)
