@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FP64 TFLOP/s he2hb+back-transform; zhegv seconds n=10k at 1/2/4/8 B200"
 DMMA_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic_r01h.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic_r02.json")
 
 
 def ncu_traffic(kernel, n, m, nb, g):
@@ -417,8 +417,8 @@ def run_b200(a, rank, world, local_rank):
         traffic = ncu_traffic(q2k, n, m, nb, a.g) if dom == "q2" else None
         roof = {"bound": "tensor", "kernel": kern[dom], "stage": dom, "achieved": ach, "peak": peak,
                 "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
-                "traffic_note": "dram read+write bytes per launch (ncu --set full, profiles/traffic_r01h.json); "
-                                "algorithmic E traffic n^2/(2g) m 16 B each way = 2 x 250 GB (the wavefront kernel moves whole 95-row windows: ~3x); compute-bound",
+                "traffic_note": "dram read+write bytes per launch (ncu --set full, profiles/traffic_r02.json); "
+                                "algorithmic E traffic n^2/(2g) m 16 B each way = 2 x 250 GB (the wavefront kernel moves whole 95-row windows: 764 GB measured, 1.5x); compute-bound",
                 "peak_source": peak_src,
                 "stage_tflops": {k: stage_flops[k] / (stages[k] * 1e-3) / 1e12 for k in stages},
                 # tensor-pipe work: 3M issues 6 real flops per complex MAC (he2hb updates, Q1, trsm), the Q2
