@@ -7,10 +7,12 @@ standard-form matrix + complexify + Q2 + Q1 + L^-H on the m eigenvector columns.
 Metric (BASELINE.json): FP64 TFLOP/s of he2hb + back-transform, nominal flops
 16/3 n^3 + 20 n^2 m (8 real flops per complex multiply-add), workload n = 10000,
 m = 10000 (configs[3]).  N > 1 (torchrun, one process per GPU): the
-collective C-ABI call eig_hotpath runs he2hb on rank 0, broadcasts the factors
-over NCCL from inside libeigb200 (lower triangles, overlapped with he2hb) and
-back-transforms each rank's eigenvector column slice (strong scaling); the
-line adds t_BT(P) (max over ranks) and t_BT(1) / t_BT(P).
+collective C-ABI call eig_hotpath runs he2hb 1D block-cyclically over the
+ranks (EIG_DIST_HE2HB, NEXT-4; --no-dist-he2hb: on rank 0 with the factors
+broadcast as lower triangles), sends V2 / L over NCCL from inside libeigb200
+and back-transforms each rank's eigenvector column slice (strong scaling); the
+line adds t_BT(P) (max over ranks) and t_BT(1) / t_BT(P), and the zhegv
+seconds with both he2hb placements.
 Inputs (1.6 GB each) exceed L2 (126 MB), so no explicit L2 flush is needed.
 """
 from __future__ import annotations
@@ -65,7 +67,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-zhegv", action="store_true", help="skip the end-to-end generalized solve timing")
-    p.add_argument("--no-dist-he2hb", action="store_true", help="N > 1: skip the EIG_DIST_HE2HB zhegv timing")
+    p.add_argument("--no-dist-he2hb", action="store_true",
+                   help="N > 1: he2hb on rank 0 instead of 1D block-cyclic over the ranks (EIG_DIST_HE2HB)")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
     p.add_argument("--gemm", default="3m", choices=["3m", "4m"],
                    help="complex GEMMs (he2hb updates, Q1, L^-H, front end) as 3 real DMMA products (3M) or 4 (4M)")
@@ -311,8 +314,10 @@ def run_b200(a, rank, world, local_rank):
 
     from paper_1207_1773_b200 import EIG_NO_3M, EIG_USE_3M
     gflags = EIG_USE_3M if a.gemm == "3m" else EIG_NO_3M
+    from paper_1207_1773_b200 import EIG_DIST_HE2HB
+    dflag = 0 if a.no_dist_he2hb else EIG_DIST_HE2HB   # N > 1: he2hb 1D block-cyclic over the ranks (NEXT-4)
     solver = (Solver(local_rank, nb=nb, q2_group=a.g, flags=gflags) if world == 1
-              else collective_solver(local_rank, nb, a.g, flags=gflags))
+              else collective_solver(local_rank, nb, a.g, flags=gflags | dflag))
     stream = solver.stream
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     stage_names = ["he2hb", "q2", "q1", "trsm"]
@@ -481,9 +486,9 @@ def run_b200(a, rank, world, local_rank):
                  "note": "collective eig_solve_gen: rank 0 potrf, hegst, he2hb, hb2st, stedc; NCCL broadcast of "
                          "L / V1 / T1 (during hb2st) and V2 (during stedc), scatter of the eigenvector slices; "
                          "back-transform sharded by eigenvector columns; max over ranks"}
-        if not a.no_dist_he2hb:   # NEXT-4: the same solve with he2hb distributed over the ranks (EIG_DIST_HE2HB)
-            from paper_1207_1773_b200 import EIG_DIST_HE2HB
-            sd = collective_solver(local_rank, nb, a.g, flags=gflags | EIG_DIST_HE2HB)
+        zhegv["dist_he2hb"] = bool(dflag)
+        if True:   # the same solve with the other he2hb placement, for comparison
+            sd = collective_solver(local_rank, nb, a.g, flags=gflags | (EIG_DIST_HE2HB ^ dflag))
             if rank == 0:
                 Aw.copy_(A0)
                 Bw.copy_(B0)
@@ -498,8 +503,8 @@ def run_b200(a, rank, world, local_rank):
             dist.barrier()
             td = torch.tensor([dst["seconds"]["total"], dst["seconds"]["he2hb"]], dtype=torch.float64, device=dev)
             dist.all_reduce(td, op=dist.ReduceOp.MAX)
-            zhegv["dist_he2hb"] = {"seconds": float(td[0].item()), "he2hb_s_max": float(td[1].item()),
-                                   "note": "EIG_DIST_HE2HB: he2hb 1D block-cyclic over the ranks (NEXT-4)"}
+            zhegv["other_he2hb_placement"] = {"dist_he2hb": not dflag, "seconds": float(td[0].item()),
+                                              "he2hb_s_max": float(td[1].item())}
             sd.close()
         del Aw, Bw, B0, w_, Z_
     if rank == 0 and world == 1 and not a.no_zhegv:
@@ -527,7 +532,9 @@ def run_b200(a, rank, world, local_rank):
                 "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded SplitMix64; G1 Hermitian A', random unitary V2, well-conditioned L, real Z)",
                 "config": {"workload": f"he2hb+BT n={n} m={m} nb={nb} g={a.g}", "n": n, "m": m, "nb": nb,
-                           "q2_group": a.g, "parallelism": f"bt-columns{world}" if world > 1 else "single",
+                           "q2_group": a.g,
+                           "parallelism": (f"bt-columns{world}" + ("+he2hb-1d-cyclic" if dflag else "")) if world > 1
+                           else "single",
                            "gemm": a.gemm.upper(),
                            "zhegv_seconds_hotpath": ms_step * 1e-3,
                            "l2": "inputs (1.6 GB each) exceed L2; no flush needed",

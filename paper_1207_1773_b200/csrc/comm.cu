@@ -196,6 +196,36 @@ int coll_hotpath(Ctx &c, int64_t n, double2 *A, int64_t lda, double2 *tau1, doub
   c.st.m = m;   // this rank's slice width (the caller slices)
   c.st.col_hi = m;
   EIG_TRY(c.stat_begin(EIG_ST_TOTAL));
+  if ((c.flags & EIG_DIST_HE2HB) && !(flags & EIG_SKIP_HE2HB)) {
+    // NEXT-4: he2hb distributed over the ranks (he2hb_dist.cu); every rank
+    // ends with V1 (in dA) and T1, so only V2 / tau2 / L travel afterwards.
+    // All NCCL work in program order (one communicator, no concurrent streams).
+    const int P = c.nranks;
+    const int64_t nloc = dist_ncols(n, c.rank, P, nb);
+    double2 *Aloc = (double2 *)c.ws(WS_C_ALOC, (size_t)n * std::max<int64_t>(nloc, 1) * sizeof(double2));
+    double2 *work = (double2 *)c.ws(WS_C_DWORK, he2hb_dist_work(n, nb, P, c.rank) * sizeof(double2));
+    double2 *pack = (root && dlda != n) ? (double2 *)c.ws(WS_C_E, (size_t)n * n * sizeof(double2)) : nullptr;
+    if (!Aloc || !work || (root && dlda != n && !pack)) return EIG_ERR_NOMEM;
+    EIG_TRY(c.stat_begin(EIG_ST_HE2HB));
+    if (root) {
+      EIG_TRY(real_diag(c, n, dA, dlda));
+      EIG_TRY(herm_full(c, n, dA, dlda));
+    }
+    EIG_TRY(dist_scatter(c, n, dA, dlda, Aloc, pack));
+    EIG_TRY(he2hb_dist_nccl(c, n, Aloc, dA, dtau1, dT1, work, root ? dA : nullptr, dlda));
+    EIG_TRY(c.stat_end(EIG_ST_HE2HB));
+    c.st.flops[EIG_ST_HE2HB] = 16.0 / 3.0 * (double)n * n * n / P;
+    if (do_bt) {
+      EIG_TRY(order(c, c.stream, c.cstream, c.ev_c[0], "comm fork"));
+      EIG_TRY(bcast(c, dV2, (size_t)slots * nb * sizeof(double2), "bcast V2"));
+      EIG_TRY(bcast(c, dtau2, (size_t)slots * sizeof(double2), "bcast tau2"));
+      EIG_TRY(bcast_lower(c, dL, n, dldl, r.pk, "bcast L"));
+      EIG_TRY(order(c, c.cstream, c.stream, c.ev_c[2], "factors in"));
+      EIG_TRY(bt_run(c, n, Z, ldz, dV2, dtau2, dA, dlda, dT1, dL, dldl, E, lde, m));
+    }
+    EIG_TRY(c.stat_end(EIG_ST_TOTAL));
+    return c.check(cudaStreamSynchronize(c.stream), "sync");
+  }
   // the communication stream starts after the inputs already queued on the compute stream
   EIG_TRY(order(c, c.stream, c.cstream, c.ev_c[0], "comm fork"));
   if (do_bt) {   // inputs of the back-transform: available now, overlap he2hb on rank 0

@@ -105,7 +105,7 @@ struct DistRank {
   int64_t nloc;
   double2 *V1;           // n x n, ld n: V1 tails in the he2hb layout (receives every panel's V)
   double2 *tau, *T;      // K nb, K nb nb
-  double2 *Vb, *Wb, *Xb, *Gb, *Sm;   // work: V (s x nb), W / X (s x nb), gathered rows, small
+  double2 *Vb, *Wb, *Xb, *Gb, *Sm;   // work: V (2 buffers of s x nb), W / X (s x nb), gathered rows, small
   double2 *Wpart;        // this rank's partial W
 };
 
@@ -172,24 +172,27 @@ int he2hb_dist_run(Ctx &c, int64_t n, DistOps &ops) {
       if (R[q].r == owner) return q;
     return -1;
   };
+  const int64_t s0 = n - nb;
+  auto vbuf = [&](DistRank &d, int64_t k) { return d.Vb + (k & 1) * s0 * nb; };   // V_k, double-buffered
+  // panel 0 on its owner
+  if (K > 0) {
+    const int qo = local_of(0);
+    if (qo >= 0)
+      EIG_TRY(panel_qr(c, R[qo].Aloc + nb, n, n - nb, nb, R[qo].tau, R[qo].T, vbuf(R[qo], 0), nullptr, n - nb,
+                       c.stream));
+  }
   for (int64_t k = 0; k < K; k++) {
     const int64_t r0 = (k + 1) * nb, s = n - r0;
     const int owner = (int)(k % P);
-    const int qo = local_of(owner);
     const int nref = (int)std::min<int64_t>(nb, s);
-    // a1-a2: panel on its owner (explicit V into Vb, ld s)
-    if (qo >= 0) {
-      DistRank &o = R[qo];
-      const int64_t lc = (k / P) * nb;   // local column of block k
-      EIG_TRY(panel_qr(c, o.Aloc + r0 + lc * n, n, s, nb, o.tau + k * nb, o.T + k * nb * nb, o.Vb, nullptr, s,
-                       c.stream));
-    }
+    // a1-a2 ran on the owner: panel 0 above, panel k > 0 on the side stream during step k-1 (look-ahead)
+    if (k > 0 && local_of(owner) >= 0) EIG_TRY(c.check(cudaStreamWaitEvent(c.stream, c.ev_join, 0), "panel join"));
     // V_k, T_k, tau_k to every rank (the BT needs them all: V1 and T1 stay replicated)
-    EIG_TRY(ops.bcast(bufs([](DistRank &d) { return d.Vb; }), (size_t)s * nb, owner));
+    EIG_TRY(ops.bcast(bufs([&](DistRank &d) { return vbuf(d, k); }), (size_t)s * nb, owner));
     EIG_TRY(ops.bcast(bufs([&](DistRank &d) { return d.T + k * nb * nb; }), (size_t)nb * nb, owner));
     EIG_TRY(ops.bcast(bufs([&](DistRank &d) { return d.tau + k * nb; }), (size_t)nb, owner));
     for (auto &d : R) {
-      place_v_kernel<<<grid_for(c, s * nref), 256, 0, c.stream>>>(s, nref, d.Vb, s, d.V1 + r0 + k * nb * n, n);
+      place_v_kernel<<<grid_for(c, s * nref), 256, 0, c.stream>>>(s, nref, vbuf(d, k), s, d.V1 + r0 + k * nb * n, n);
       EIG_TRY(c.launched("place_v_kernel"));
     }
     // a3: W_r = A[r0:, J_r] V[J_r]
@@ -199,7 +202,7 @@ int he2hb_dist_run(Ctx &c, int64_t n, DistOps &ops) {
       lc0[q] = std::min<int64_t>(d.nloc, first_local_ge(r0, d.r, P, nb));
       nl[q] = d.nloc - lc0[q];
       if (nl[q] > 0) {
-        gather_rows_kernel<<<grid_for(c, nl[q] * nb), 256, 0, c.stream>>>(nl[q], lc0[q], d.r, P, nb, r0, nb, d.Vb, s,
+        gather_rows_kernel<<<grid_for(c, nl[q] * nb), 256, 0, c.stream>>>(nl[q], lc0[q], d.r, P, nb, r0, nb, vbuf(d, k), s,
                                                                            d.Gb, nl[q]);
         EIG_TRY(c.launched("gather_rows_kernel"));
         Zgemm g;
@@ -219,14 +222,14 @@ int he2hb_dist_run(Ctx &c, int64_t n, DistOps &ops) {
       g.M = s; g.N = nb; g.K = nb; g.A = d.Wb; g.lda = s; g.B = Tk; g.ldb = nb; g.C = d.Xb; g.ldc = s;
       EIG_TRY(zgemm(c, g));   // X = W T
       g = Zgemm();
-      g.opa = OP_C; g.M = nb; g.N = nb; g.K = s; g.A = d.Vb; g.lda = s; g.B = d.Xb; g.ldb = s; g.C = d.Sm; g.ldc = nb;
+      g.opa = OP_C; g.M = nb; g.N = nb; g.K = s; g.A = vbuf(d, k); g.lda = s; g.B = d.Xb; g.ldb = s; g.C = d.Sm; g.ldc = nb;
       EIG_TRY(zgemm(c, g));   // V^H (W T)
       g = Zgemm();
       g.opa = OP_C; g.M = nb; g.N = nb; g.K = nb; g.A = Tk; g.lda = nb; g.B = d.Sm; g.ldb = nb; g.C = d.Sm + nb * nb;
       g.ldc = nb;
       EIG_TRY(zgemm(c, g));   // M = T^H V^H W T
       g = Zgemm();
-      g.M = s; g.N = nb; g.K = nb; g.A = d.Vb; g.lda = s; g.B = d.Sm + nb * nb; g.ldb = nb; g.C = d.Xb; g.ldc = s;
+      g.M = s; g.N = nb; g.K = nb; g.A = vbuf(d, k); g.lda = s; g.B = d.Sm + nb * nb; g.ldb = nb; g.C = d.Xb; g.ldc = s;
       g.alpha = -0.5; g.beta = 1.0;
       EIG_TRY(zgemm(c, g));   // X = W T - 1/2 V M
     }
@@ -238,16 +241,35 @@ int he2hb_dist_run(Ctx &c, int64_t n, DistOps &ops) {
       gather_rows_kernel<<<grid_for(c, nl[q] * nb), 256, 0, c.stream>>>(nl[q], lc0[q], d.r, P, nb, r0, nb, d.Xb, s,
                                                                          XV, nl[q]);
       EIG_TRY(c.launched("gather_rows_kernel"));
-      gather_rows_kernel<<<grid_for(c, nl[q] * nb), 256, 0, c.stream>>>(nl[q], lc0[q], d.r, P, nb, r0, nb, d.Vb, s,
+      gather_rows_kernel<<<grid_for(c, nl[q] * nb), 256, 0, c.stream>>>(nl[q], lc0[q], d.r, P, nb, r0, nb, vbuf(d, k), s,
                                                                          XV + nl[q] * nb, nl[q]);
       EIG_TRY(c.launched("gather_rows_kernel"));
       // [V | X] side by side: V in Vb, X in Xb (both ld s) -> two K = nb products
-      Zgemm g;
-      g.opb = OP_C; g.M = s; g.N = nl[q]; g.K = nb; g.A = d.Vb; g.lda = s; g.B = XV; g.ldb = nl[q];
-      g.C = d.Aloc + r0 + lc0[q] * n; g.ldc = n; g.alpha = -1.0; g.beta = 1.0;
-      EIG_TRY(zgemm(c, g));   // -= V X_g^H
-      g.A = d.Xb; g.B = XV + nl[q] * nb;
-      EIG_TRY(zgemm(c, g));   // -= X V_g^H
+      auto update = [&](int64_t c0, int64_t cn) -> int {   // local trailing columns lc0 + c0 .. + cn
+        if (cn <= 0) return 0;
+        Zgemm g;
+        g.opb = OP_C; g.M = s; g.N = cn; g.K = nb; g.A = vbuf(d, k); g.lda = s; g.B = XV + c0; g.ldb = nl[q];
+        g.C = d.Aloc + r0 + (lc0[q] + c0) * n; g.ldc = n; g.alpha = -1.0; g.beta = 1.0;
+        EIG_TRY(zgemm(c, g));   // -= V X_g^H
+        g.A = d.Xb; g.B = XV + nl[q] * nb + c0;
+        return zgemm(c, g);     // -= X V_g^H
+      };
+      const bool next_mine = (k + 1 < K) && (int)((k + 1) % P) == d.r;
+      if (next_mine) {
+        // look-ahead (Fig. 1 "(a) can be overlapped with (c)"): block k+1 is this
+        // rank's first trailing block; update it, run panel k+1 on the side
+        // stream, and update the remaining columns meanwhile
+        EIG_TRY(update(0, nb));
+        EIG_TRY(c.check(cudaEventRecord(c.ev_fork, c.stream), "fork"));
+        EIG_TRY(c.check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "fork wait"));
+        const int64_t r1 = r0 + nb;
+        EIG_TRY(panel_qr(c, d.Aloc + r1 + lc0[q] * n, n, n - r1, nb, d.tau + (k + 1) * nb, d.T + (k + 1) * nb * nb,
+                         vbuf(d, k + 1), nullptr, n - r1, c.side));
+        EIG_TRY(c.check(cudaEventRecord(c.ev_join, c.side), "join"));
+        EIG_TRY(update(nb, nl[q] - nb));
+      } else {
+        EIG_TRY(update(0, nl[q]));
+      }
     }
   }
   return 0;
@@ -286,7 +308,7 @@ int he2hb_sim(Ctx &c, int64_t n, int P, double2 *A, int64_t lda, double2 *tau, d
     if (q != 0) d.V1 = dalloc((size_t)n * n);
     d.tau = (q == 0) ? tau : dalloc((size_t)K * nb);
     d.T = (q == 0) ? T : dalloc((size_t)K * nb * nb);
-    d.Vb = dalloc((size_t)s0 * nb);
+    d.Vb = dalloc((size_t)2 * s0 * nb);
     d.Wb = dalloc((size_t)s0 * nb);
     d.Xb = dalloc((size_t)s0 * nb);
     d.Wpart = dalloc((size_t)s0 * nb);
@@ -416,7 +438,7 @@ int he2hb_dist_nccl(Ctx &c, int64_t n, double2 *Aloc, double2 *V1, double2 *tau,
   d.tau = tau;
   d.T = T;
   d.Vb = work;
-  d.Wb = d.Vb + s0 * nb;
+  d.Wb = d.Vb + 2 * s0 * nb;
   d.Xb = d.Wb + s0 * nb;
   d.Wpart = d.Xb + s0 * nb;
   d.Gb = d.Wpart + s0 * nb;
@@ -469,7 +491,7 @@ size_t he2hb_dist_work(int64_t n, int nb, int P, int rank) {
   const int64_t s0 = std::max<int64_t>(n - nb, 1);
   const int64_t NB = (n + nb - 1) / nb, maxblk = (NB + P - 1) / P;
   const size_t slab = (size_t)maxblk * 2 * nb * nb;
-  return (size_t)4 * s0 * nb + (size_t)n * 2 * nb + 2 * nb * nb + slab * (rank == 0 ? P : 1);
+  return (size_t)5 * s0 * nb + (size_t)n * 2 * nb + 2 * nb * nb + slab * (rank == 0 ? P : 1);
 }
 int64_t dist_ncols(int64_t n, int rank, int P, int nb) { return ncols_of(n, rank, P, nb); }
 

@@ -112,3 +112,26 @@ def test_collective_solve_gen_distributed_he2hb_p1(n, nb):
     assert one(R) / (n * one(Ad) * one(Z)) < 1e-14
     assert one(Z.conj().T @ Bd @ Z - torch.eye(n, dtype=Z.dtype, device=Z.device)) / n < 1e-14
     assert st["seconds"]["he2hb"] > 0 and st["bytes_comm"] > 0
+
+
+@gpu
+@pytest.mark.parametrize("n,nb,g,m", [(600, 64, 32, 333), (513, 32, 16, 100)])
+def test_collective_hotpath_distributed_he2hb_p1(n, nb, g, m):
+    """EIG_DIST_HE2HB in the collective hot path (one-rank communicator): E
+    agrees with the single-GPU hot path to the parity tolerance (the
+    distributed reduction sums W by ranks and updates full columns, so it is
+    not bitwise the one-GPU reduction)."""
+    from paper_1207_1773_b200 import EIG_DIST_HE2HB, Solver
+    A = synth.rand_hermitian(n, 4)
+    V2, tau2 = synth.synthetic_v2(n, nb, 4)
+    L = synth.unit_lower(n, 4)
+    Z = synth.real_orthonormalish(n, m, 4)
+    dV2, dt2 = torch.from_numpy(V2).cuda(), torch.from_numpy(tau2).cuda()
+    E1, _, _ = Solver(0, nb=nb, q2_group=g).hotpath(_dev(A), dV2, dt2, _dev(L), _dev(Z))
+    sc = _coll(nb=nb, g=g, flags=EIG_DIST_HE2HB)
+    E, _, _ = sc.hotpath(_dev(A), dV2, dt2, _dev(L), _dev(Z))
+    torch.cuda.synchronize()
+    err = (E - E1).abs().max().item() / E1.abs().max().item()
+    assert err < 1e-11, err
+    st = sc.last_stats()
+    assert st["seconds"]["he2hb"] > 0 and st["seconds"]["bt"] > 0
