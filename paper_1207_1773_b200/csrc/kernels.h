@@ -36,6 +36,9 @@ struct Zgemm {
 // N used by the back-transform GEMMs for their split-K choice (columns of E
 // are the sharded dimension)
 constexpr int64_t kBtSplitN = 1024;
+// 3M products with K <= kShortK take the short-K engine
+// variant (64 x 32 tiles, two CTAs per SM); see zgemm.cu
+constexpr int64_t kShortK = 256;
 
 // Enqueue C = alpha op(A) op(B) + beta C on ctx's stream.  Returns 0 or error.
 int zgemm(Ctx &ctx, const Zgemm &g);

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -32,21 +33,25 @@
 namespace eig {
 namespace {
 
-constexpr int BM = 64, BN = 64;
-// 3M warp tile: 16 complex rows x M3_WN complex cols (4 x (64 / M3_WN) warps)
-#ifndef M3_WN
-#define M3_WN 32
-#endif
-__host__ __device__ constexpr int threads_of(bool m3) { return m3 ? 32 * 4 * (BN / M3_WN) : 256; }
+constexpr int BM = 64, THREADS = 256;
+// Engine variants V: 0 = real embedding (4 real products; BN 64, BK 16, two
+// 120-register CTAs per SM); 1 = 3M, long K (BN 64, BK 32, warp tile 16 x 32,
+// one 208-register CTA per SM); 2 = 3M, short K (BN 32, BK 16, warp tile
+// 16 x 16, two CTAs per SM, so one CTA's prologue / epilogue overlaps the
+// other's main loop — the he2hb rank-2k update and the K = 256 Q1 update).
 // Shared-memory layouts (complex elements).  4M: 8-byte fragment loads;
 // 3M: 16-byte complex loads, eight lanes per phase (row g = lane>>2 in {0,1},
 // k t = lane&3), so the k-major strides are 2 mod 8 and the k-contiguous ones
 // 4 mod 8 (eight distinct 16-byte bank groups per phase).
-template <bool M3>
+template <int V>
 struct Lay {
-  // K tile (complex): 3M runs one 198-register CTA per SM, so it takes twice
-  // the K per pipeline stage (half the CTA barriers per flop)
-  static constexpr int BK = M3 ? 32 : 16;
+  static constexpr bool M3 = V >= 1;
+  static constexpr int BN = V == 2 ? 32 : 64;
+  static constexpr int WN = V == 2 ? 16 : 32;   // 3M warp tile width (complex columns)
+  static constexpr int MINB = V == 1 ? 1 : 2;   // resident CTAs per SM
+  // K tile (complex): variant 1 runs one CTA per SM, so it takes twice the K
+  // per pipeline stage (half the CTA barriers per flop)
+  static constexpr int BK = V == 1 ? 32 : 16;
   static constexpr int STAGES = 3;
   static constexpr int LDA_S = M3 ? BM + 2 : BM + 4;  // sA[k][m]: k-major, m contiguous
   static constexpr int LDB_S = M3 ? BK + 4 : BK + 2;  // sB[n][k]: n-major, k contiguous
@@ -73,10 +78,11 @@ struct Params {
   int tiles_m;
 };
 
-template <int OPA, int OPB, bool HERM, int LOWER, bool M3>
-__global__ void __launch_bounds__(threads_of(M3), M3 ? 1 : 2) zgemm_kernel(Params p) {
-  constexpr int THREADS = threads_of(M3);
-  using LY = Lay<M3>;
+template <int OPA, int OPB, bool HERM, int LOWER, int V>
+__global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) {
+  using LY = Lay<V>;
+  constexpr bool M3 = LY::M3;
+  constexpr int BN = LY::BN, M3_WN = LY::WN;
   constexpr int BK = LY::BK, STAGES = LY::STAGES;
   constexpr int LDA_S = LY::LDA_S, LDB_S = LY::LDB_S, LDAK = LY::LDAK, LDBN = LY::LDBN;
   constexpr int SA_ELEMS = LY::SA_ELEMS, STAGE_ELEMS = LY::STAGE_ELEMS;
@@ -86,12 +92,15 @@ __global__ void __launch_bounds__(threads_of(M3), M3 ? 1 : 2) zgemm_kernel(Param
 
   int tm, tn;
   if (LOWER == 1) {
+    // tile row I holds q (I + 1) column tiles (q = BM / BN): rows before it
+    // hold q I (I + 1) / 2 tiles
+    constexpr int q = BM / BN;
     const int64_t x = blockIdx.x;
-    int64_t I = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
-    while ((I + 1) * (I + 2) / 2 <= x) I++;
-    while (I * (I + 1) / 2 > x) I--;
+    int64_t I = (int64_t)((sqrt(8.0 * (double)x / q + 1.0) - 1.0) * 0.5);
+    while (q * (I + 1) * (I + 2) / 2 <= x) I++;
+    while (q * I * (I + 1) / 2 > x) I--;
     tm = (int)I;
-    tn = (int)(x - I * (I + 1) / 2);
+    tn = (int)(x - q * I * (I + 1) / 2);
   } else {
     tm = blockIdx.x % p.tiles_m;
     tn = blockIdx.x / p.tiles_m;
@@ -431,18 +440,18 @@ __global__ void splitk_reduce_kernel(int64_t M, int64_t N, int split, const doub
   }
 }
 
-template <int OPA, int OPB, bool HERM, int LOWER>
-int launch_t(Ctx &ctx, const Params &p, dim3 grid, bool m3) {
-  if (m3) {
-    constexpr size_t sm = Lay<true>::SMEM_BYTES;
-    EIG_TRY(ctx.smem_attr((const void *)zgemm_kernel<OPA, OPB, HERM, LOWER, true>, (int)sm, "zgemm attr"));
-    zgemm_kernel<OPA, OPB, HERM, LOWER, true><<<grid, threads_of(true), sm, ctx.stream>>>(p);
-  } else {
-    constexpr size_t sm = Lay<false>::SMEM_BYTES;
-    EIG_TRY(ctx.smem_attr((const void *)zgemm_kernel<OPA, OPB, HERM, LOWER, false>, (int)sm, "zgemm attr"));
-    zgemm_kernel<OPA, OPB, HERM, LOWER, false><<<grid, threads_of(false), sm, ctx.stream>>>(p);
-  }
+template <int OPA, int OPB, bool HERM, int LOWER, int V>
+int launch_v(Ctx &ctx, const Params &p, dim3 grid) {
+  constexpr size_t sm = Lay<V>::SMEM_BYTES;
+  EIG_TRY(ctx.smem_attr((const void *)zgemm_kernel<OPA, OPB, HERM, LOWER, V>, (int)sm, "zgemm attr"));
+  zgemm_kernel<OPA, OPB, HERM, LOWER, V><<<grid, THREADS, sm, ctx.stream>>>(p);
   return ctx.launched("zgemm_kernel");
+}
+template <int OPA, int OPB, bool HERM, int LOWER>
+int launch_t(Ctx &ctx, const Params &p, dim3 grid, int v) {
+  if (v == 2) return launch_v<OPA, OPB, HERM, LOWER, 2>(ctx, p, grid);
+  if (v == 1) return launch_v<OPA, OPB, HERM, LOWER, 1>(ctx, p, grid);
+  return launch_v<OPA, OPB, HERM, LOWER, 0>(ctx, p, grid);
 }
 
 }  // namespace
@@ -453,27 +462,37 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   if (g.herm_a && (g.opa != OP_N || g.M != g.K)) return -2;
   if (g.lower_c == 1 && g.M != g.N) return -2;
 
+  const bool m3 = g.m3 > 0 || (g.m3 == 0 && ctx.use_3m);
+  // 3M short-K variant (2 CTAs/SM) where the K loop is too short to hide a
+  // CTA's prologue and epilogue; EIG_ZGEMM_SHORTK=<K> moves the threshold
+  // (0 disables it)
+  static const int64_t shortk = [] {
+    const char *e = getenv("EIG_ZGEMM_SHORTK");
+    return e ? (int64_t)atoll(e) : (int64_t)kShortK;
+  }();
+  const int v = !m3 ? 0 : (g.K <= shortk ? 2 : 1);
+  const int BN = v == 2 ? Lay<2>::BN : Lay<0>::BN;
+  const int64_t q = BM / BN;
   const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
-  const int64_t tiles = g.lower_c == 1 ? (int64_t)tiles_m * (tiles_m + 1) / 2 : (int64_t)tiles_m * tiles_n;
+  const int64_t tiles = g.lower_c == 1 ? q * tiles_m * (tiles_m + 1) / 2 : (int64_t)tiles_m * tiles_n;
   // the split model sees N = split_n when set (N-independent split, see kernels.h)
   const int64_t Nm = g.split_n > 0 ? g.split_n : g.N;
   const int64_t tiles_model =
       g.split_n > 0 ? (int64_t)tiles_m * ((g.split_n + BN - 1) / BN) : tiles;
-  const bool m3 = g.m3 > 0 || (g.m3 == 0 && ctx.use_3m);
-  const int BK = m3 ? Lay<true>::BK : Lay<false>::BK;
+  const int BK = v == 1 ? Lay<1>::BK : Lay<0>::BK;
   const int64_t ktiles = std::max<int64_t>(1, (g.K + BK - 1) / BK);
   int split = g.splitk;
   if (split <= 0) {
-    // pick the split that minimises (waves of 2 CTAs/SM) x (k-tiles per CTA + fixed per-CTA cost),
+    // pick the split that minimises (waves of resident CTAs) x (k-tiles per CTA + fixed per-CTA cost),
     // plus the partial-sum traffic of the reduction (in k-tile units)
-    const int64_t cap = (m3 ? 1LL : 2LL) * ctx.num_sms;   // resident CTAs (3M: one 255-register CTA per SM)
+    const int64_t cap = (v == 1 ? 1LL : 2LL) * ctx.num_sms;   // resident CTAs (variant 1: one 208-register CTA per SM)
     const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(64, ktiles / 4));
     double best = 1e300;
     split = 1;
     for (int64_t sp = 1; sp <= maxs; sp++) {
       const int64_t kt = (ktiles + sp - 1) / sp;
       const int64_t waves = (tiles_model * sp + cap - 1) / cap;
-      const double red = sp > 1 ? 0.02 * (double)sp * (double)g.M * (double)Nm / (double)(cap * 64 * 64) * 8.0 : 0.0;
+      const double red = sp > 1 ? 0.02 * (double)sp * (double)g.M * (double)Nm / (double)(cap * BM * BN) * 8.0 : 0.0;
       const double t = (double)waves * (double)(kt + 3) + red;
       if (t < best * 0.98) {
         best = t;
@@ -508,22 +527,22 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   dim3 grid((unsigned)tiles, (unsigned)split);
   int rc;
   if (g.herm_a)
-    rc = launch_t<OP_N, OP_N, true, 0>(ctx, p, grid, m3);
+    rc = launch_t<OP_N, OP_N, true, 0>(ctx, p, grid, v);
   else if (g.lower_c == 1) {
-    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 1>(ctx, p, grid, m3);
-    else if (g.opa == OP_N && g.opb == OP_N) rc = launch_t<OP_N, OP_N, false, 1>(ctx, p, grid, m3);
+    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 1>(ctx, p, grid, v);
+    else if (g.opa == OP_N && g.opb == OP_N) rc = launch_t<OP_N, OP_N, false, 1>(ctx, p, grid, v);
     else return -2;
   } else if (g.lower_c == 2) {
-    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 2>(ctx, p, grid, m3);
+    if (g.opa == OP_N && g.opb == OP_C) rc = launch_t<OP_N, OP_C, false, 2>(ctx, p, grid, v);
     else return -2;
   } else if (g.opa == OP_N && g.opb == OP_N)
-    rc = launch_t<OP_N, OP_N, false, 0>(ctx, p, grid, m3);
+    rc = launch_t<OP_N, OP_N, false, 0>(ctx, p, grid, v);
   else if (g.opa == OP_C && g.opb == OP_N)
-    rc = launch_t<OP_C, OP_N, false, 0>(ctx, p, grid, m3);
+    rc = launch_t<OP_C, OP_N, false, 0>(ctx, p, grid, v);
   else if (g.opa == OP_N && g.opb == OP_C)
-    rc = launch_t<OP_N, OP_C, false, 0>(ctx, p, grid, m3);
+    rc = launch_t<OP_N, OP_C, false, 0>(ctx, p, grid, v);
   else
-    rc = launch_t<OP_C, OP_C, false, 0>(ctx, p, grid, m3);
+    rc = launch_t<OP_C, OP_C, false, 0>(ctx, p, grid, v);
   if (rc) return rc;
   if (split > 1) {
     const int64_t total = g.M * g.N;
