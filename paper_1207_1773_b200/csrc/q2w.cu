@@ -356,15 +356,199 @@ constexpr int OFF_WAVE_WIN = OFF_WAVE_T + T_STAGE;
 constexpr int OFF_WAVE_END = OFF_WAVE_WIN + WAVE_WARPS * 8 * LDWV;
 static_assert(OFF_WAVE_END * 16 + 32 <= 227 * 1024, "wave kernel shared memory");
 
+// ---------------------------------------------------------------- 3M form
+// The three contractions of an item with complex operands split into real
+// planes (reading R18, Gauss): per contraction three real DMMA products
+// instead of the embedding's four, on 8 x 4 real tiles:
+//   phase A  Y = V^H E:   P1 = Vr.Er, P2 = Vi.Ei, P3 = (Vr+Vi).(Er-Ei);
+//                         Re Y = P1 + P2, Im Y = P1 - P2 - P3
+//   phase B  Y' = T Y:    P1 = Tr.Yr, P2 = Ti.Yi, P3 = (Tr+Ti).(Yr+Yi);
+//                         -Y' = (P2 - P1, P1 + P2 - P3)   (kept negated)
+//   phase C  E += V (-Y'): accumulators start at (Er, 0, Er+Ei);
+//                         E' = (P1 - P2, P3 - P1 - P2)
+// DMMA count per item 216 + 60 + 216 = 492 (the embedding: 616).  The V and
+// T planes (Vr, Vi, Vr+Vi; Tr, Ti, Tr+Ti) are built once per block when the
+// CTA stages them; only the E / Y plane sums and the recombinations are
+// per-item FP64 adds (184 per lane, ~0.16 DMMA each, tools/peaks/dmma_dadd.cu).
+//
+// V plane layout (doubles): V[q][t] (t = reflector, q = window row, 0 <= q-t
+// < 64) at t LDP + PADP + q - t, LDP = 77: the accesses of both phases read
+// q - t in [-7, 71], which stays inside row t's zero pads (rows overlap only
+// in pads), and 76 = 12 mod 16 makes the 8-byte fragment loads of phase A
+// (t = lane>>2, q = lane&3) and phase C (q = lane>>2, t = lane&3)
+// conflict-free.  T planes: the 20 nonzero 8 x 4 tiles of the upper
+// triangle, each in fragment (lane) order.
+constexpr int LDP = 77, PADP = 8;
+constexpr int VP_PLANE = 2472;   // >= 31 LDP + PADP + 72, multiple of 8
+constexpr int TP_PLANE = 640;    // 20 tiles x 32
+constexpr int OFF3_T = 3 * VP_PLANE / 2;            // complex units
+constexpr int OFF3_WIN = OFF3_T + 3 * TP_PLANE / 2;
+__host__ __device__ constexpr int ttile(int mf, int ks) { return mf * (9 - mf) + ks - 2 * mf; }
+// phase A reads window column sigma(n) as B column n (conflict-free 16-byte
+// loads); the phase-B result is returned to E column order in its shuffle
+__host__ __device__ constexpr int sigma_col(int n) { return (n >> 1) + 4 * (n & 1); }
+__host__ __device__ constexpr int sigma_inv(int e) { return e < 4 ? 2 * e : 2 * (e - 4) + 1; }
+
+// accumulator (rows 8mf + lane>>2, columns 2(lane&3) + h) -> B operand of
+// k-step ks (row 4ks + (lane&3), column n = the lane's column index ncol)
+__device__ __forceinline__ void acc_to_b3(const double (&acc)[4][2], double (&bl)[8], int lane, int ncol) {
+  const int src_lo = 4 * (lane & 3) + (ncol >> 1);
+  const bool hi = ncol & 1;
+#pragma unroll
+  for (int ks = 0; ks < 8; ks++) {
+    const int src = src_lo + 16 * (ks & 1);
+    const double v0 = __shfl_sync(0xffffffffu, acc[ks >> 1][0], src);
+    const double v1 = __shfl_sync(0xffffffffu, acc[ks >> 1][1], src);
+    bl[ks] = hi ? v1 : v0;
+  }
+}
+
+struct Item3 {
+  const double2 *Ew;      // warp's window (complex), column stride LDWV
+  int s0, s1, s2;         // chunk slot bases (complex rows)
+  int64_t rs, n, lde;     // first window row, matrix rows, E leading dimension
+  double2 *gE;            // E + rs + c0 lde
+  int ncols;
+};
+
+// phase-C row groups (8 rows) per batch: k-step counts 2,4,6,8,8,8,8,8,8,6,4,2
+// balanced as (r, r+4, r+8) = 18 k-steps each
+template <int WPEND>
+__device__ __forceinline__ void full_block3(const Item3 &F, int lane, const double *vp, const double *tp) {
+  const int g8 = lane >> 2, t4 = lane & 3;
+  // ---------------- phase A: Y = V^H E (tile (mf, ks) nonzero for 0 <= 4ks - 8mf <= 68)
+  double p1[4][2], p2[4][2], p3[4][2];
+#pragma unroll
+  for (int mf = 0; mf < 4; mf++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) p1[mf][h] = p2[mf][h] = p3[mf][h] = 0.0;
+  const double2 *ewA = F.Ew + sigma_col(g8) * LDWV + t4;
+  const double *vA = vp + g8 * (LDP - 1) + t4 + PADP;
+#pragma unroll
+  for (int ks = 0; ks < 24; ks++) {
+    if (ks == 0) {
+      cp_async_wait<WPEND>();
+      __syncwarp();
+    }
+    if (ks == 8) {
+      cp_async_wait<WPEND - 1>();
+      __syncwarp();
+    }
+    if (ks == 16) {
+      cp_async_wait<WPEND - 2>();
+      __syncwarp();
+    }
+    const int sb = ks < 8 ? F.s0 : (ks < 16 ? F.s1 : F.s2);
+    const double2 e = ewA[sb + 4 * (ks & 7)];
+    const double ed = e.x - e.y;
+#pragma unroll
+    for (int mf = 0; mf < 4; mf++) {
+      const int d = 4 * ks - 8 * mf;
+      if (d >= 0 && d <= 68) {
+        const double *a = vA + 8 * mf * (LDP - 1) + 4 * ks;
+        dmma_nv(p1[mf], a[0], e.x);
+        dmma_nv(p2[mf], a[VP_PLANE], e.y);
+        dmma_nv(p3[mf], a[2 * VP_PLANE], ed);
+      }
+    }
+  }
+  double yr[4][2], yi[4][2];
+#pragma unroll
+  for (int mf = 0; mf < 4; mf++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      yr[mf][h] = p1[mf][h] + p2[mf][h];
+      yi[mf][h] = (p1[mf][h] - p2[mf][h]) - p3[mf][h];
+    }
+  double br[8], bi[8], bs[8];
+  acc_to_b3(yr, br, lane, g8);
+  acc_to_b3(yi, bi, lane, g8);
+#pragma unroll
+  for (int k = 0; k < 8; k++) bs[k] = br[k] + bi[k];
+  // ---------------- phase B: -Y' = -T Y (T upper triangular: tiles ks >= 2mf)
+#pragma unroll
+  for (int mf = 0; mf < 4; mf++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) p1[mf][h] = p2[mf][h] = p3[mf][h] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < 8; ks++)
+#pragma unroll
+    for (int mf = 0; mf < 4; mf++)
+      if (ks >= 2 * mf) {
+        const double *a = tp + ttile(mf, ks) * 32 + lane;
+        dmma_nv(p1[mf], a[0], br[ks]);
+        dmma_nv(p2[mf], a[TP_PLANE], bi[ks]);
+        dmma_nv(p3[mf], a[2 * TP_PLANE], bs[ks]);
+      }
+#pragma unroll
+  for (int mf = 0; mf < 4; mf++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      yr[mf][h] = p2[mf][h] - p1[mf][h];
+      yi[mf][h] = (p1[mf][h] + p2[mf][h]) - p3[mf][h];
+    }
+  acc_to_b3(yr, br, lane, sigma_inv(g8));
+  acc_to_b3(yi, bi, lane, sigma_inv(g8));
+#pragma unroll
+  for (int k = 0; k < 8; k++) bs[k] = br[k] + bi[k];
+  // ---------------- phase C: E += V (-Y'), row groups r (rows 8r..8r+7): k-steps
+  // max(0, 2r-16) .. min(7, 2r+1)
+  const double *vC = vp + t4 * (LDP - 1) + g8 + PADP;
+  const bool ok0 = 2 * t4 < F.ncols, ok1 = 2 * t4 + 1 < F.ncols;
+#pragma unroll
+  for (int b = 0; b < 4; b++) {
+    double c1[3][2], c2[3][2], c3[3][2];
+#pragma unroll
+    for (int u = 0; u < 3; u++) {
+      const int r = b + 4 * u;
+      const int sb = u == 0 ? F.s0 : (u == 1 ? F.s1 : F.s2);
+      const double2 *w = F.Ew + 2 * t4 * LDWV + sb + 8 * b + g8;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const double2 x = w[h * LDWV];
+        c1[u][h] = x.x;
+        c2[u][h] = 0.0;
+        c3[u][h] = x.x + x.y;
+      }
+      (void)r;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 8; ks++)
+#pragma unroll
+      for (int u = 0; u < 3; u++) {
+        const int r = b + 4 * u;
+        if (ks >= 2 * r - 16 && ks <= 2 * r + 1) {
+          const double *a = vC + 4 * ks * (LDP - 1) + 8 * r;
+          dmma_nv(c1[u], a[0], br[ks]);
+          dmma_nv(c2[u], a[VP_PLANE], bi[ks]);
+          dmma_nv(c3[u], a[2 * VP_PLANE], bs[ks]);
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < 3; u++) {
+      const int q = 8 * (b + 4 * u) + g8;
+      if (q < W && F.rs + q < F.n) {
+        double2 *g = F.gE + q + 2 * t4 * F.lde;
+        if (ok0) g[0] = make_double2(c1[u][0] - c2[u][0], (c3[u][0] - c1[u][0]) - c2[u][0]);
+        if (ok1) g[F.lde] = make_double2(c1[u][1] - c2[u][1], (c3[u][1] - c1[u][1]) - c2[u][1]);
+      }
+    }
+  }
+}
+
+constexpr int OFF3_END = OFF3_WIN + WAVE_WARPS * 8 * LDWV;
+static_assert(OFF3_END * 16 + 32 <= 227 * 1024, "3M wave kernel shared memory");
+
+template <bool M3>
 __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArgs a, int64_t T) {
   namespace cg = cooperative_groups;
   constexpr int TH = 32 * WAVE_WARPS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   __shared__ int s_claim;   // next unclaimed item of this CTA's share of the step
   // layout: V | T | one window of 8 x LDWV per warp
-  double2 *vc = q2w_sm, *tb = q2w_sm + OFF_WAVE_T;
-  double2 *win0 = q2w_sm + OFF_WAVE_WIN;
-  for (int e = threadIdx.x; e < VC_STAGE; e += TH) vc[e] = czero();
+  double2 *vc = q2w_sm, *tb = q2w_sm + (M3 ? OFF3_T : OFF_WAVE_T);
+  double2 *win0 = q2w_sm + (M3 ? OFF3_WIN : OFF_WAVE_WIN);
+  for (int e = threadIdx.x; e < (M3 ? OFF3_T : VC_STAGE); e += TH) vc[e] = czero();
   __syncthreads();
   const int64_t Gn = a.ngroups, F = a.nfr_total;
   const Lane L(lane, LDWV);
@@ -429,6 +613,73 @@ __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArg
         const double2 *v2 = a.V2 + (a.off[j] + gi0) * NB;
         const double2 *t2 = a.T2 + (a.first[g] + j) * G * G;
         __syncthreads();   // the previous block's V / T are no longer read
+        if constexpr (M3) {
+          // V planes Vr, Vi, Vr + Vi (rows t >= nvalid keep the previous
+          // block's finite values: T's zero rows and columns cancel them)
+          double *vp = reinterpret_cast<double *>(vc), *tp = reinterpret_cast<double *>(tb);
+          constexpr int NV = (G * NB + TH - 1) / TH;
+          double2 buf[NV];
+#pragma unroll
+          for (int i = 0; i < NV; i++) {
+            const int e = threadIdx.x + i * TH;
+            buf[i] = (e < G * NB && e / NB < nvalid) ? v2[e] : czero();
+          }
+#pragma unroll
+          for (int i = 0; i < NV; i++) {
+            const int e = threadIdx.x + i * TH;
+            const int tt = e / NB, ss = e - tt * NB;
+            if (e < G * NB && tt < nvalid) {
+              double *d = vp + tt * LDP + PADP + ss;
+              d[0] = buf[i].x;
+              d[VP_PLANE] = buf[i].y;
+              d[2 * VP_PLANE] = buf[i].x + buf[i].y;
+            }
+          }
+          // T planes: upper-triangle tiles in fragment order, zeros below the diagonal
+          constexpr int NT = (G * G + TH - 1) / TH;
+#pragma unroll
+          for (int i = 0; i < NT; i++) {
+            const int e = threadIdx.x + i * TH;
+            const int kk = e / G, xx = e - kk * G;   // column, row
+            const int mf = xx >> 3, ks = kk >> 2;
+            if (e < G * G && ks >= 2 * mf) {
+              const double2 v = xx <= kk ? t2[e] : czero();
+              double *d = tp + ttile(mf, ks) * 32 + (((xx & 7) << 2) | (kk & 3));
+              d[0] = v.x;
+              d[TP_PLANE] = v.y;
+              d[2 * TP_PLANE] = v.x + v.y;
+            }
+          }
+          __syncthreads();
+          while (cur >= 0 && cur < seg_end) {
+            const int64_t f = cur % F;
+            Item3 It;
+            It.Ew = Fr.Ew;
+            It.s0 = 32 * sa;
+            It.s1 = 32 * sb;
+            It.s2 = 32 * sc;
+            It.rs = gi0 + 1 + j * NB;
+            It.n = a.n;
+            It.lde = a.lde;
+            It.gE = a.E + It.rs + f * 8 * a.lde;
+            It.ncols = (int)imin64(8, a.m - f * 8);
+            const int64_t nxt = claim();
+            full_block3<2>(It, lane, vp, tp);
+            __syncwarp();
+            if (nxt >= 0) {
+              const int64_t nf = nxt % F;
+              const int64_t nrs = item_rs(nxt), nc0 = nf * 8;
+              const int nnc = (int)imin64(8, a.m - nc0);
+              load_chunk(nrs, nc0, nnc, 0, sa);
+              cp_async_commit();
+              load_chunk(nrs, nc0, nnc, 1, sb);
+              cp_async_commit();
+              load_chunk(nrs, nc0, nnc, 2, sc);
+              cp_async_commit();
+            }
+            cur = nxt;
+          }
+        } else {
         for (int e = threadIdx.x; e < G * NB; e += TH) {
           const int tt = e / NB, ss = e - tt * NB;
           if (tt < nvalid) cp_async16(vc + vrow(tt) + PADL + ss, v2 + tt * NB + ss, true);
@@ -490,6 +741,7 @@ __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArg
           }
           cur = nxt;
         }
+        }   // M3
       }
       cp_async_wait<0>();
     }
@@ -500,7 +752,7 @@ __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArg
 
 }  // namespace
 
-size_t q2w_smem_bytes() { return (size_t)OFF_WAVE_END * sizeof(double2) + 32; }
+size_t q2w_smem_bytes(bool m3) { return (size_t)(m3 ? OFF3_END : OFF_WAVE_END) * sizeof(double2) + 32; }
 
 // Returns 1 if the shape is not handled here (caller falls back to the
 // generic grouped kernel of q2.cu, which EIG_Q2_WAVE=0 also selects).
@@ -524,17 +776,23 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
   a.nfr_total = (int)((m + 7) / 8);
   a.prof = ctx.q2_prof;
   a.nslab = 1;
-  const size_t smem = q2w_smem_bytes();
+  // 3M form by default; EIG_Q2_3M=0 selects the real embedding
+  static const bool m3 = [] {
+    const char *e = getenv("EIG_Q2_3M");
+    return e ? atoi(e) != 0 : true;
+  }();
+  const size_t smem = q2w_smem_bytes(m3);
   int64_t T = 0;   // wavefront steps
   for (int64_t g = 0; g < a.ngroups; g++) {
     const int64_t i0 = g * G;
     const int64_t J = (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
     if (J > 0) T = std::max<int64_t>(T, J - 1 + (a.ngroups - 1 - g) + 1);
   }
-  EIG_TRY(ctx.smem_attr((const void *)apply_q2wave_kernel, (int)smem, "q2wave attr"));
+  const void *kfn = m3 ? (const void *)apply_q2wave_kernel<true> : (const void *)apply_q2wave_kernel<false>;
+  EIG_TRY(ctx.smem_attr(kfn, (int)smem, "q2wave attr"));
   void *args[] = {&a, &T};
-  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)apply_q2wave_kernel, dim3(ctx.num_sms), dim3(32 * WAVE_WARPS),
-                                                args, smem, ctx.stream), "q2wave launch"));
+  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel(kfn, dim3(ctx.num_sms), dim3(32 * WAVE_WARPS), args, smem, ctx.stream),
+                    "q2wave launch"));
   return ctx.launched("apply_q2wave_kernel");
 }
 

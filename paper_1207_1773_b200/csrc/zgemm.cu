@@ -470,7 +470,11 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
     const char *e = getenv("EIG_ZGEMM_SHORTK");
     return e ? (int64_t)atoll(e) : (int64_t)kShortK;
   }();
-  const int v = !m3 ? 0 : (g.K <= shortk ? 2 : 1);
+  static const int64_t narrow = [] {
+    const char *e = getenv("EIG_ZGEMM_NARROW");
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  const int v = !m3 ? 0 : (g.K <= shortk || g.N <= narrow ? 2 : 1);
   const int BN = v == 2 ? Lay<2>::BN : Lay<0>::BN;
   const int64_t q = BM / BN;
   const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);

@@ -249,10 +249,13 @@ def test_hotpath_parity(n, nb, g, m, m3):
 
 
 @gpu
-def test_apply_q2_generic_kernel_subprocess():
+@pytest.mark.parametrize("env", [("EIG_Q2_WAVE", "0"), ("EIG_Q2_3M", "0")])
+def test_apply_q2_generic_kernel_subprocess(env):
     """EIG_Q2_WAVE=0 routes nb = 64, g = 32 to the generic grouped kernel
-    (apply_q2_kernel, q2.cu) instead of the wavefront; the switch is read once
-    per process, so the check runs in a child process (same oracle comparison)."""
+    (apply_q2_kernel, q2.cu) instead of the wavefront; EIG_Q2_3M=0 runs the
+    wavefront in the real-embedding form instead of the 3M form.  The
+    switches are read once per process, so the check runs in a child process
+    (same oracle comparison)."""
     import os
     import subprocess
     import sys
@@ -274,7 +277,7 @@ for n, m in [(517, 130), (300, 5000), (129, 1333)]:
     assert err < 1e-11, (n, m, err)
 print("ok")
 """ % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, EIG_Q2_WAVE="0")
+    env = dict(os.environ, **{env[0]: env[1]})
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
