@@ -411,10 +411,8 @@ struct Item3 {
   int ncols;
 };
 
-// phase-C row groups (8 rows) per batch: k-step counts 2,4,6,8,8,8,8,8,8,6,4,2
-// balanced as (r, r+4, r+8) = 18 k-steps each
-template <int WPEND>
-__device__ __forceinline__ void full_block3(const Item3 &F, int lane, const double *vp, const double *tp) {
+template <int WPEND, class Pre>
+__device__ __forceinline__ void full_block3(const Item3 &F, int lane, const double *vp, const double *tp, Pre &&pre) {
   const int g8 = lane >> 2, t4 = lane & 3;
   // ---------------- phase A: Y = V^H E (tile (mf, ks) nonzero for 0 <= 4ks - 8mf <= 68)
   double p1[4][2], p2[4][2], p3[4][2];
@@ -492,17 +490,23 @@ __device__ __forceinline__ void full_block3(const Item3 &F, int lane, const doub
 #pragma unroll
   for (int k = 0; k < 8; k++) bs[k] = br[k] + bi[k];
   // ---------------- phase C: E += V (-Y'), row groups r (rows 8r..8r+7): k-steps
-  // max(0, 2r-16) .. min(7, 2r+1)
+  // max(0, 2r-16) .. min(7, 2r+1).  Row groups go chunk by chunk, two per
+  // batch ((0,3), (1,2) | (4,5), (6,7) | (8,11), (9,10): 10 / 16 / 10 k-steps);
+  // once a chunk's rows are in registers, pre(c) refills its slot with the
+  // next item's chunk, so those loads overlap the rest of phase C.
   const double *vC = vp + t4 * (LDP - 1) + g8 + PADP;
   const bool ok0 = 2 * t4 < F.ncols, ok1 = 2 * t4 + 1 < F.ncols;
 #pragma unroll
-  for (int b = 0; b < 4; b++) {
-    double c1[3][2], c2[3][2], c3[3][2];
+  for (int b = 0; b < 6; b++) {
+    const int c = b >> 1;
+    const int ra = c == 1 ? 4 + 2 * (b & 1) : 4 * c + (b & 1);
+    const int rb = c == 1 ? ra + 1 : 4 * c + 3 - (b & 1);
+    const int sb = c == 0 ? F.s0 : (c == 1 ? F.s1 : F.s2);
+    double c1[2][2], c2[2][2], c3[2][2];
 #pragma unroll
-    for (int u = 0; u < 3; u++) {
-      const int r = b + 4 * u;
-      const int sb = u == 0 ? F.s0 : (u == 1 ? F.s1 : F.s2);
-      const double2 *w = F.Ew + 2 * t4 * LDWV + sb + 8 * b + g8;
+    for (int u = 0; u < 2; u++) {
+      const int r = u ? rb : ra;
+      const double2 *w = F.Ew + 2 * t4 * LDWV + sb + 8 * (r & 3) + g8;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const double2 x = w[h * LDWV];
@@ -510,13 +514,16 @@ __device__ __forceinline__ void full_block3(const Item3 &F, int lane, const doub
         c2[u][h] = 0.0;
         c3[u][h] = x.x + x.y;
       }
-      (void)r;
+    }
+    if (b & 1) {
+      __syncwarp();   // every lane has read chunk c
+      pre(c);
     }
 #pragma unroll
     for (int ks = 0; ks < 8; ks++)
 #pragma unroll
-      for (int u = 0; u < 3; u++) {
-        const int r = b + 4 * u;
+      for (int u = 0; u < 2; u++) {
+        const int r = u ? rb : ra;
         if (ks >= 2 * r - 16 && ks <= 2 * r + 1) {
           const double *a = vC + 4 * ks * (LDP - 1) + 8 * r;
           dmma_nv(c1[u], a[0], br[ks]);
@@ -525,8 +532,8 @@ __device__ __forceinline__ void full_block3(const Item3 &F, int lane, const doub
         }
       }
 #pragma unroll
-    for (int u = 0; u < 3; u++) {
-      const int q = 8 * (b + 4 * u) + g8;
+    for (int u = 0; u < 2; u++) {
+      const int q = 8 * (u ? rb : ra) + g8;
       if (q < W && F.rs + q < F.n) {
         double2 *g = F.gE + q + 2 * t4 * F.lde;
         if (ok0) g[0] = make_double2(c1[u][0] - c2[u][0], (c3[u][0] - c1[u][0]) - c2[u][0]);
@@ -664,19 +671,18 @@ __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArg
             It.gE = a.E + It.rs + f * 8 * a.lde;
             It.ncols = (int)imin64(8, a.m - f * 8);
             const int64_t nxt = claim();
-            full_block3<2>(It, lane, vp, tp);
-            __syncwarp();
+            int64_t nrs = 0, nc0 = 0;
+            int nnc = 0;
             if (nxt >= 0) {
-              const int64_t nf = nxt % F;
-              const int64_t nrs = item_rs(nxt), nc0 = nf * 8;
-              const int nnc = (int)imin64(8, a.m - nc0);
-              load_chunk(nrs, nc0, nnc, 0, sa);
-              cp_async_commit();
-              load_chunk(nrs, nc0, nnc, 1, sb);
-              cp_async_commit();
-              load_chunk(nrs, nc0, nnc, 2, sc);
-              cp_async_commit();
+              nrs = item_rs(nxt);
+              nc0 = (nxt % F) * 8;
+              nnc = (int)imin64(8, a.m - nc0);
             }
+            // the next item's chunk c goes into slot c as soon as phase C has read it
+            full_block3<2>(It, lane, vp, tp, [&](int c) {
+              if (nxt >= 0) load_chunk(nrs, nc0, nnc, c, c == 0 ? sa : (c == 1 ? sb : sc));
+              cp_async_commit();
+            });
             cur = nxt;
           }
         } else {
