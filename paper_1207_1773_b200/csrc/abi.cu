@@ -359,6 +359,7 @@ static int trsm_rlh_lower(Ctx &c, int64_t n, const double2 *L, int64_t ldl, doub
       g = Zgemm();
       g.opb = OP_C; g.M = n - j0; g.N = bj; g.K = bj; g.A = X + j0 + j0 * ldx; g.lda = ldx;
       g.B = Linv + (j0 / bs) * bs * bs; g.ldb = bs; g.C = X + j0 + j0 * ldx; g.ldc = ldx; g.splitk = 1;
+      g.whole_n = true;
       EIG_TRY(zgemm(c, g));
     }
   }

@@ -143,7 +143,7 @@ int potrf_lower(Ctx &c, int64_t n, double2 *B, int64_t ldb, int64_t *d_info) {
     if (s <= 0) return 0;
     Zgemm g;   // in place: one 64-col N tile, no split-K
     g.opb = OP_C; g.M = s; g.N = b; g.K = b; g.A = A11 + b; g.lda = ldb; g.B = Linv; g.ldb = FB; g.C = A11 + b;
-    g.ldc = ldb; g.splitk = 1;
+    g.ldc = ldb; g.splitk = 1; g.whole_n = true;
     const cudaStream_t keep = c.stream;
     c.stream = st;
     const int rc = zgemm(c, g);

@@ -31,6 +31,9 @@ struct Zgemm {
   int64_t split_n = 0;
   // 3M (Gauss) product: 0 = the handle's setting (EIG_USE_3M), 1 = on, -1 = off
   int m3 = 0;
+  // in-place right products (C aliases A): every CTA must cover all N <= 64
+  // columns, so the 64-column engine variants are required
+  bool whole_n = false;
 };
 
 // N used by the back-transform GEMMs for their split-K choice (columns of E

@@ -474,7 +474,8 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
     const char *e = getenv("EIG_ZGEMM_NARROW");
     return e ? (int64_t)atoll(e) : (int64_t)0;
   }();
-  const int v = !m3 ? 0 : (g.K <= shortk || g.N <= narrow ? 2 : 1);
+  if (g.whole_n && g.N > Lay<0>::BN) return -2;
+  const int v = !m3 ? 0 : ((g.K <= shortk || g.N <= narrow) && !g.whole_n ? 2 : 1);
   const int BN = v == 2 ? Lay<2>::BN : Lay<0>::BN;
   const int64_t q = BM / BN;
   const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
