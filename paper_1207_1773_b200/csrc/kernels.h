@@ -42,6 +42,9 @@ constexpr int64_t kBtSplitN = 1024;
 // 3M products with K <= kShortK take the short-K engine
 // variant (64 x 32 tiles, two CTAs per SM); see zgemm.cu
 constexpr int64_t kShortK = 256;
+// ... and so do products with N <= kNarrowN (the he2hb hemm W = A22 V, N = nb):
+// twice the tiles of the 64-column variant (EIG_ZGEMM_NARROW overrides)
+constexpr int64_t kNarrowN = 64;
 
 // Enqueue C = alpha op(A) op(B) + beta C on ctx's stream.  Returns 0 or error.
 int zgemm(Ctx &ctx, const Zgemm &g);

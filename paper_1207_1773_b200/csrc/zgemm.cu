@@ -472,7 +472,7 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   }();
   static const int64_t narrow = [] {
     const char *e = getenv("EIG_ZGEMM_NARROW");
-    return e ? (int64_t)atoll(e) : (int64_t)0;
+    return e ? (int64_t)atoll(e) : (int64_t)kNarrowN;
   }();
   if (g.whole_n && g.N > Lay<0>::BN) return -2;
   const int v = !m3 ? 0 : ((g.K <= shortk || g.N <= narrow) && !g.whole_n ? 2 : 1);
