@@ -28,6 +28,7 @@ enum WsId {
   WS_T2,          // Q2 T factors
   WS_Q2PLAN,      // Q2 plan tables
   WS_Q2PROF,      // debug counters
+  WS_Q2DONE,      // Q2 3M wavefront: per-block completion counters
   WS_BAND,        // hb2st band buffer (2nb+2 diagonals)
   WS_HBPROG,      // hb2st sweep progress flags
   WS_HBOFF,       // hb2st V2 slot offsets

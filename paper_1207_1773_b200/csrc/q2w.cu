@@ -546,16 +546,15 @@ __device__ __forceinline__ void full_block3(const Item3 &F, int lane, const doub
 constexpr int OFF3_END = OFF3_WIN + WAVE_WARPS * 8 * LDWV;
 static_assert(OFF3_END * 16 + 32 <= 227 * 1024, "3M wave kernel shared memory");
 
-template <bool M3>
 __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArgs a, int64_t T) {
   namespace cg = cooperative_groups;
   constexpr int TH = 32 * WAVE_WARPS;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   __shared__ int s_claim;   // next unclaimed item of this CTA's share of the step
   // layout: V | T | one window of 8 x LDWV per warp
-  double2 *vc = q2w_sm, *tb = q2w_sm + (M3 ? OFF3_T : OFF_WAVE_T);
-  double2 *win0 = q2w_sm + (M3 ? OFF3_WIN : OFF_WAVE_WIN);
-  for (int e = threadIdx.x; e < (M3 ? OFF3_T : VC_STAGE); e += TH) vc[e] = czero();
+  double2 *vc = q2w_sm, *tb = q2w_sm + OFF_WAVE_T;
+  double2 *win0 = q2w_sm + OFF_WAVE_WIN;
+  for (int e = threadIdx.x; e < VC_STAGE; e += TH) vc[e] = czero();
   __syncthreads();
   const int64_t Gn = a.ngroups, F = a.nfr_total;
   const Lane L(lane, LDWV);
@@ -620,72 +619,6 @@ __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArg
         const double2 *v2 = a.V2 + (a.off[j] + gi0) * NB;
         const double2 *t2 = a.T2 + (a.first[g] + j) * G * G;
         __syncthreads();   // the previous block's V / T are no longer read
-        if constexpr (M3) {
-          // V planes Vr, Vi, Vr + Vi (rows t >= nvalid keep the previous
-          // block's finite values: T's zero rows and columns cancel them)
-          double *vp = reinterpret_cast<double *>(vc), *tp = reinterpret_cast<double *>(tb);
-          constexpr int NV = (G * NB + TH - 1) / TH;
-          double2 buf[NV];
-#pragma unroll
-          for (int i = 0; i < NV; i++) {
-            const int e = threadIdx.x + i * TH;
-            buf[i] = (e < G * NB && e / NB < nvalid) ? v2[e] : czero();
-          }
-#pragma unroll
-          for (int i = 0; i < NV; i++) {
-            const int e = threadIdx.x + i * TH;
-            const int tt = e / NB, ss = e - tt * NB;
-            if (e < G * NB && tt < nvalid) {
-              double *d = vp + tt * LDP + PADP + ss;
-              d[0] = buf[i].x;
-              d[VP_PLANE] = buf[i].y;
-              d[2 * VP_PLANE] = buf[i].x + buf[i].y;
-            }
-          }
-          // T planes: upper-triangle tiles in fragment order, zeros below the diagonal
-          constexpr int NT = (G * G + TH - 1) / TH;
-#pragma unroll
-          for (int i = 0; i < NT; i++) {
-            const int e = threadIdx.x + i * TH;
-            const int kk = e / G, xx = e - kk * G;   // column, row
-            const int mf = xx >> 3, ks = kk >> 2;
-            if (e < G * G && ks >= 2 * mf) {
-              const double2 v = xx <= kk ? t2[e] : czero();
-              double *d = tp + ttile(mf, ks) * 32 + (((xx & 7) << 2) | (kk & 3));
-              d[0] = v.x;
-              d[TP_PLANE] = v.y;
-              d[2 * TP_PLANE] = v.x + v.y;
-            }
-          }
-          __syncthreads();
-          while (cur >= 0 && cur < seg_end) {
-            const int64_t f = cur % F;
-            Item3 It;
-            It.Ew = Fr.Ew;
-            It.s0 = 32 * sa;
-            It.s1 = 32 * sb;
-            It.s2 = 32 * sc;
-            It.rs = gi0 + 1 + j * NB;
-            It.n = a.n;
-            It.lde = a.lde;
-            It.gE = a.E + It.rs + f * 8 * a.lde;
-            It.ncols = (int)imin64(8, a.m - f * 8);
-            const int64_t nxt = claim();
-            int64_t nrs = 0, nc0 = 0;
-            int nnc = 0;
-            if (nxt >= 0) {
-              nrs = item_rs(nxt);
-              nc0 = (nxt % F) * 8;
-              nnc = (int)imin64(8, a.m - nc0);
-            }
-            // the next item's chunk c goes into slot c as soon as phase C has read it
-            full_block3<2>(It, lane, vp, tp, [&](int c) {
-              if (nxt >= 0) load_chunk(nrs, nc0, nnc, c, c == 0 ? sa : (c == 1 ? sb : sc));
-              cp_async_commit();
-            });
-            cur = nxt;
-          }
-        } else {
         for (int e = threadIdx.x; e < G * NB; e += TH) {
           const int tt = e / NB, ss = e - tt * NB;
           if (tt < nvalid) cp_async16(vc + vrow(tt) + PADL + ss, v2 + tt * NB + ss, true);
@@ -747,12 +680,169 @@ __global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave_kernel(Q2wArg
           }
           cur = nxt;
         }
-        }   // M3
       }
       cp_async_wait<0>();
     }
     __threadfence();
     grid.sync();
+  }
+}
+
+// ---------------------------------------------------------------- 3M wavefront, dataflow
+// Same steps and item split as apply_q2wave_kernel, but without a grid
+// barrier between steps: a CTA's share of block (g, j) starts as soon as the
+// blocks it overlaps from earlier steps are complete — (g, j-1), (g+1, j-1)
+// and (g+1, j) (every other overlapping earlier block precedes one of these,
+// tests/test_q2_schedule.py) — counted per block in done[] (fragments
+// finished, released after a CTA barrier, acquired by thread 0).  A CTA that
+// finishes a step early runs on into the next instead of waiting for the
+// slowest CTA of the step.
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(32 * WAVE_WARPS, 1) apply_q2wave3_kernel(Q2wArgs a, int64_t T, int *done) {
+  constexpr int TH = 32 * WAVE_WARPS;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ int s_claim;
+  double2 *vc = q2w_sm, *tb = q2w_sm + OFF3_T;
+  double2 *win0 = q2w_sm + OFF3_WIN;
+  double *vp = reinterpret_cast<double *>(vc), *tp = reinterpret_cast<double *>(tb);
+  for (int e = threadIdx.x; e < OFF3_T; e += TH) vc[e] = czero();
+  const int64_t Gn = a.ngroups, F = a.nfr_total;
+  const double2 *Ew = win0 + w * 8 * LDWV;
+  double2 *Eww = win0 + w * 8 * LDWV;
+  auto load_chunk = [&](int64_t rs, int64_t c0, int ncols, int c) {
+    for (int e = lane; e < 32 * 8; e += 32) {
+      const int q = e & 31, col = e >> 5;
+      const int row_in = 32 * c + q;
+      const int64_t row = rs + row_in;
+      const bool ok = row_in < W && row < a.n && col < ncols;
+      cp_async16m(&Eww[col * LDWV + 32 * c + q], ok ? a.E + row + (c0 + col) * a.lde : a.E, ok);
+    }
+  };
+  auto J_of = [&](int64_t g) { return wave_J(a, g); };
+  int64_t prev_b = -1;
+  int prev_cnt = 0;
+  for (int64_t t = 0; t < T; t++) {
+    const int64_t dhi = imin64(Gn - 1, t);
+    int64_t dlo = 0;
+    while (dlo <= dhi && t - dlo >= J_of(Gn - 1 - dlo)) dlo++;
+    const int64_t nblk = dhi - dlo + 1;
+    if (nblk <= 0) continue;
+    const int64_t items = nblk * F;
+    const int64_t i0c = items * blockIdx.x / gridDim.x, i1c = items * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t seg0 = i0c; seg0 < i1c;) {
+      const int64_t seg_end = imin64(i1c, (seg0 / F + 1) * F);
+      const int64_t d = dlo + seg0 / F, g = Gn - 1 - d, j = t - d, gi0 = g * G;
+      const int nvalid = (int)imax64(0, imin64(G, a.n - 2 - j * NB - gi0 + 1));
+      const double2 *v2 = a.V2 + (a.off[j] + gi0) * NB;
+      const double2 *t2 = a.T2 + (a.first[g] + j) * G * G;
+      __syncthreads();   // every warp is done with the previous segment (its items and V / T)
+      if (threadIdx.x == 0) {
+        if (prev_b >= 0) {
+          __threadfence();
+          atomicAdd(done + prev_b, prev_cnt);
+        }
+        // RAW / WAR on E: the overlapping blocks of earlier steps
+        if (j >= 1) while (ld_acquire_gpu(done + a.first[g] + j - 1) < F) {}
+        if (g + 1 < Gn) {
+          const int64_t J1 = J_of(g + 1);
+          if (j >= 1 && j - 1 < J1) while (ld_acquire_gpu(done + a.first[g + 1] + j - 1) < F) {}
+          if (j < J1) while (ld_acquire_gpu(done + a.first[g + 1] + j) < F) {}
+        }
+        s_claim = 0;
+      }
+      // ---- stage the V planes (Vr, Vi, Vr + Vi) and T planes of block (g, j)
+      // (V2 / T2 are inputs: no dependency; rows t >= nvalid keep the previous
+      // block's finite values, which T's zero rows and columns cancel)
+      {
+        constexpr int NV = (G * NB + TH - 1) / TH;
+        double2 buf[NV];
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+          const int e = threadIdx.x + i * TH;
+          buf[i] = (e < G * NB && e / NB < nvalid) ? v2[e] : czero();
+        }
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+          const int e = threadIdx.x + i * TH;
+          const int tt = e / NB, ss = e - tt * NB;
+          if (e < G * NB && tt < nvalid) {
+            double *dd = vp + tt * LDP + PADP + ss;
+            dd[0] = buf[i].x;
+            dd[VP_PLANE] = buf[i].y;
+            dd[2 * VP_PLANE] = buf[i].x + buf[i].y;
+          }
+        }
+        constexpr int NT = (G * G + TH - 1) / TH;
+#pragma unroll
+        for (int i = 0; i < NT; i++) {
+          const int e = threadIdx.x + i * TH;
+          const int kk = e / G, xx = e - kk * G;   // column, row
+          const int mf = xx >> 3, ks = kk >> 2;
+          if (e < G * G && ks >= 2 * mf) {
+            const double2 v = xx <= kk ? t2[e] : czero();
+            double *dd = tp + ttile(mf, ks) * 32 + (((xx & 7) << 2) | (kk & 3));
+            dd[0] = v.x;
+            dd[TP_PLANE] = v.y;
+            dd[2 * TP_PLANE] = v.x + v.y;
+          }
+        }
+      }
+      __syncthreads();   // V / T staged, dependencies acquired (thread 0), s_claim reset
+      auto claim = [&]() -> int64_t {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(&s_claim, 1);
+        v = __shfl_sync(0xffffffffu, v, 0);
+        return seg0 + v < seg_end ? seg0 + v : -1;
+      };
+      const int64_t rs = gi0 + 1 + j * NB;
+      int64_t cur = claim();
+      if (cur >= 0) {
+        const int64_t c0 = (cur % F) * 8;
+        const int nc = (int)imin64(8, a.m - c0);
+        load_chunk(rs, c0, nc, 0);
+        cp_async_commit();
+        load_chunk(rs, c0, nc, 1);
+        cp_async_commit();
+        load_chunk(rs, c0, nc, 2);
+        cp_async_commit();
+      }
+      while (cur >= 0) {
+        const int64_t f = cur % F;
+        Item3 It;
+        It.Ew = Ew;
+        It.s0 = 0;
+        It.s1 = 32;
+        It.s2 = 64;
+        It.rs = rs;
+        It.n = a.n;
+        It.lde = a.lde;
+        It.gE = a.E + rs + f * 8 * a.lde;
+        It.ncols = (int)imin64(8, a.m - f * 8);
+        const int64_t nxt = claim();
+        const int64_t nc0 = nxt >= 0 ? (nxt % F) * 8 : 0;
+        const int nnc = nxt >= 0 ? (int)imin64(8, a.m - nc0) : 0;
+        // the next item (same block) reuses the slots chunk by chunk
+        full_block3<2>(It, lane, vp, tp, [&](int c) {
+          if (nxt >= 0) load_chunk(rs, nc0, nnc, c);
+          cp_async_commit();
+        });
+        cur = nxt;
+      }
+      cp_async_wait<0>();
+      prev_b = a.first[g] + j;
+      prev_cnt = (int)(seg_end - seg0);
+      seg0 = seg_end;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && prev_b >= 0) {
+    __threadfence();
+    atomicAdd(done + prev_b, prev_cnt);
   }
 }
 
@@ -794,8 +884,24 @@ int q2w_apply(Ctx &ctx, const Q2Plan &p, const double2 *V2, const double2 *T2, d
     const int64_t J = (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
     if (J > 0) T = std::max<int64_t>(T, J - 1 + (a.ngroups - 1 - g) + 1);
   }
-  const void *kfn = m3 ? (const void *)apply_q2wave_kernel<true> : (const void *)apply_q2wave_kernel<false>;
+  const void *kfn = m3 ? (const void *)apply_q2wave3_kernel : (const void *)apply_q2wave_kernel;
   EIG_TRY(ctx.smem_attr(kfn, (int)smem, "q2wave attr"));
+  if (m3) {
+    // per-block completion counters (fragments done) of the dataflow schedule
+    int64_t nblocks = 0;
+    for (int64_t g = 0; g < a.ngroups; g++) {
+      const int64_t i0 = g * G;
+      nblocks += (i0 > a.n - 2) ? 0 : (a.n - 2 - i0) / NB + 1;
+    }
+    int *done = (int *)ctx.ws(WS_Q2DONE, (size_t)std::max<int64_t>(1, nblocks) * sizeof(int));
+    if (!done) return EIG_ERR_NOMEM;
+    EIG_TRY(ctx.check(cudaMemsetAsync(done, 0, (size_t)std::max<int64_t>(1, nblocks) * sizeof(int), ctx.stream),
+                      "q2wave done reset"));
+    void *args3[] = {&a, &T, &done};
+    EIG_TRY(ctx.check(cudaLaunchCooperativeKernel(kfn, dim3(ctx.num_sms), dim3(32 * WAVE_WARPS), args3, smem,
+                                                  ctx.stream), "q2wave3 launch"));
+    return ctx.launched("apply_q2wave3_kernel");
+  }
   void *args[] = {&a, &T};
   EIG_TRY(ctx.check(cudaLaunchCooperativeKernel(kfn, dim3(ctx.num_sms), dim3(32 * WAVE_WARPS), args, smem, ctx.stream),
                     "q2wave launch"));

@@ -75,3 +75,41 @@ def test_wavefront_parallelism_n10000():
     nblocks = sum(len(s) for s in sched)
     assert nblocks == sum(steps(10000, g) for g in range(groups(10000)))
     assert len(sched) < 500 and max(len(s) for s in sched) > 100
+
+
+def dataflow_deps(n, g, j):
+    """Blocks apply_q2wave3_kernel waits for before block (g, j): (g, j-1),
+    (g+1, j-1), (g+1, j), those that exist."""
+    Gn = groups(n)
+    out = []
+    for gg, jj in ((g, j - 1), (g + 1, j - 1), (g + 1, j)):
+        if 0 <= gg < Gn and 0 <= jj < steps(n, gg):
+            out.append((gg, jj))
+    return out
+
+
+@pytest.mark.parametrize("n", [2, 3, 65, 66, 100, 257, 517, 1000, 2049])
+def test_dataflow_waits_cover_every_overlapping_predecessor(n):
+    """The 3M kernel replaces the grid barrier between steps by per-block
+    completion counters and waits only for dataflow_deps: every block that
+    precedes b in R7's order and overlaps it must be reachable from b through
+    those waits (then it is complete when b starts), and every wait must point
+    to an earlier step (no cycles)."""
+    sched = schedule(n)
+    when = {b: t for t, blocks in enumerate(sched) for b in blocks}
+    Gn = groups(n)
+    seq = [(g, j) for g in range(Gn - 1, -1, -1) for j in range(steps(n, g))]
+    pos = {b: k for k, b in enumerate(seq)}
+    reach = {}
+    for b in sorted(seq, key=lambda x: when[x]):     # deps are at earlier steps: closure in step order
+        r = set()
+        for d in dataflow_deps(n, *b):
+            assert when[d] < when[b], (d, b)
+            r.add(d)
+            r |= reach[d]
+        reach[b] = r
+    for b in seq:
+        rb = rows(n, *b)
+        for a in seq[:pos[b]]:
+            if rows(n, *a) & rb:
+                assert a in reach[b], (a, b)
