@@ -32,6 +32,8 @@ enum WsId {
   WS_BAND,        // hb2st band buffer (2nb+2 diagonals)
   WS_HBPROG,      // hb2st sweep progress flags
   WS_HBOFF,       // hb2st V2 slot offsets
+  WS_HBMSG,       // hb2st position-stationary kernel: reflector / row messages
+  WS_HBFLAG,      // ... and their flags
   WS_DC,          // stedc buffers
   WS_DC_SMALL,    // stedc per-level node tables
   WS_FRONT,       // potrf diagonal-block inverse

@@ -18,6 +18,9 @@
 // global memory (release/acquire), the band (2nb+1 diagonals, lower) lives in
 // L2 and is accessed with L1-bypassing loads.
 #include <algorithm>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -289,6 +292,311 @@ __global__ void __launch_bounds__(HT, 1) hb2st_kernel(HbArgs a) {
     for (int k = 0; k < 6; k++) atomicAdd(&a.prof[16 + k], (unsigned long long)tacc[k]);
 }
 
+// ---------------------------------------------------------------- systolic chase
+// Position-stationary form of the same chase (same tasks, same reflectors,
+// DESIGN.md §7): position j owns, for every sweep i, the windows of task
+// (i, j) in shared memory —
+//   D_j = M[R_ij, R_ij] (lower, packed)   and   B_j = M[R_ij, R_i,j-1]
+// (R_ij = [i+1+j nb, i+(j+1) nb]; B_j's column 0 is task (i, j)'s target
+// column, columns 1.. its previous bulge; position 0 keeps only the target
+// column M[R_i0, i], in B's last column).  Task (i, j) at position j:
+//   (c) of task (i, j-1):  B_j <- B_j H_{i,j-1}   (v, tau from position j-1)
+//   reflector of B_j's target column             (published to position j+1)
+//   (a) B_j[:, 1:] <- H^H B_j[:, 1:],  (b) D_j <- H^H D_j H.
+// From sweep i to i+1 both windows slide one row and one column down the
+// band: the updates of (a) and (b) are written one row and column up-left,
+// D_j's first column becomes B_j's last column, and the entering last row
+// comes from position j+1 (its B row 0 and D(0,0) after sweep i; the rest of
+// B's new row is zero: those entries left a target column below its beta).
+// Position j runs sweep i at tick 2i + j; the CTA of positions 2k, 2k+1
+// alternates between them, so only a reflector (65 values) and a row (65
+// values) cross between CTAs per task, with release/acquire flags.
+constexpr int LB = 65;                  // B column stride (complex)
+constexpr int DPK = 64 * 65 / 2;        // packed lower D
+__device__ __forceinline__ int dix(int r, int c) { return r * (r + 1) / 2 + c; }   // r >= c
+
+struct SysArgs {
+  int64_t n;
+  int nb, ldab, J;
+  double2 *AB;
+  double2 *V2, *tau2;
+  const int64_t *off;
+  double2 *vmsg;   // [J][2][nb + 1]: v, tau of task (i, j)   (by sweep parity)
+  double2 *rmsg;   // [J][2][nb + 1]: B_j row 0, D_j(0, 0) after task (i, j)
+  int *vflag, *rflag;   // [J]: sweeps published
+  unsigned long long *prof;   // optional: CTA 0 cycles [16..21] (row wait, v wait + (c), reflector, (a), (b), end)
+};
+
+__device__ __forceinline__ double2 ldcg2(const double2 *p) { return __ldcg(p); }
+
+__global__ void __launch_bounds__(HT, 1) hb2sys_kernel(SysArgs a) {
+  namespace cg = cooperative_groups;
+  extern __shared__ __align__(16) double2 ysm[];
+  __shared__ double2 sv[64], svin[64], sp[64], sg[64], sf[64];
+  __shared__ double2 spart[8][64], spart2[8][64];
+  __shared__ double2 s_tau2[1], s_beta2[1], s_tauin;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = a.n;
+  const int nb = a.nb, ldab = a.ldab;
+  double2 *AB = a.AB;
+  auto Mget = [&](int64_t r, int64_t c) -> double2 {
+    return (c >= 0 && c < n && r < n && r >= c && r - c < ldab) ? AB[(r - c) + c * (int64_t)ldab] : czero();
+  };
+  const int k = blockIdx.x;
+  const bool prof = a.prof != nullptr && k == 0 && tid == 0;
+  long long tm = 0, tacc[6] = {0, 0, 0, 0, 0, 0};
+  auto mark = [&](int kk) {
+    if (prof) {
+      const long long now = clock64();
+      if (kk >= 0) tacc[kk] += now - tm;
+      tm = now;
+    }
+  };
+  auto Dq = [&](int q) { return ysm + q * DPK; };
+  auto Bq = [&](int q) { return ysm + 2 * DPK + q * 64 * LB; };
+  for (int q = 0; q < 2; q++) {   // windows of sweep 0
+    const int j = 2 * k + q;
+    if (j >= a.J) break;
+    const int64_t r0 = 1 + (int64_t)j * nb;
+    for (int e = tid; e < nb * nb; e += HT) {
+      const int r = e % nb, c = e / nb;
+      if (r >= c) Dq(q)[dix(r, c)] = Mget(r0 + r, r0 + c);
+      double2 v = czero();
+      if (j >= 1) v = Mget(r0 + r, r0 - nb + c);
+      else if (c == nb - 1) v = Mget(r0 + r, 0);
+      Bq(q)[c * LB + r] = v;
+    }
+  }
+  cg::this_grid().sync();   // every window is loaded before the first output lands in AB
+
+  // zlarfg (reading R1) of x = (x0 at lane, x1 at lane + 32), length len, by one warp
+  auto reflector = [&](double2 x0, double2 x1, double alx, double aly, int len) {
+    const double2 al = make_double2(alx, aly);
+    double nrm = (lane >= 1 ? x0.x * x0.x + x0.y * x0.y : 0.0) + x1.x * x1.x + x1.y * x1.y;
+    nrm = warp_sum(nrm);
+    double2 tau, scale;
+    double beta;
+    if (nrm == 0.0 && al.y == 0.0) {
+      tau = czero();
+      beta = al.x;
+      scale = czero();
+    } else {
+      beta = -copysign(sqrt(al.x * al.x + al.y * al.y + nrm), al.x);
+      const double ib = 1.0 / beta;
+      tau = make_double2((beta - al.x) * ib, -al.y * ib);
+      const double2 d = make_double2(al.x - beta, al.y);
+      const double idd = 1.0 / (d.x * d.x + d.y * d.y);
+      scale = make_double2(d.x * idd, -d.y * idd);
+    }
+    sv[lane] = (lane == 0) ? make_double2(1.0, 0.0) : (lane < len ? cmul(x0, scale) : czero());
+    sv[lane + 32] = (lane + 32 < len) ? cmul(x1, scale) : czero();
+    if (lane == 0) {
+      s_tau2[0] = tau;
+      s_beta2[0] = make_double2(beta, 0.0);
+    }
+  };
+
+  const int G8 = (nb + 7) / 8;   // terms per group in the 8-group matvecs
+  for (int64_t i = 0; i + 1 < n; i++) {
+    if (i + 1 + (int64_t)(2 * k) * nb > n - 1) break;   // both positions are past the matrix
+    for (int q = 0; q < 2; q++) {
+      const int j = 2 * k + q;
+      if (j >= a.J) break;
+      const int64_t r0 = i + 1 + (int64_t)j * nb;
+      if (r0 > n - 1) break;   // position j (and every later one) is past the matrix
+      const int len = (int)imin64(nb, n - r0);
+      double2 *D = Dq(q), *B = Bq(q);
+      const int par = (int)(i & 1);
+      mark(-1);
+      // ---- waits: position j+1's row of sweep i-1 (other CTA when q = 1) and
+      // position j-1's reflector of sweep i (other CTA when q = 0)
+      const bool act1 = i > 0 && i + (int64_t)(j + 1) * nb <= n - 1;   // position j+1 ran sweep i-1
+      if (tid == 0) {
+        if (act1 && q == 1)
+          while (ld_acquire_i32(a.rflag + j + 1) < i) {
+          }
+        if (j >= 1 && q == 0)
+          while (ld_acquire_i32(a.vflag + j - 1) < i + 1) {
+          }
+      }
+      __syncthreads();
+      mark(0);
+      // entering row of the windows (sweep i-1 -> i) and the incoming reflector
+      if (i > 0 && tid < nb) {
+        const double2 *m = a.rmsg + ((int64_t)(j + 1) * 2 + ((i - 1) & 1)) * (nb + 1);
+        D[dix(nb - 1, tid)] = act1 ? ldcg2(m + (tid < nb - 1 ? tid + 1 : nb)) : czero();
+        B[tid * LB + nb - 1] = (tid < nb - 1 || !act1) ? czero() : ldcg2(m);
+      }
+      if (j >= 1 && tid >= 64 && tid <= 64 + nb) {
+        const double2 x = ldcg2(a.vmsg + ((int64_t)(j - 1) * 2 + par) * (nb + 1) + (tid - 64));
+        if (tid - 64 < nb) svin[tid - 64] = x;
+        else s_tauin = x;
+      }
+      __syncthreads();
+      // ---- (c) of task (i, j-1): g = tau_in B v_in
+      const double2 tin = j >= 1 ? s_tauin : czero();
+      const bool updc = tin.x != 0.0 || tin.y != 0.0;
+      if (updc) {
+        {
+          const int g = tid >> 6, r = tid & 63;
+          double2 acc = czero();
+          if (r < nb)
+            for (int c = g * G8; c < imin64(nb, (g + 1) * G8); c++) acc = cadd(acc, cmul(B[c * LB + r], svin[c]));
+          spart[g][r] = acc;
+        }
+        __syncthreads();
+        if (tid < nb) {
+          double2 s = spart[0][tid];
+          for (int g = 1; g < 8; g++) s = cadd(s, spart[g][tid]);
+          sg[tid] = cmul(tin, s);
+        }
+        __syncthreads();
+      }
+      mark(1);
+      // ---- warp 0: the reflector of task (i, j) from the target column (after
+      // (c): x = B[:, 0] - g conj(v_in[0])), its outputs and the message to
+      // position j+1; warps 1..: the rest of (c), B[:, 1:] -= g v_in^H
+      const int tc = j == 0 ? nb - 1 : 0;
+      if (warp == 0) {
+        double2 x0 = czero(), x1 = czero();
+        if (lane < len) x0 = B[tc * LB + lane];
+        if (lane + 32 < len) x1 = B[tc * LB + lane + 32];
+        if (updc) {
+          const double2 cv0 = cconj(svin[0]);
+          if (lane < len) x0 = csub(x0, cmul(sg[lane], cv0));
+          if (lane + 32 < len) x1 = csub(x1, cmul(sg[lane + 32], cv0));
+        }
+        reflector(x0, x1, __shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0), len);
+        __syncwarp();
+        const double2 tau = s_tau2[0];
+        const int64_t slot = a.off[j] + i;
+        double2 *vm = a.vmsg + ((int64_t)j * 2 + par) * (nb + 1);
+        for (int t = lane; t < nb; t += 32) {
+          a.V2[slot * nb + t] = sv[t];
+          vm[t] = sv[t];
+        }
+        if (lane == 0) {
+          a.tau2[slot] = tau;
+          vm[nb] = tau;
+          if (j == 0) AB[1 + i * (int64_t)ldab] = s_beta2[0];   // e_i (scaled units)
+        }
+        __syncwarp();   // orders the lanes' stores before lane 0's (cumulative) release
+        if (lane == 0) st_release_i32(a.vflag + j, (int)(i + 1));
+      } else if (updc) {
+        for (int e = tid - 32; e < nb * (nb - 1); e += HT - 32) {
+          const int r = e % nb, c = 1 + e / nb;
+          B[c * LB + r] = csub(B[c * LB + r], cmul(sg[r], cconj(svin[c])));
+        }
+      }
+      __syncthreads();
+      mark(2);
+      const double2 tau = s_tau2[0], ctau = cconj(tau);
+      const bool upd = tau.x != 0.0 || tau.y != 0.0;
+      // ---- (a) f_c = conj(tau) v^H B[:, c] (c >= 1) and (b) p = tau D v, one pass
+      if (upd) {
+        const int g = tid >> 6, x = tid & 63;
+        double2 accf = czero(), accp = czero();
+        if (j >= 1 && x >= 1 && x < nb)
+          for (int r = g * G8; r < imin64(nb, (g + 1) * G8); r++) accf = cadd(accf, cmulc(sv[r], B[x * LB + r]));
+        if (x < nb)
+          for (int c = g * G8; c < imin64(nb, (g + 1) * G8); c++) {
+            double2 d = D[c <= x ? dix(x, c) : dix(c, x)];   // Hermitian from the lower triangle
+            d.y = c < x ? d.y : (c > x ? -d.y : 0.0);
+            accp = cadd(accp, cmul(d, sv[c]));
+          }
+        spart[g][x] = accf;
+        spart2[g][x] = accp;
+        __syncthreads();
+        if (tid < 64) {
+          if (tid >= 1 && tid < nb) {
+            double2 s = spart[0][tid];
+            for (int gg = 1; gg < 8; gg++) s = cadd(s, spart[gg][tid]);
+            sf[tid] = cmul(ctau, s);
+          }
+        } else if (tid < 128) {
+          const int r = tid - 64;
+          if (r < nb) {
+            double2 s = spart2[0][r];
+            for (int gg = 1; gg < 8; gg++) s = cadd(s, spart2[gg][r]);
+            sp[r] = cmul(tau, s);
+          }
+        }
+        __syncthreads();
+        if (warp == 0) {   // w = p - 1/2 tau (p^H v) v
+          double2 sdot = czero();
+          for (int t = lane; t < nb; t += 32) sdot = cadd(sdot, cmulc(sp[t], sv[t]));
+          sdot = warp_sum2(sdot);
+          const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), sdot);
+          for (int t = lane; t < nb; t += 32) sp[t] = cadd(sp[t], cmul(al, sv[t]));
+        }
+      }
+      mark(3);
+      // ---- warp 0: the row leaving the windows -> message to position j-1
+      // (B row 0 after (a), D(0, 0) after (b)); j = 0: D(0, 0) is d_{i+1}
+      if (warp == 0) {
+        __syncwarp();
+        double2 *rm = a.rmsg + ((int64_t)j * 2 + par) * (nb + 1);
+        if (j >= 1)
+          for (int c = lane; c < nb; c += 32) {
+            double2 b = c == 0 ? s_beta2[0] : B[c * LB];
+            if (c >= 1 && upd) b = csub(b, cmul(sv[0], sf[c]));
+            rm[c] = b;
+          }
+        if (lane == 0) {
+          double2 d00 = D[0];
+          if (upd) d00 = csub(d00, cadd(cmul(sv[0], cconj(sp[0])), cmul(sp[0], cconj(sv[0]))));
+          d00.y = 0.0;
+          if (j == 0) AB[(i + 1) * (int64_t)ldab] = d00;   // d_{i+1} (final after sweep i)
+          else rm[nb] = d00;
+        }
+        __syncwarp();
+        if (j >= 1 && lane == 0) st_release_i32(a.rflag + j, (int)(i + 1));
+      }
+      __syncthreads();   // w (sp) is visible to every warp
+      mark(4);
+      // ---- (a) and (b) updates, written one row / column up-left (the next
+      // sweep's windows); D's column 0 becomes B's last column
+      {
+        // thread: row r = tid & 63, columns c = g + 8u (B: 1 + g + 8u), g = tid >> 6,
+        // so v_r, w_r stay in registers and v_c, w_c, f_c are warp broadcasts
+        const int r = tid & 63, g = tid >> 6;
+        const bool rok = r >= 1 && r < nb;
+        const double2 vr = sv[r], pr = upd ? sp[r] : czero();
+        double2 vb[8], vd[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int cb = 1 + g + 8 * u, cd = g + 8 * u;
+          vb[u] = czero();
+          if (j >= 1 && rok && cb < nb) {
+            const double2 b = B[cb * LB + r];
+            vb[u] = upd ? csub(b, cmul(vr, sf[cb])) : b;
+          }
+          vd[u] = czero();
+          if (rok && cd <= r) {
+            double2 d = D[dix(r, cd)];
+            if (upd) d = csub(d, cadd(cmul(vr, cconj(sp[cd])), cmul(pr, cconj(sv[cd]))));
+            if (r == cd) d.y = 0.0;
+            vd[u] = d;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int cb = 1 + g + 8 * u, cd = g + 8 * u;
+          if (j >= 1 && rok && cb < nb) B[(cb - 1) * LB + r - 1] = vb[u];
+          if (rok && cd <= r) {
+            if (cd >= 1) D[dix(r - 1, cd - 1)] = vd[u];
+            else B[(nb - 1) * LB + r - 1] = vd[u];
+          }
+        }
+      }
+      mark(5);
+    }
+  }
+  if (prof)
+    for (int kk = 0; kk < 6; kk++) atomicAdd(&a.prof[16 + kk], (unsigned long long)tacc[kk]);
+}
+
 // Band copy plus the magnitude key of its largest entry (atomicMax into *key).
 __global__ void band_in_kernel(int64_t n, int nb, const double2 *A, int64_t lda, double2 *AB, int ldab,
                                unsigned *key) {
@@ -349,7 +657,40 @@ int hb2st(Ctx &ctx, int64_t n, int nb, const double2 *A, int64_t lda, double *d,
   EIG_TRY(ctx.launched("band_in_kernel"));
   band_scale_kernel<<<bgrid, 256, 0, ctx.stream>>>(total, AB, key);
   EIG_TRY(ctx.launched("band_scale_kernel"));
-  if (n > 1) {
+  const int64_t Jpos = n > 1 ? (n - 2) / nb + 1 : 0;   // positions of sweep 0
+  // position-stationary kernel (default) when its ceil(J / 2) CTAs are co-resident;
+  // EIG_HB2ST_SYS=0 selects the sweep-per-CTA kernel
+  static const int sys_env = [] {
+    const char *e = getenv("EIG_HB2ST_SYS");
+    return e ? atoi(e) : 1;
+  }();
+  const size_t sys_smem = (size_t)2 * (DPK + 64 * LB) * sizeof(double2);
+  if (n > 1 && sys_env && (Jpos + 1) / 2 <= ctx.num_sms) {
+    const size_t msg = (size_t)Jpos * 2 * (nb + 1);
+    double2 *mbuf = (double2 *)ctx.ws(WS_HBMSG, 2 * msg * sizeof(double2));
+    int *flags = (int *)ctx.ws(WS_HBFLAG, (size_t)2 * Jpos * sizeof(int));
+    if (!mbuf || !flags) return EIG_ERR_NOMEM;
+    EIG_TRY(ctx.check(cudaMemsetAsync(flags, 0, (size_t)2 * Jpos * sizeof(int), ctx.stream), "memset hb flags"));
+    SysArgs s;
+    s.n = n;
+    s.nb = nb;
+    s.ldab = ldab;
+    s.J = (int)Jpos;
+    s.AB = AB;
+    s.V2 = V2;
+    s.tau2 = tau2;
+    s.off = d_off;
+    s.vmsg = mbuf;
+    s.rmsg = mbuf + msg;
+    s.vflag = flags;
+    s.rflag = flags + Jpos;
+    s.prof = ctx.q2_prof;
+    void *args[] = {&s};
+    EIG_TRY(ctx.smem_attr((const void *)hb2sys_kernel, (int)sys_smem, "hb2sys attr"));
+    EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)hb2sys_kernel, dim3((unsigned)((Jpos + 1) / 2)), dim3(HT),
+                                                  args, sys_smem, ctx.stream), "hb2sys launch"));
+    EIG_TRY(ctx.launched("hb2sys_kernel"));
+  } else if (n > 1) {
     HbArgs a;
     a.n = n;
     a.nb = nb;
