@@ -328,11 +328,16 @@ struct SysArgs {
 };
 
 __device__ __forceinline__ double2 ldcg2(const double2 *p) { return __ldcg(p); }
+// named barriers (bar.sync 0 is __syncthreads): producer arrives, consumer syncs
+__device__ __forceinline__ void nbar_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
 
 __global__ void __launch_bounds__(HT, 1) hb2sys_kernel(SysArgs a) {
   namespace cg = cooperative_groups;
   extern __shared__ __align__(16) double2 ysm[];
-  __shared__ double2 sv[64], svin[64], sp[64], sg[64], sf[64];
+  __shared__ double2 sv[64], svin[64], sp[64], sg[64], sf[64], srow[65], srowx[65], svx[65], srx[65];
   __shared__ double2 spart[8][64], spart2[8][64];
   __shared__ double2 s_tau2[1], s_beta2[1], s_tauin;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(HT, 1) hb2sys_kernel(SysArgs a) {
     return (c >= 0 && c < n && r < n && r >= c && r - c < ldab) ? AB[(r - c) + c * (int64_t)ldab] : czero();
   };
   const int k = blockIdx.x;
-  const bool prof = a.prof != nullptr && k == 0 && tid == 0;
+  const bool prof = a.prof != nullptr && k == 1 && tid == 0;   // a CTA with two full positions
   long long tm = 0, tacc[6] = {0, 0, 0, 0, 0, 0};
   auto mark = [&](int kk) {
     if (prof) {
@@ -396,203 +401,291 @@ __global__ void __launch_bounds__(HT, 1) hb2sys_kernel(SysArgs a) {
     }
   };
 
-  const int G8 = (nb + 7) / 8;   // terms per group in the 8-group matvecs
+  const int G7 = (nb + 6) / 7;   // terms per group, 7-group matvecs (workers)
+  // Roles: warp 0 = leader (reflector; fetches the next task's cross-CTA
+  // message), warps 1-14 = workers ((c), (a), (b); warp 1 also builds w and
+  // the leaving row), warp 15 = messenger (every global store of the chase:
+  // the messages with their releases, V2 / tau2, d / e).  The compute warps
+  // synchronise with named barriers that leave the messenger out, so a
+  // release (which waits for its stores) never stalls the compute warps.
+  // Messages between the two positions of a CTA (v of 2k -> 2k+1, row of
+  // 2k+1 -> 2k) stay in shared memory.
+  // Barriers: 5 compute warps (480); 1, 8 workers (448); 3 leader -> workers;
+  // 2 leader -> messenger (reflector ready), 7 messenger -> leader (read);
+  // 4 warp 1 -> messenger (row ready), 6 messenger -> warp 1 (read).
+  const int t = tid - 32;                     // worker index (warps 1-14: 0..447)
+  const int wr = t & 63, wg = t >> 6;         // worker row, group
+  auto active = [&](int64_t ii, int jj) { return jj < a.J && ii + 1 + (int64_t)jj * nb <= n - 1; };
+  auto has_next = [&](int64_t ii, int qq) { return (qq == 0 && active(ii, 2 * k + 1)) || active(ii + 1, 2 * k); };
+  if (warp == 15) {
+    // ================= messenger
+    for (int64_t i = 0; i + 1 < n; i++) {
+      if (!active(i, 2 * k)) break;
+      for (int q = 0; q < 2; q++) {
+        const int j = 2 * k + q;
+        if (!active(i, j)) break;
+        const int par = (int)(i & 1);
+        nbar_sync(2, 64);   // the leader's reflector
+        const double2 v0 = sv[lane], v1 = sv[lane + 32], tau = s_tau2[0], beta = s_beta2[0];
+        __syncwarp();
+        if (has_next(i, q)) nbar_arrive(7, 64);
+        if (q == 1) {   // v of an odd position -> CTA k+1
+          double2 *vm = a.vmsg + ((int64_t)j * 2 + par) * (nb + 1);
+          if (lane < nb) vm[lane] = v0;
+          if (lane + 32 < nb) vm[lane + 32] = v1;
+          if (lane == 0) vm[nb] = tau;
+          __syncwarp();   // orders the lanes' stores before lane 0's (cumulative) release
+          if (lane == 0) st_release_i32(a.vflag + j, (int)(i + 1));
+        }
+        const int64_t slot = a.off[j] + i;
+        if (lane < nb) a.V2[slot * nb + lane] = v0;
+        if (lane + 32 < nb) a.V2[slot * nb + lane + 32] = v1;
+        if (lane == 0) {
+          a.tau2[slot] = tau;
+          if (j == 0) AB[1 + i * (int64_t)ldab] = beta;   // e_i (scaled units)
+        }
+        if (q == 0) {
+          nbar_sync(4, 64);   // the leaving row of an even position
+          const double2 r0v = srowx[lane], r1v = srowx[lane + 32], rn = srowx[nb];
+          __syncwarp();
+          if (active(i + 1, 2 * k)) nbar_arrive(6, 64);
+          if (j >= 1) {   // -> CTA k-1
+            double2 *rm = a.rmsg + ((int64_t)j * 2 + par) * (nb + 1);
+            if (lane < nb) rm[lane] = r0v;
+            if (lane + 32 < nb) rm[lane + 32] = r1v;
+            if (lane == 0) rm[nb] = rn;
+            __syncwarp();
+            if (lane == 0) st_release_i32(a.rflag + j, (int)(i + 1));
+          } else if (lane == 0) {
+            AB[(i + 1) * (int64_t)ldab] = rn;   // d_{i+1} (final after sweep i)
+          }
+        }
+      }
+    }
+  } else {
+  // ================= compute warps
+  // leader: fetch the cross-CTA message task (ii, 2k+qq) needs into shared memory
+  auto prefetch = [&](int64_t ii, int qq) {
+    if (qq == 0) {
+      if (k == 0) return;
+      const int jp = 2 * k - 1;
+      if (lane == 0)
+        while (ld_acquire_i32(a.vflag + jp) < ii + 1) {
+        }
+      __syncwarp();
+      const double2 *m = a.vmsg + ((int64_t)jp * 2 + (ii & 1)) * (nb + 1);
+      for (int u = lane; u <= nb; u += 32) svx[u] = ldcg2(m + u);
+    } else {
+      const int jn = 2 * k + 2;
+      if (!(ii > 0 && active(ii - 1, jn))) return;
+      if (lane == 0)
+        while (ld_acquire_i32(a.rflag + jn) < ii) {
+        }
+      __syncwarp();
+      const double2 *m = a.rmsg + ((int64_t)jn * 2 + ((ii - 1) & 1)) * (nb + 1);
+      for (int u = lane; u <= nb; u += 32) srx[u] = ldcg2(m + u);
+    }
+  };
+  if (warp == 0 && active(0, 2 * k)) prefetch(0, 0);
+  bool first = true, first0 = true;
   for (int64_t i = 0; i + 1 < n; i++) {
-    if (i + 1 + (int64_t)(2 * k) * nb > n - 1) break;   // both positions are past the matrix
+    if (!active(i, 2 * k)) break;   // both positions are past the matrix
     for (int q = 0; q < 2; q++) {
       const int j = 2 * k + q;
-      if (j >= a.J) break;
+      if (!active(i, j)) break;
       const int64_t r0 = i + 1 + (int64_t)j * nb;
-      if (r0 > n - 1) break;   // position j (and every later one) is past the matrix
       const int len = (int)imin64(nb, n - r0);
       double2 *D = Dq(q), *B = Bq(q);
-      const int par = (int)(i & 1);
       mark(-1);
-      // ---- waits: position j+1's row of sweep i-1 (other CTA when q = 1) and
-      // position j-1's reflector of sweep i (other CTA when q = 0)
-      const bool act1 = i > 0 && i + (int64_t)(j + 1) * nb <= n - 1;   // position j+1 ran sweep i-1
-      if (tid == 0) {
-        if (act1 && q == 1)
-          while (ld_acquire_i32(a.rflag + j + 1) < i) {
-          }
-        if (j >= 1 && q == 0)
-          while (ld_acquire_i32(a.vflag + j - 1) < i + 1) {
-          }
-      }
-      __syncthreads();
+      const bool act1 = i > 0 && active(i - 1, j + 1);   // position j+1 ran sweep i-1
+      nbar_sync(5, HT - 32);   // prefetched messages are in shared memory; the previous task is done
       mark(0);
       // entering row of the windows (sweep i-1 -> i) and the incoming reflector
-      if (i > 0 && tid < nb) {
-        const double2 *m = a.rmsg + ((int64_t)(j + 1) * 2 + ((i - 1) & 1)) * (nb + 1);
-        D[dix(nb - 1, tid)] = act1 ? ldcg2(m + (tid < nb - 1 ? tid + 1 : nb)) : czero();
-        B[tid * LB + nb - 1] = (tid < nb - 1 || !act1) ? czero() : ldcg2(m);
+      if (i > 0 && t >= 0 && t < nb) {   // (workers: the leader goes straight to its barrier)
+        const double2 *m = q == 0 ? srow : srx;
+        D[dix(nb - 1, t)] = act1 ? m[t < nb - 1 ? t + 1 : nb] : czero();
+        B[t * LB + nb - 1] = (t < nb - 1 || !act1) ? czero() : m[0];
       }
-      if (j >= 1 && tid >= 64 && tid <= 64 + nb) {
-        const double2 x = ldcg2(a.vmsg + ((int64_t)(j - 1) * 2 + par) * (nb + 1) + (tid - 64));
-        if (tid - 64 < nb) svin[tid - 64] = x;
+      if (j >= 1 && t >= 64 && t <= 64 + nb) {
+        const int u = t - 64;
+        const double2 x = q == 0 ? svx[u] : (u < nb ? sv[u] : s_tau2[0]);
+        if (u < nb) svin[u] = x;
         else s_tauin = x;
       }
-      __syncthreads();
-      // ---- (c) of task (i, j-1): g = tau_in B v_in
+      mark(5);
+      nbar_sync(5, HT - 32);
+      mark(4);
+      // ---- (c) of task (i, j-1): partials of g = tau_in B v_in (workers)
       const double2 tin = j >= 1 ? s_tauin : czero();
       const bool updc = tin.x != 0.0 || tin.y != 0.0;
       if (updc) {
-        {
-          const int g = tid >> 6, r = tid & 63;
+        if (warp > 0 && wr < nb) {
           double2 acc = czero();
-          if (r < nb)
-            for (int c = g * G8; c < imin64(nb, (g + 1) * G8); c++) acc = cadd(acc, cmul(B[c * LB + r], svin[c]));
-          spart[g][r] = acc;
+          for (int c = wg * G7; c < imin64(nb, (wg + 1) * G7); c++) acc = cadd(acc, cmul(B[c * LB + wr], svin[c]));
+          spart[wg][wr] = acc;
         }
-        __syncthreads();
-        if (tid < nb) {
-          double2 s = spart[0][tid];
-          for (int g = 1; g < 8; g++) s = cadd(s, spart[g][tid]);
-          sg[tid] = cmul(tin, s);
-        }
-        __syncthreads();
+        nbar_sync(5, HT - 32);
       }
       mark(1);
-      // ---- warp 0: the reflector of task (i, j) from the target column (after
-      // (c): x = B[:, 0] - g conj(v_in[0])), its outputs and the message to
-      // position j+1; warps 1..: the rest of (c), B[:, 1:] -= g v_in^H
       const int tc = j == 0 ? nb - 1 : 0;
       if (warp == 0) {
+        // ================= leader: reflector of task (i, j) from the target
+        // column after (c) (x = B[:, 0] - g conj(v_in[0]))
         double2 x0 = czero(), x1 = czero();
         if (lane < len) x0 = B[tc * LB + lane];
         if (lane + 32 < len) x1 = B[tc * LB + lane + 32];
         if (updc) {
           const double2 cv0 = cconj(svin[0]);
-          if (lane < len) x0 = csub(x0, cmul(sg[lane], cv0));
-          if (lane + 32 < len) x1 = csub(x1, cmul(sg[lane + 32], cv0));
+          double2 g0 = czero(), g1 = czero();
+          for (int g = 0; g < 7; g++) {
+            g0 = cadd(g0, spart[g][lane]);
+            g1 = cadd(g1, spart[g][lane + 32]);
+          }
+          if (lane < len) x0 = csub(x0, cmul(cmul(tin, g0), cv0));
+          if (lane + 32 < len) x1 = csub(x1, cmul(cmul(tin, g1), cv0));
         }
+        if (!first) nbar_sync(7, 64);   // the messenger has read the previous reflector
+        first = false;
         reflector(x0, x1, __shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0), len);
         __syncwarp();
-        const double2 tau = s_tau2[0];
-        const int64_t slot = a.off[j] + i;
-        double2 *vm = a.vmsg + ((int64_t)j * 2 + par) * (nb + 1);
-        for (int t = lane; t < nb; t += 32) {
-          a.V2[slot * nb + t] = sv[t];
-          vm[t] = sv[t];
-        }
-        if (lane == 0) {
-          a.tau2[slot] = tau;
-          vm[nb] = tau;
-          if (j == 0) AB[1 + i * (int64_t)ldab] = s_beta2[0];   // e_i (scaled units)
-        }
-        __syncwarp();   // orders the lanes' stores before lane 0's (cumulative) release
-        if (lane == 0) st_release_i32(a.vflag + j, (int)(i + 1));
-      } else if (updc) {
-        for (int e = tid - 32; e < nb * (nb - 1); e += HT - 32) {
-          const int r = e % nb, c = 1 + e / nb;
-          B[c * LB + r] = csub(B[c * LB + r], cmul(sg[r], cconj(svin[c])));
-        }
-      }
-      __syncthreads();
-      mark(2);
-      const double2 tau = s_tau2[0], ctau = cconj(tau);
-      const bool upd = tau.x != 0.0 || tau.y != 0.0;
-      // ---- (a) f_c = conj(tau) v^H B[:, c] (c >= 1) and (b) p = tau D v, one pass
-      if (upd) {
-        const int g = tid >> 6, x = tid & 63;
-        double2 accf = czero(), accp = czero();
-        if (j >= 1 && x >= 1 && x < nb)
-          for (int r = g * G8; r < imin64(nb, (g + 1) * G8); r++) accf = cadd(accf, cmulc(sv[r], B[x * LB + r]));
-        if (x < nb)
-          for (int c = g * G8; c < imin64(nb, (g + 1) * G8); c++) {
-            double2 d = D[c <= x ? dix(x, c) : dix(c, x)];   // Hermitian from the lower triangle
-            d.y = c < x ? d.y : (c > x ? -d.y : 0.0);
-            accp = cadd(accp, cmul(d, sv[c]));
+        nbar_arrive(3, HT - 32);   // workers: the reflector is in shared memory
+        nbar_arrive(2, 64);        // messenger
+        mark(2);
+        // the next task's cross-CTA message
+        if (q == 0 && active(i, j + 1)) prefetch(i, 1);
+        else if (active(i + 1, 2 * k)) prefetch(i + 1, 0);
+        mark(3);
+      } else {
+        // ================= workers
+        // rest of (c): B[:, 1:] -= g v_in^H   (g combined by worker warps 1-2)
+        if (updc) {
+          if (t < nb) {
+            double2 s = spart[0][t];
+            for (int g = 1; g < 7; g++) s = cadd(s, spart[g][t]);
+            sg[t] = cmul(tin, s);
           }
-        spart[g][x] = accf;
-        spart2[g][x] = accp;
-        __syncthreads();
-        if (tid < 64) {
-          if (tid >= 1 && tid < nb) {
-            double2 s = spart[0][tid];
-            for (int gg = 1; gg < 8; gg++) s = cadd(s, spart[gg][tid]);
-            sf[tid] = cmul(ctau, s);
-          }
-        } else if (tid < 128) {
-          const int r = tid - 64;
-          if (r < nb) {
-            double2 s = spart2[0][r];
-            for (int gg = 1; gg < 8; gg++) s = cadd(s, spart2[gg][r]);
-            sp[r] = cmul(tau, s);
+          nbar_sync(1, HT - 64);
+          if (wr < nb) {
+            const double2 gr = sg[wr];
+            for (int c = 1 + wg; c < nb; c += 7) B[c * LB + wr] = csub(B[c * LB + wr], cmul(gr, cconj(svin[c])));
           }
         }
-        __syncthreads();
-        if (warp == 0) {   // w = p - 1/2 tau (p^H v) v
-          double2 sdot = czero();
-          for (int t = lane; t < nb; t += 32) sdot = cadd(sdot, cmulc(sp[t], sv[t]));
-          sdot = warp_sum2(sdot);
-          const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), sdot);
-          for (int t = lane; t < nb; t += 32) sp[t] = cadd(sp[t], cmul(al, sv[t]));
+        nbar_sync(3, HT - 32);   // the leader's reflector
+        const double2 tau = s_tau2[0], ctau = cconj(tau);
+        const bool upd = tau.x != 0.0 || tau.y != 0.0;
+        // (a) f_c = conj(tau) v^H B[:, c] (c >= 1) and (b) p = tau D v: partials
+        if (upd) {
+          const int x = wr;
+          double2 accf = czero(), accp = czero();
+          if (x < nb) {
+            for (int r = wg * G7; r < imin64(nb, (wg + 1) * G7); r++) {
+              if (j >= 1 && x >= 1) accf = cadd(accf, cmulc(sv[r], B[x * LB + r]));
+              double2 d = D[r <= x ? dix(x, r) : dix(r, x)];   // Hermitian from the lower triangle (c = r)
+              d.y = r < x ? d.y : (r > x ? -d.y : 0.0);
+              accp = cadd(accp, cmul(d, sv[r]));
+            }
+          }
+          spart[wg][x] = accf;
+          spart2[wg][x] = accp;
+          nbar_sync(1, HT - 64);
         }
-      }
-      mark(3);
-      // ---- warp 0: the row leaving the windows -> message to position j-1
-      // (B row 0 after (a), D(0, 0) after (b)); j = 0: D(0, 0) is d_{i+1}
-      if (warp == 0) {
-        __syncwarp();
-        double2 *rm = a.rmsg + ((int64_t)j * 2 + par) * (nb + 1);
-        if (j >= 1)
+        // worker warp 1: f, w = p - 1/2 tau (p^H v) v, and the leaving row
+        if (warp == 1) {
+          double2 p0 = czero(), p1 = czero();
+          if (upd) {
+            double2 f0 = czero(), f1 = czero();
+            for (int g = 0; g < 7; g++) {
+              f0 = cadd(f0, spart[g][lane]);
+              f1 = cadd(f1, spart[g][lane + 32]);
+              p0 = cadd(p0, spart2[g][lane]);
+              p1 = cadd(p1, spart2[g][lane + 32]);
+            }
+            sf[lane] = cmul(ctau, f0);
+            sf[lane + 32] = cmul(ctau, f1);
+            p0 = lane < nb ? cmul(tau, p0) : czero();
+            p1 = lane + 32 < nb ? cmul(tau, p1) : czero();
+            const double2 v0 = sv[lane], v1 = sv[lane + 32];
+            const double2 sdot = warp_sum2(cadd(cmulc(p0, v0), cmulc(p1, v1)));
+            const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), sdot);
+            p0 = cadd(p0, cmul(al, v0));
+            p1 = cadd(p1, cmul(al, v1));
+            sp[lane] = p0;
+            sp[lane + 32] = p1;
+          }
+          __syncwarp();
+          // leaving row: B row 0 after (a) (j >= 1), D(0, 0) after (b); an even
+          // position's row goes to the messenger, an odd one's stays here
+          double2 *so = srow;
+          if (q == 0) {
+            if (!first0) nbar_sync(6, 64);   // the messenger has read the previous one
+            first0 = false;
+            so = srowx;
+          }
+          const double2 vv0 = sv[0];
           for (int c = lane; c < nb; c += 32) {
             double2 b = c == 0 ? s_beta2[0] : B[c * LB];
-            if (c >= 1 && upd) b = csub(b, cmul(sv[0], sf[c]));
-            rm[c] = b;
+            if (c >= 1 && upd) b = csub(b, cmul(vv0, sf[c]));
+            so[c] = b;
           }
-        if (lane == 0) {
-          double2 d00 = D[0];
-          if (upd) d00 = csub(d00, cadd(cmul(sv[0], cconj(sp[0])), cmul(sp[0], cconj(sv[0]))));
-          d00.y = 0.0;
-          if (j == 0) AB[(i + 1) * (int64_t)ldab] = d00;   // d_{i+1} (final after sweep i)
-          else rm[nb] = d00;
+          if (lane == 0) {
+            double2 d00 = D[0];
+            if (upd) {
+              const double2 w0 = sp[0];
+              d00 = csub(d00, cadd(cmul(vv0, cconj(w0)), cmul(w0, cconj(vv0))));
+            }
+            d00.y = 0.0;
+            so[nb] = d00;
+          }
+          __syncwarp();
+          if (q == 0) nbar_arrive(4, 64);
         }
-        __syncwarp();
-        if (j >= 1 && lane == 0) st_release_i32(a.rflag + j, (int)(i + 1));
-      }
-      __syncthreads();   // w (sp) is visible to every warp
-      mark(4);
-      // ---- (a) and (b) updates, written one row / column up-left (the next
-      // sweep's windows); D's column 0 becomes B's last column
-      {
-        // thread: row r = tid & 63, columns c = g + 8u (B: 1 + g + 8u), g = tid >> 6,
-        // so v_r, w_r stay in registers and v_c, w_c, f_c are warp broadcasts
-        const int r = tid & 63, g = tid >> 6;
-        const bool rok = r >= 1 && r < nb;
-        const double2 vr = sv[r], pr = upd ? sp[r] : czero();
-        double2 vb[8], vd[8];
+        nbar_sync(1, HT - 64);   // w is staged
+        // (a) and (b) updates, written one row / column up-left; D's column 0 -> B's last column
+        {
+          const int r = wr;
+          const bool rok = r >= 1 && r < nb;
+          const double2 vr = sv[r], pr = upd ? sp[r] : czero();
+          double2 vb[9], vd[10];
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
-          const int cb = 1 + g + 8 * u, cd = g + 8 * u;
-          vb[u] = czero();
-          if (j >= 1 && rok && cb < nb) {
-            const double2 b = B[cb * LB + r];
-            vb[u] = upd ? csub(b, cmul(vr, sf[cb])) : b;
+          for (int u = 0; u < 9; u++) {
+            const int cb = 1 + wg + 7 * u;
+            vb[u] = czero();
+            if (j >= 1 && rok && cb < nb) {
+              const double2 b = B[cb * LB + r];
+              vb[u] = upd ? csub(b, cmul(vr, sf[cb])) : b;
+            }
           }
-          vd[u] = czero();
-          if (rok && cd <= r) {
-            double2 d = D[dix(r, cd)];
-            if (upd) d = csub(d, cadd(cmul(vr, cconj(sp[cd])), cmul(pr, cconj(sv[cd]))));
-            if (r == cd) d.y = 0.0;
-            vd[u] = d;
-          }
-        }
-        __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
-          const int cb = 1 + g + 8 * u, cd = g + 8 * u;
-          if (j >= 1 && rok && cb < nb) B[(cb - 1) * LB + r - 1] = vb[u];
-          if (rok && cd <= r) {
-            if (cd >= 1) D[dix(r - 1, cd - 1)] = vd[u];
-            else B[(nb - 1) * LB + r - 1] = vd[u];
+          for (int u = 0; u < 10; u++) {
+            const int cd = wg + 7 * u;
+            vd[u] = czero();
+            if (rok && cd <= r) {
+              double2 d = D[dix(r, cd)];
+              if (upd) d = csub(d, cadd(cmul(vr, cconj(sp[cd])), cmul(pr, cconj(sv[cd]))));
+              if (r == cd) d.y = 0.0;
+              vd[u] = d;
+            }
+          }
+          nbar_sync(8, HT - 64);
+#pragma unroll
+          for (int u = 0; u < 9; u++) {
+            const int cb = 1 + wg + 7 * u;
+            if (j >= 1 && rok && cb < nb) B[(cb - 1) * LB + r - 1] = vb[u];
+          }
+#pragma unroll
+          for (int u = 0; u < 10; u++) {
+            const int cd = wg + 7 * u;
+            if (rok && cd <= r) {
+              if (cd >= 1) D[dix(r - 1, cd - 1)] = vd[u];
+              else B[(nb - 1) * LB + r - 1] = vd[u];
+            }
           }
         }
       }
       mark(5);
     }
   }
+  }   // compute warps
   if (prof)
     for (int kk = 0; kk < 6; kk++) atomicAdd(&a.prof[16 + kk], (unsigned long long)tacc[kk]);
 }

@@ -475,7 +475,9 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
     return e ? (int64_t)atoll(e) : (int64_t)kNarrowN;
   }();
   if (g.whole_n && g.N > Lay<0>::BN) return -2;
-  const int v = !m3 ? 0 : ((g.K <= shortk || g.N <= narrow) && !g.whole_n ? 2 : 1);
+  // (with split_n set the choice must not depend on N: column slices stay bitwise)
+  const bool narrow_n = g.split_n <= 0 && g.N <= narrow;
+  const int v = !m3 ? 0 : ((g.K <= shortk || narrow_n) && !g.whole_n ? 2 : 1);
   const int BN = v == 2 ? Lay<2>::BN : Lay<0>::BN;
   const int64_t q = BM / BN;
   const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
