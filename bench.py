@@ -414,7 +414,9 @@ def run_b200(a, rank, world, local_rank):
     if stages:
         stage_flops = {"he2hb": 16.0 / 3.0 * n ** 3, "q2": 8.0 * n * n * m, "q1": 8.0 * n * n * m,
                        "trsm": 4.0 * n * n * m}
-        q2k = "apply_q2wave_kernel" if (nb == 64 and a.g == 32) else "apply_q2_kernel"
+        q2_3m = os.environ.get("EIG_Q2_3M", "1") != "0"
+        q2k = (("apply_q2wave3_kernel" if q2_3m else "apply_q2wave_kernel") if (nb == 64 and a.g == 32)
+               else "apply_q2_kernel")
         kern = {"he2hb": "zgemm_kernel (hemm+her2k) + panel_qr_kernel", "q2": q2k,
                 "q1": "zgemm_kernel", "trsm": "zgemm_kernel"}
         dom = max(stages, key=stages.get)
@@ -423,13 +425,14 @@ def run_b200(a, rank, world, local_rank):
         roof = {"bound": "tensor", "kernel": kern[dom], "stage": dom, "achieved": ach, "peak": peak,
                 "unit": "TFLOP/s", "frac": ach / peak, "traffic": traffic,
                 "traffic_note": "dram read+write bytes per launch (ncu --set full, profiles/traffic_r02.json); "
-                                "algorithmic E traffic n^2/(2g) m 16 B each way = 2 x 250 GB (the wavefront kernel moves whole 95-row windows: 764 GB measured, 1.5x); compute-bound",
+                                "algorithmic E traffic n^2/(2g) m 16 B each way = 2 x 250 GB (the wavefront kernel moves whole 95-row windows: 786 GB measured, 1.6x); compute-bound",
                 "peak_source": peak_src,
                 "stage_tflops": {k: stage_flops[k] / (stages[k] * 1e-3) / 1e12 for k in stages},
-                # tensor-pipe work: 3M issues 6 real flops per complex MAC (he2hb updates, Q1, trsm), the Q2
-                # real embedding 8 (plus its 616/512 parallelogram overhead, not counted here)
+                # tensor-pipe work: 3M issues 6 real flops per complex MAC (he2hb updates, Q1, trsm and, by
+                # default, Q2), the real embedding 8 (Q2's 492/384 or 616/512 parallelogram overhead not counted)
                 "gemm_mode": a.gemm.upper(),
-                "stage_pipe_frac": {k: stage_flops[k] * (0.75 if (a.gemm == "3m" and k != "q2") else 1.0)
+                "stage_pipe_frac": {k: stage_flops[k] * (0.75 if ((a.gemm == "3m" and k != "q2") or (k == "q2" and q2_3m))
+                                                         else 1.0)
                                     / (stages[k] * 1e-3) / 1e12 / peak for k in stages}}
 
     # e2e through the C ABI with HOST buffers (pinned), N = 1

@@ -79,3 +79,36 @@ def test_full_size_hb2st_known_spectrum():
     idx = np.unique(np.linspace(1, n, 64).astype(int))
     w = np.array([oracle.sturm_values(dd, ee, k, k)[0] for k in idx])
     assert np.max(np.abs(w - D[idx - 1])) < 1e-10
+
+
+@gpu
+def test_hb2st_sweep_per_cta_kernel_subprocess():
+    """EIG_HB2ST_SYS=0 selects the sweep-per-CTA chase (hb2st_kernel, also the
+    kernel for n beyond the position-stationary kernel's co-residency limit);
+    the switch is read once per process, so the oracle comparison runs in a
+    child process."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import oracle, synth
+from test_gpu_hb2st import _band_full, _dev
+from paper_1207_1773_b200 import Solver
+for n, nb in [(150, 16), (517, 64), (64, 8)]:
+    s = Solver(0, nb=nb)
+    A = synth.rand_hermitian(n, n + nb)
+    A_o, _ = oracle.he2hb(A, nb)
+    d, e, V2, tau2 = s.hb2st(_dev(A_o))
+    d_o, e_o, V2_o, tau2_o = oracle.hb2st(_band_full(A_o, nb), nb)
+    scale = np.max(np.abs(A))
+    assert np.max(np.abs(d.cpu().numpy() - d_o)) < 1e-12 * scale * max(1, n / 100)
+    assert np.max(np.abs(e.cpu().numpy() - e_o)) < 1e-12 * scale * max(1, n / 100)
+    assert np.max(np.abs(V2.cpu().numpy() - V2_o)) < 1e-10 * max(1, n / 100)
+print("ok")
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EIG_HB2ST_SYS="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

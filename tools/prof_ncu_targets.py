@@ -7,11 +7,17 @@ import sys
 
 R = sys.argv[1] if len(sys.argv) > 1 else "r02"
 T = [
-    # (name, kernel regex, skip count, command)
-    ("zgemm_CN", "regex:zgemm_kernel<.int.1, .int.0, .bool.0, .int.0, .bool.1>", 0, "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
-    ("zgemm_NN", "regex:zgemm_kernel<.int.0, .int.0, .bool.0, .int.0, .bool.1>", 1, "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
+    # (name, kernel regex, skip count, command); zgemm_kernel<OPA, OPB, HERM, LOWER, variant>
+    ("zgemm_CN", "regex:zgemm_kernel<.int.1, .int.0, .bool.0, .int.0, .int.1>", 0,
+     "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
+    ("zgemm_NN", "regex:zgemm_kernel<.int.0, .int.0, .bool.0, .int.0, .int.1>", 1,
+     "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
+    ("her2k", "regex:zgemm_kernel<.int.0, .int.1, .bool.0, .int.1, .int.2>", 1,
+     "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
+    ("hemm", "regex:zgemm_kernel<.int.0, .int.0, .bool.1, .int.0, .int.2>", 1,
+     "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
     ("panel", "regex:panel_qr_kernel", 20, "python tools/prof_kernels.py he2hb --n 10000 --reps 1"),
-    ("hb2st", "regex:hb2st_kernel", 0, "python tools/prof_kernels.py hb2st --n 10000 --reps 1"),
+    ("hb2sys", "regex:hb2sys_kernel", 0, "python tools/prof_kernels.py hb2st --n 10000 --reps 1"),
 ]
 for name, k, skip, cmd in T:
     rep = f"gpurun_out/{name}_full_{R}"
