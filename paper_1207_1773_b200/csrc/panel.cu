@@ -73,7 +73,17 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 // so the trailing-column update and the T column
 //   T[0:j, j] = -tau_j T[0:j, 0:j] y   (zlarft, forward/columnwise)
 // need no second reduction.
-__global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
+// Warp PT/32 (the messenger) writes the exchange records to global memory and
+// releases the arrival; the PT compute threads hand it each record through a
+// shared-memory slot (bar.arrive) and synchronise among themselves with a
+// named barrier, so no compute barrier waits for the records' global stores
+// or for the release (a CTA barrier right after global stores and a release
+// costs ~1 us; see the bulge chase).
+__device__ __forceinline__ void pbar() { asm volatile("bar.sync 1, %0;" ::"n"(PT) : "memory"); }
+__device__ __forceinline__ void pmsg_arrive() { asm volatile("bar.arrive 2, %0;" ::"n"(PT + 32) : "memory"); }
+__device__ __forceinline__ void pmsg_sync() { asm volatile("bar.sync 2, %0;" ::"n"(PT + 32) : "memory"); }
+
+__global__ void __launch_bounds__(PT + 32, 1) panel_qr_kernel(PanelArgs a) {
   extern __shared__ __align__(16) double2 sm[];
   const int nb = a.nb, R = a.R, G = a.G;
   const int LR = R | 1;   // odd column stride of the resident rows: conflict-free column-parallel access
@@ -93,6 +103,18 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
 
   const int tid = threadIdx.x;
   const int g = blockIdx.x;
+  __shared__ double2 sRec[2][128];   // the next record, by column parity (messenger input)
+  if (tid >= PT) {   // ================= messenger: one record per column, in order
+    const int lane = tid - PT;
+    for (int c = 0; c < a.nref; c++) {
+      pmsg_sync();
+      double2 *out = a.rec + ((int64_t)(c & 1) * G + g) * recw;
+      for (int e = lane; e < recw; e += 32) __stcg(&out[e], sRec[c & 1][e]);
+      __syncwarp();   // orders the lanes' stores before lane 0's (cumulative) release
+      if (lane == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
+    }
+    return;
+  }
   const int64_t row0 = g == 0 ? 0 : (int64_t)a.R0 + (int64_t)(g - 1) * R;
   const int64_t left = a.pn - row0;
   const int cap = g == 0 ? a.R0 : R;
@@ -105,7 +127,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
     for (int r = tid; r < R; r += PT) sP[l * LR + r] = (r < rows) ? a.P[(row0 + r) + (int64_t)l * a.lda] : czero();
   if (g == 0)
     for (int e = tid; e < nb * nb; e += PT) sT[(e % nb) + (e / nb) * LR] = czero();
-  __syncthreads();
+  pbar();
   // column magnitude keys of this CTA's rows (thread cl, rows rlo..rhi)
   {
     unsigned k = 0;
@@ -113,7 +135,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       for (int r = rlo; r < rhi; r++) k = max(k, mag_key2(sP[cl * LR + r]));
     reinterpret_cast<unsigned *>(sPart)[rq * 64 + cl] = k;
   }
-  __syncthreads();
+  pbar();
   // exchange round 0 (records of parity 1: the column-1 records are written
   // only after every CTA has published column 0, i.e. has read these keys)
   {
@@ -124,14 +146,14 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       for (int q = 0; q < NQ; q++) k = max(k, reinterpret_cast<const unsigned *>(sPart)[q * 64 + tid]);
       __stcg(&out[tid], make_double2(__longlong_as_double((long long)k), 0.0));
     }
-    __syncthreads();
+    pbar();
     if (tid == 0) {
       asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
       const unsigned long long target = a.epoch0 + (unsigned long long)G;
       while (ld_acquire_u64(a.cnt) < target) {
       }
     }
-    __syncthreads();
+    pbar();
     {   // every thread takes CTAs q = rq, rq + NQ, ... of column cl (loads batched 4 at a time)
       unsigned k = 0;
       if (cl < nb)
@@ -147,7 +169,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
         }
       reinterpret_cast<unsigned *>(sPart)[NQ * 64 + rq * 64 + cl] = k;   // second half of sPart
     }
-    __syncthreads();
+    pbar();
     if (tid < nb) {
       unsigned k = 0;
 #pragma unroll
@@ -156,13 +178,13 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       sColUp[tid] = U == kExpZero ? 1.0 : pow2i(U);
       sW[tid] = make_double2(U == kExpZero ? 1.0 : pow2i(-U), 0.0);   // 2^-U_l (sW is free until column 0)
     }
-    __syncthreads();
+    pbar();
     for (int l = 0; l < nb; l++) {
       const double f = sW[l].x;
       for (int r = tid; r < rows; r += PT) sP[l * LR + r] = cscale(f, sP[l * LR + r]);
     }
   }
-  __syncthreads();
+  pbar();
 
   const bool prof = a.prof != nullptr && g == 0 && tid == 0;
   long long tm = prof ? clock64() : 0, tacc[6] = {0, 0, 0, 0, 0, 0};
@@ -190,8 +212,8 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       }
     }
     sPart[rq * 64 + cl] = acc;
-    __syncthreads();
-    double2 *out = a.rec + ((int64_t)(jn & 1) * G + g) * recw;
+    pbar();
+    double2 *out = sRec[jn & 1];
     if (tid < nb) {
       double2 t = sPart[tid];
 #pragma unroll
@@ -203,20 +225,16 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
         for (int q = 1; q < NQ; q++) c1 = cadd(c1, sPart[q * 64 + jp]);
         t = csub(t, cmul(ctau, cmul(sW[tid], c1)));
       }
-      __stcg(&out[tid], t);
+      out[tid] = t;
     }
     if (jn >= row0 && jn < row0 + rows)
       for (int l = tid; l < nb; l += PT) {
         double2 pv = sP[l * LR + (jn - row0)];
         if (corr && l > jn) pv = csub(pv, cmul(ctau, cmul(sP[(jn - 1) * LR + (jn - row0)], sW[l])));
-        __stcg(&out[nb + l], pv);
+        out[nb + l] = pv;
       }
-    // the barrier orders every thread's record stores before thread 0's
-    // release increment (fence cumulativity): one release instead of a
-    // membar in every thread; it also keeps the bulk update below from
-    // overwriting row jn before it is recorded
-    __syncthreads();
-    if (tid == 0) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.cnt) : "memory");
+    pmsg_arrive();   // the messenger stores the record and releases the arrival
+    pbar();          // keeps the bulk update below from overwriting row jn before it is recorded
   };
   // record q (CTA q) of the exchange for column j
   auto rec_of = [&](int q, int j) -> const double2 * { return a.rec + ((int64_t)(j & 1) * G + q) * recw; };
@@ -229,7 +247,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       while (ld_acquire_u64(a.cnt) < target) {
       }
     }
-    __syncthreads();
+    pbar();
     mark(0);
     {
       // s_l for l >= j (every CTA: norm, w_l); s_i for i < j only feed T (CTA 0)
@@ -253,7 +271,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       const int owner = j < a.R0 ? 0 : 1 + (j - a.R0) / R;
       if (tid < nb) sRow[tid] = __ldcg(rec_of(owner, j) + nb + tid);
     }
-    __syncthreads();
+    pbar();
     // thread l < nb keeps the reduced s_l in a register; thread j (which holds
     // ||x||^2 and has row j) forms beta / tau / scale: one CTA barrier fewer
     double2 sl = czero();
@@ -285,7 +303,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       s_beta = beta;
       sTau[j] = tau;
     }
-    __syncthreads();
+    pbar();
     mark(2);
     const double2 tau = s_tau, scale = s_scale;
     const double2 ctau = cconj(tau);
@@ -315,7 +333,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
       }
       if (la) pn1[r] = csub(pn1[r], cmul(v, cw));
     }
-    __syncthreads();
+    pbar();
     if (la) {
       mark(3);
       publish(j + 1, true, ctau);
@@ -358,7 +376,7 @@ __global__ void __launch_bounds__(PT, 1) panel_qr_kernel(PanelArgs a) {
         sT[i + j * LR] = make_double2(-(tau.x * acc.x - tau.y * acc.y), -(tau.x * acc.y + tau.y * acc.x));
       if (tid == 0) sT[j + j * LR] = tau;
     }
-    __syncthreads();
+    pbar();
     mark(5);
   }
 
@@ -450,7 +468,7 @@ int panel_qr(Ctx &ctx, double2 *P, int64_t lda, int64_t pn, int nb, double2 *tau
   if (!a.rec || !a.cnt) return EIG_ERR_NOMEM;
   EIG_TRY(ctx.smem_attr((const void *)panel_qr_kernel, 220 * 1024, "panel attr"));
   void *args[] = {&a};
-  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel, dim3(G), dim3(PT), args, smem, stream),
+  EIG_TRY(ctx.check(cudaLaunchCooperativeKernel((void *)panel_qr_kernel, dim3(G), dim3(PT + 32), args, smem, stream),
                     "panel_qr_kernel launch"));
   ctx.bar_epoch += (unsigned long long)G * (nref + 1);   // arrivals this launch performs (scaling round + columns)
   return ctx.launched("panel_qr_kernel");
