@@ -45,6 +45,8 @@ constexpr int64_t kShortK = 256;
 // ... and so do products with N <= kNarrowN (the he2hb hemm W = A22 V, N = nb):
 // twice the tiles of the 64-column variant (EIG_ZGEMM_NARROW overrides)
 constexpr int64_t kNarrowN = 64;
+// 1: plain long-K 3M products take the 128 x 64-tile variant (EIG_ZGEMM_V4 overrides)
+constexpr int kZgemmV4 = 1;
 
 // Enqueue C = alpha op(A) op(B) + beta C on ctx's stream.  Returns 0 or error.
 int zgemm(Ctx &ctx, const Zgemm &g);

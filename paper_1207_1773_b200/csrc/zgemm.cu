@@ -33,7 +33,7 @@
 namespace eig {
 namespace {
 
-constexpr int BM = 64, THREADS = 256;
+constexpr int BM = 64, THREADS = 256;   // (variant 4: BM 128, see Lay)
 // Engine variants V: 0 = real embedding (4 real products; BN 64, BK 16, two
 // 120-register CTAs per SM); 1 = 3M, long K (BN 64, BK 32, warp tile 16 x 32,
 // one 208-register CTA per SM); 2 = 3M, short K (BN 32, BK 16, warp tile
@@ -46,18 +46,23 @@ constexpr int BM = 64, THREADS = 256;
 template <int V>
 struct Lay {
   static constexpr bool M3 = V >= 1;
+  // variant 4 = 3M, 128 x 64 tiles, 32 x 32 warp tiles (8 DADDs per 48 DMMAs
+  // instead of 6 per 24), BK 16, one CTA per SM; plain products only
+  static constexpr int BMV = V == 4 ? 128 : 64;
+  static constexpr int WMR = V == 4 ? 32 : 16;   // 3M warp tile height (complex rows)
+  static constexpr int WARPS_M = BMV / WMR;
   static constexpr int BN = V == 2 ? 32 : 64;
   static constexpr int WN = V == 2 ? 16 : 32;   // 3M warp tile width (complex columns)
-  static constexpr int MINB = V == 1 ? 1 : 2;   // resident CTAs per SM
+  static constexpr int MINB = (V == 1 || V == 4) ? 1 : 2;   // resident CTAs per SM
   // K tile (complex): variant 1 runs one CTA per SM, so it takes twice the K
   // per pipeline stage (half the CTA barriers per flop)
   static constexpr int BK = V == 1 ? 32 : 16;
   static constexpr int STAGES = 3;
-  static constexpr int LDA_S = M3 ? BM + 2 : BM + 4;  // sA[k][m]: k-major, m contiguous
+  static constexpr int LDA_S = M3 ? BMV + 2 : BMV + 4;  // sA[k][m]: k-major, m contiguous
   static constexpr int LDB_S = M3 ? BK + 4 : BK + 2;  // sB[n][k]: n-major, k contiguous
   static constexpr int LDAK = M3 ? BK + 4 : BK + 2;   // op(A) = A^H: sA[m][k], k contiguous
   static constexpr int LDBN = M3 ? BN + 2 : BN + 4;   // op(B) = B^H: sB[k][n], n contiguous
-  static constexpr int SA_ELEMS = (BK * LDA_S > BM * LDAK) ? BK * LDA_S : BM * LDAK;
+  static constexpr int SA_ELEMS = (BK * LDA_S > BMV * LDAK) ? BK * LDA_S : BMV * LDAK;
   static constexpr int SB_ELEMS = (BN * LDB_S > BK * LDBN) ? BN * LDB_S : BK * LDBN;
   static constexpr int STAGE_ELEMS = SA_ELEMS + SB_ELEMS;
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double2);
@@ -81,6 +86,7 @@ struct Params {
 template <int OPA, int OPB, bool HERM, int LOWER, int V>
 __global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) {
   using LY = Lay<V>;
+  constexpr int BM = LY::BMV;   // (shadows the file-scope 64)
   constexpr bool M3 = LY::M3;
   constexpr int BN = LY::BN, M3_WN = LY::WN;
   constexpr int BK = LY::BK, STAGES = LY::STAGES;
@@ -203,14 +209,15 @@ __global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) 
 
   if constexpr (M3) {
     // ------------------------------------------------------------ 3M path
-    // warp tile 16 complex rows (wm) x M3_WN complex cols (wn): 2 x NJ tiles per plane
+    // warp tile WMR complex rows (wm) x M3_WN complex cols (wn): MI x NJ tiles per plane
     const int g8 = lane >> 2, t4 = lane & 3;
-    constexpr int NJ = M3_WN / 8;
-    double acc[3][2][NJ][2];
+    constexpr int NJ = M3_WN / 8, MI = LY::WMR / 8;
+    const int wm3 = warp % LY::WARPS_M, wn3 = warp / LY::WARPS_M;
+    double acc[3][MI][NJ][2];
 #pragma unroll
     for (int q = 0; q < 3; q++)
 #pragma unroll
-      for (int i = 0; i < 2; i++)
+      for (int i = 0; i < MI; i++)
 #pragma unroll
         for (int j = 0; j < NJ; j++) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
     // alpha = -1 (fused): accumulate from -C and negate at the end (exact), so
@@ -218,12 +225,12 @@ __global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) 
     const double cs = aflip ? -1.0 : 1.0;
     if (fuse_c) {   // P1 = Re C, P2 = 0, P3 = Re C + Im C  (times cs)
 #pragma unroll
-      for (int i = 0; i < 2; i++)
+      for (int i = 0; i < MI; i++)
 #pragma unroll
         for (int j = 0; j < NJ; j++)
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            const int64_t gm = m0 + wm * 16 + i * 8 + g8, gn = n0 + wn * M3_WN + j * 8 + 2 * t4 + h;
+            const int64_t gm = m0 + wm3 * LY::WMR + i * 8 + g8, gn = n0 + wn3 * M3_WN + j * 8 + 2 * t4 + h;
             const double2 c = (gm < p.M && gn < p.N) ? p.C[gm + gn * p.ldc] : czero();
             acc[0][i][j][h] = cs * c.x;
             acc[2][i][j][h] = cs * (c.x + c.y);
@@ -247,10 +254,10 @@ __global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) 
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ks++) {
           const int kk = ks * 4 + t4;
-          double ar[2], ai[2], as[2], br[NJ], bi[NJ], bs[NJ];
+          double ar[MI], ai[MI], as[MI], br[NJ], bi[NJ], bs[NJ];
 #pragma unroll
-          for (int i = 0; i < 2; i++) {
-            const int mm = wm * 16 + i * 8 + g8;
+          for (int i = 0; i < MI; i++) {
+            const int mm = wm3 * LY::WMR + i * 8 + g8;
             const double2 v = KM ? a2[mm * LDAK + kk] : a2[kk * LDA_S + mm];
             ar[i] = v.x;
             ai[i] = conjA ? -v.y : v.y;
@@ -258,7 +265,7 @@ __global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) 
           }
 #pragma unroll
           for (int j = 0; j < NJ; j++) {
-            const int nn = wn * M3_WN + j * 8 + g8;
+            const int nn = wn3 * M3_WN + j * 8 + g8;
             const double2 v = OPB == OP_C ? b2[kk * LDBN + nn] : b2[nn * LDB_S + kk];
             br[j] = v.x;
             bi[j] = OPB == OP_C ? -v.y : v.y;
@@ -266,15 +273,15 @@ __global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) 
           }
           // plane-major order: consecutive DMMAs share their A operand
 #pragma unroll
-          for (int i = 0; i < 2; i++)
+          for (int i = 0; i < MI; i++)
 #pragma unroll
             for (int j = 0; j < NJ; j++) dmma(acc[0][i][j], ar[i], br[j]);
 #pragma unroll
-          for (int i = 0; i < 2; i++)
+          for (int i = 0; i < MI; i++)
 #pragma unroll
             for (int j = 0; j < NJ; j++) dmma(acc[1][i][j], ai[i], bi[j]);
 #pragma unroll
-          for (int i = 0; i < 2; i++)
+          for (int i = 0; i < MI; i++)
 #pragma unroll
             for (int j = 0; j < NJ; j++) dmma(acc[2][i][j], as[i], bs[j]);
         }
@@ -289,12 +296,12 @@ __global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) 
     cp_async_wait<0>();
     // epilogue: lane holds complex (row g8, cols 2 t4 + h) of every tile
 #pragma unroll
-    for (int i = 0; i < 2; i++)
+    for (int i = 0; i < MI; i++)
 #pragma unroll
       for (int j = 0; j < NJ; j++)
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-          const int64_t gm = m0 + wm * 16 + i * 8 + g8, gn = n0 + wn * M3_WN + j * 8 + 2 * t4 + h;
+          const int64_t gm = m0 + wm3 * LY::WMR + i * 8 + g8, gn = n0 + wn3 * M3_WN + j * 8 + 2 * t4 + h;
           if (gm >= p.M || gn >= p.N) continue;
           const double p1 = acc[0][i][j][h], p2 = acc[1][i][j][h], p3 = acc[2][i][j][h];
           const double2 v = make_double2(cs * (p1 - p2), cs * (p3 - p1 - p2));
@@ -449,6 +456,10 @@ int launch_v(Ctx &ctx, const Params &p, dim3 grid) {
 }
 template <int OPA, int OPB, bool HERM, int LOWER>
 int launch_t(Ctx &ctx, const Params &p, dim3 grid, int v) {
+  if (v == 4) {
+    if constexpr (LOWER == 0 && !HERM) return launch_v<OPA, OPB, HERM, LOWER, 4>(ctx, p, grid);
+    return -2;
+  }
   if (v == 2) return launch_v<OPA, OPB, HERM, LOWER, 2>(ctx, p, grid);
   if (v == 1) return launch_v<OPA, OPB, HERM, LOWER, 1>(ctx, p, grid);
   return launch_v<OPA, OPB, HERM, LOWER, 0>(ctx, p, grid);
@@ -475,12 +486,19 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
     return e ? (int64_t)atoll(e) : (int64_t)kNarrowN;
   }();
   if (g.whole_n && g.N > Lay<0>::BN) return -2;
+  // variant 4 (128 x 64 tiles) for plain long-K products when EIG_ZGEMM_V4=1
+  static const int v4_env = [] {
+    const char *e = getenv("EIG_ZGEMM_V4");
+    return e ? atoi(e) : kZgemmV4;
+  }();
   // (with split_n set the choice must not depend on N: column slices stay bitwise)
   const bool narrow_n = g.split_n <= 0 && g.N <= narrow;
-  const int v = !m3 ? 0 : ((g.K <= shortk || narrow_n) && !g.whole_n ? 2 : 1);
+  int v = !m3 ? 0 : ((g.K <= shortk || narrow_n) && !g.whole_n ? 2 : 1);
+  if (v == 1 && v4_env && g.lower_c == 0 && !g.herm_a && !g.whole_n) v = 4;
+  const int BMv = v == 4 ? Lay<4>::BMV : BM;
   const int BN = v == 2 ? Lay<2>::BN : Lay<0>::BN;
   const int64_t q = BM / BN;
-  const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
+  const int tiles_m = (int)((g.M + BMv - 1) / BMv), tiles_n = (int)((g.N + BN - 1) / BN);
   const int64_t tiles = g.lower_c == 1 ? q * tiles_m * (tiles_m + 1) / 2 : (int64_t)tiles_m * tiles_n;
   // the split model sees N = split_n when set (N-independent split, see kernels.h)
   const int64_t Nm = g.split_n > 0 ? g.split_n : g.N;
@@ -492,14 +510,14 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   if (split <= 0) {
     // pick the split that minimises (waves of resident CTAs) x (k-tiles per CTA + fixed per-CTA cost),
     // plus the partial-sum traffic of the reduction (in k-tile units)
-    const int64_t cap = (v == 1 ? 1LL : 2LL) * ctx.num_sms;   // resident CTAs (variant 1: one 208-register CTA per SM)
+    const int64_t cap = (v == 1 || v == 4 ? 1LL : 2LL) * ctx.num_sms;   // resident CTAs (variant 1: one 208-register CTA per SM)
     const int64_t maxs = std::max<int64_t>(1, std::min<int64_t>(64, ktiles / 4));
     double best = 1e300;
     split = 1;
     for (int64_t sp = 1; sp <= maxs; sp++) {
       const int64_t kt = (ktiles + sp - 1) / sp;
       const int64_t waves = (tiles_model * sp + cap - 1) / cap;
-      const double red = sp > 1 ? 0.02 * (double)sp * (double)g.M * (double)Nm / (double)(cap * BM * BN) * 8.0 : 0.0;
+      const double red = sp > 1 ? 0.02 * (double)sp * (double)g.M * (double)Nm / (double)(cap * BMv * BN) * 8.0 : 0.0;
       const double t = (double)waves * (double)(kt + 3) + red;
       if (t < best * 0.98) {
         best = t;

@@ -51,6 +51,42 @@ def test_zgemm_ops(opa, opb, M, N, K, m3):
 
 
 @gpu
+@pytest.mark.parametrize("env", [("EIG_ZGEMM_V4", "0"), ("EIG_ZGEMM_SHORTK", "0"), ("EIG_ZGEMM_NARROW", "0")])
+def test_zgemm_engine_variants_subprocess(env):
+    """The 3M engine picks a tile variant per call (128x64 for plain long-K
+    products, 64x32 for K <= 256 or N <= 64, else 64x64); each switch forces
+    another variant onto the same shapes, checked against numpy in a child
+    process (the switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import synth
+from paper_1207_1773_b200 import Solver, colmajor, EIG_USE_3M
+s = Solver(0, flags=EIG_USE_3M)
+dev = torch.device("cuda:0")
+for opa, opb in [("N", "N"), ("C", "N"), ("N", "C")]:
+    for M, N, K in [(300, 200, 700), (257, 64, 129), (129, 333, 300), (64, 40, 1000)]:
+        A = synth.cnormal(1, 1, (M, K) if opa == "N" else (K, M))
+        B = synth.cnormal(1, 2, (K, N) if opb == "N" else (N, K))
+        C0 = synth.cnormal(1, 3, (M, N))
+        opA = A if opa == "N" else A.conj().T
+        opB = B if opb == "N" else B.conj().T
+        ref = -0.5 * opA @ opB + C0
+        dC = colmajor(C0, dev)
+        s.zgemm(opa, opb, colmajor(A, dev), colmajor(B, dev), dC, alpha=-0.5, beta=1.0, K=K)
+        err = np.max(np.abs(dC.cpu().numpy() - ref)) / np.max(np.abs(ref))
+        assert err < 1e-11, (opa, opb, M, N, K, err)
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **{env[0]: env[1]}), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@gpu
 @pytest.mark.parametrize("m3", [False, True])
 def test_zgemm_splitk_and_hermitian_and_lower(m3):
     s = _solver(m3=m3)
