@@ -251,27 +251,31 @@ def zhegv_timing(solver, A0, B0, stream):
     e1.record(stream)
     torch.cuda.synchronize()
     total = e0.elapsed_time(e1) * 1e-3
-    # stage breakdown (same work through the stage entry points)
-    A.copy_(A0)
-    B.copy_(B0)
-    torch.cuda.synchronize()
-    evs = [ev() for _ in range(7)]
-    evs[0].record(stream)
-    solver.potrf(B)
-    evs[1].record(stream)
-    solver.hegst(A, B)
-    evs[2].record(stream)
-    tau1, T1 = solver.he2hb(A)
-    evs[3].record(stream)
-    d, e, V2, tau2 = solver.hb2st(A)
-    evs[4].record(stream)
-    w2, Zr = solver.stedc(d, e)
-    evs[5].record(stream)
-    solver.apply_q2(V2, tau2, Z, Z=Zr)
-    solver.apply_q1(A, T1, Z)
-    solver.trsm_lh(B, Z)
-    evs[6].record(stream)
-    torch.cuda.synchronize()
+    # stage breakdown (same work through the stage entry points); the second of
+    # two passes is timed, so the stages' output tensors come from the
+    # allocator's cache instead of a cudaMalloc inside a stage
+    for rep in range(2):
+        A.copy_(A0)
+        B.copy_(B0)
+        torch.cuda.synchronize()
+        evs = [ev() for _ in range(7)]
+        evs[0].record(stream)
+        solver.potrf(B)
+        evs[1].record(stream)
+        solver.hegst(A, B)
+        evs[2].record(stream)
+        tau1, T1 = solver.he2hb(A)
+        evs[3].record(stream)
+        d, e, V2, tau2 = solver.hb2st(A)
+        evs[4].record(stream)
+        w2, Zr = solver.stedc(d, e)
+        evs[5].record(stream)
+        solver.apply_q2(V2, tau2, Z, Z=Zr)
+        solver.apply_q1(A, T1, Z)
+        solver.trsm_lh(B, Z)
+        evs[6].record(stream)
+        torch.cuda.synchronize()
+        del tau1, T1, d, e, V2, tau2, w2, Zr
     names = ["potrf", "hegst", "he2hb", "hb2st", "stedc", "backtransform"]
     stages = {nm: evs[i].elapsed_time(evs[i + 1]) for i, nm in enumerate(names)}
     return total, stages

@@ -8,9 +8,9 @@ import sys
 R = sys.argv[1] if len(sys.argv) > 1 else "r02"
 T = [
     # (name, kernel regex, skip count, command); zgemm_kernel<OPA, OPB, HERM, LOWER, variant>
-    ("zgemm_CN", "regex:zgemm_kernel<.int.1, .int.0, .bool.0, .int.0, .int.1>", 0,
+    ("zgemm_CN", "regex:zgemm_kernel<.int.1, .int.0, .bool.0, .int.0, .int.4>", 0,
      "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
-    ("zgemm_NN", "regex:zgemm_kernel<.int.0, .int.0, .bool.0, .int.0, .int.1>", 1,
+    ("zgemm_NN", "regex:zgemm_kernel<.int.0, .int.0, .bool.0, .int.0, .int.4>", 1,
      "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
     ("her2k", "regex:zgemm_kernel<.int.0, .int.1, .bool.0, .int.1, .int.2>", 1,
      "python tools/prof_kernels.py gemm --n 10000 --m 10000 --kw 256 --k 10000 --reps 1 --m3"),
