@@ -49,11 +49,14 @@ struct Lay {
   // variant 4 = 3M, 128 x 64 tiles, 32 x 32 warp tiles (8 DADDs per 48 DMMAs
   // instead of 6 per 24), BK 16, one CTA per SM; plain products only
   static constexpr int BMV = V == 4 ? 128 : 64;
-  static constexpr int WMR = V == 4 ? 32 : 16;   // 3M warp tile height (complex rows)
+  // variant 5 = variant 2's 64 x 32 tiles with 4 warps of 32 x 16 (6 DADDs per
+  // 24 DMMAs instead of 4 per 12), 128 threads, two CTAs per SM
+  static constexpr int WMR = (V == 4 || V == 5) ? 32 : 16;   // 3M warp tile height (complex rows)
   static constexpr int WARPS_M = BMV / WMR;
-  static constexpr int BN = V == 2 ? 32 : 64;
-  static constexpr int WN = V == 2 ? 16 : 32;   // 3M warp tile width (complex columns)
+  static constexpr int BN = (V == 2 || V == 5) ? 32 : 64;
+  static constexpr int WN = (V == 2 || V == 5) ? 16 : 32;   // 3M warp tile width (complex columns)
   static constexpr int MINB = (V == 1 || V == 4) ? 1 : 2;   // resident CTAs per SM
+  static constexpr int NT = V == 5 ? 128 : THREADS;         // threads per CTA
   // K tile (complex): variant 1 runs one CTA per SM, so it takes twice the K
   // per pipeline stage (half the CTA barriers per flop)
   static constexpr int BK = V == 1 ? 32 : 16;
@@ -84,8 +87,9 @@ struct Params {
 };
 
 template <int OPA, int OPB, bool HERM, int LOWER, int V>
-__global__ void __launch_bounds__(THREADS, Lay<V>::MINB) zgemm_kernel(Params p) {
+__global__ void __launch_bounds__(Lay<V>::NT, Lay<V>::MINB) zgemm_kernel(Params p) {
   using LY = Lay<V>;
+  constexpr int THREADS = LY::NT;   // (shadows the file-scope 256)
   constexpr int BM = LY::BMV;   // (shadows the file-scope 64)
   constexpr bool M3 = LY::M3;
   constexpr int BN = LY::BN, M3_WN = LY::WN;
@@ -451,7 +455,7 @@ template <int OPA, int OPB, bool HERM, int LOWER, int V>
 int launch_v(Ctx &ctx, const Params &p, dim3 grid) {
   constexpr size_t sm = Lay<V>::SMEM_BYTES;
   EIG_TRY(ctx.smem_attr((const void *)zgemm_kernel<OPA, OPB, HERM, LOWER, V>, (int)sm, "zgemm attr"));
-  zgemm_kernel<OPA, OPB, HERM, LOWER, V><<<grid, THREADS, sm, ctx.stream>>>(p);
+  zgemm_kernel<OPA, OPB, HERM, LOWER, V><<<grid, Lay<V>::NT, sm, ctx.stream>>>(p);
   return ctx.launched("zgemm_kernel");
 }
 template <int OPA, int OPB, bool HERM, int LOWER>
@@ -460,6 +464,7 @@ int launch_t(Ctx &ctx, const Params &p, dim3 grid, int v) {
     if constexpr (LOWER == 0 && !HERM) return launch_v<OPA, OPB, HERM, LOWER, 4>(ctx, p, grid);
     return -2;
   }
+  if (v == 5) return launch_v<OPA, OPB, HERM, LOWER, 5>(ctx, p, grid);
   if (v == 2) return launch_v<OPA, OPB, HERM, LOWER, 2>(ctx, p, grid);
   if (v == 1) return launch_v<OPA, OPB, HERM, LOWER, 1>(ctx, p, grid);
   return launch_v<OPA, OPB, HERM, LOWER, 0>(ctx, p, grid);
@@ -495,8 +500,13 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   const bool narrow_n = g.split_n <= 0 && g.N <= narrow;
   int v = !m3 ? 0 : ((g.K <= shortk || narrow_n) && !g.whole_n ? 2 : 1);
   if (v == 1 && v4_env && g.lower_c == 0 && !g.herm_a && !g.whole_n) v = 4;
+  static const int v5_env = [] {
+    const char *e = getenv("EIG_ZGEMM_V5");
+    return e ? atoi(e) : 0;
+  }();
+  if (v == 2 && v5_env) v = 5;
   const int BMv = v == 4 ? Lay<4>::BMV : BM;
-  const int BN = v == 2 ? Lay<2>::BN : Lay<0>::BN;
+  const int BN = (v == 2 || v == 5) ? Lay<2>::BN : Lay<0>::BN;
   const int64_t q = BM / BN;
   const int tiles_m = (int)((g.M + BMv - 1) / BMv), tiles_n = (int)((g.N + BN - 1) / BN);
   const int64_t tiles = g.lower_c == 1 ? q * tiles_m * (tiles_m + 1) / 2 : (int64_t)tiles_m * tiles_n;
