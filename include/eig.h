@@ -59,7 +59,10 @@ extern "C" {
 #define EIG_GATHER_Z     1u  /* collective eig_solve_gen: rank 0's Z receives all m columns      */
 #define EIG_USE_3M       2u  /* complex GEMMs (he2hb updates, Q1, triangular solves, hegst) as
                                 three real DMMA products (3M, Gauss) instead of four: 0.75 of
-                                the tensor-pipe work; nominal flops stay 8 per complex MAC   */
+                                the tensor-pipe work; nominal flops stay 8 per complex MAC.
+                                (The nb = 64, g = 32 Q2 wavefront is 3M by default
+                                independently of these flags; environment EIG_Q2_3M=0
+                                selects its four-product form.)                          */
 #define EIG_NO_3M        4u  /* force the four-product form (overrides EIG_USE_3M / EIG_3M)   */
 #define EIG_DIST_HE2HB   8u  /* collective eig_solve_gen: he2hb distributed over all ranks (1D
                                 block-cyclic columns, NEXT-4) instead of on rank 0; every rank
@@ -83,7 +86,8 @@ typedef struct {
                         (0 for nb <= 2: no Q2).  Explicit values must satisfy
                         4 <= g <= 32, g % 4 == 0, g <= nb + 1 (else eig_init
                         returns -2).  nb = 64 with g = 32 selects the wavefront
-                        kernel; other shapes the generic grouped kernel          */
+                        kernel (3M form, blocks released by per-block completion
+                        counters); other shapes the generic grouped kernel       */
   void *stream;      /* cudaStream_t to order with; NULL = legacy default stream    */
   int rank, nranks;  /* this process's rank and the number of ranks (GPUs); nranks
                         <= 1 with nccl_id == NULL: single GPU (non-collective)     */
@@ -203,7 +207,12 @@ int eig_apply_q2(eig_handle h, int64_t n, const void *V2, const void *tau2, cons
  * sub-diagonal (e_i = beta of sweep i, LAPACK zlarfg convention, so T is
  * real without a phase diagonal).  V2 [slots*nb], tau2 [slots]: the chase
  * reflectors in the V2 layout below, so that Band = Q2 T Q2^H.  Uses nb of
- * the handle; library workspace holds a (2nb+2) x n band copy. */
+ * the handle; library workspace holds a (2nb+2) x n band copy.  The chase
+ * runs position-stationary (each nb-row position's diagonal and bulge blocks
+ * resident in one CTA's shared memory for all sweeps) while ceil(J/2) CTAs,
+ * J = (n-2)/nb + 1, fit on the device at once (n <= ~18900 at nb = 64 on a
+ * 148-SM B200), else sweep per CTA; same reflectors and outputs either way
+ * (up to rounding); environment EIG_HB2ST_SYS=0 forces the latter. */
 int eig_hb2st(eig_handle h, int64_t n, const void *A, int64_t lda, double *d, double *e, void *V2, void *tau2);
 
 /* ------------------------------------------------------------------ NEXT-2
