@@ -500,6 +500,9 @@ int zgemm(Ctx &ctx, const Zgemm &g) {
   const bool narrow_n = g.split_n <= 0 && g.N <= narrow;
   int v = !m3 ? 0 : ((g.K <= shortk || narrow_n) && !g.whole_n ? 2 : 1);
   if (v == 1 && v4_env && g.lower_c == 0 && !g.herm_a && !g.whole_n) v = 4;
+  // tall plain products with 128 < K <= 256 (Q1's E -= (V T) Y): the 128 x 64
+  // tiles beat the two-CTA 64 x 32 ones once M fills the machine
+  if (v == 2 && v4_env && g.K > 128 && g.M >= 2048 && g.lower_c == 0 && !g.herm_a && !g.whole_n) v = 4;
   static const int v5_env = [] {
     const char *e = getenv("EIG_ZGEMM_V5");
     return e ? atoi(e) : 0;
